@@ -1,0 +1,142 @@
+/*
+ * fastgauss_b200.h -- C ABI of the B200-native Gaussian-summation engine.
+ *
+ * Drop-in boundary for the reference package `fastgauss`
+ * (/root/reference/pkg/src/fastgauss/, cited below as `file.py:line`).
+ * The reference has no FFI of its own (it is pure Python/NumPy); each entry
+ * point here replaces the Python function named in its comment, and the
+ * Python shim `paper_1206_6857_b200` binds them with ctypes (INTEGRATION.md
+ * shows the binding).  Plain pointers and sizes only; no torch types.
+ *
+ * Pointers marked "host or device" are classified with
+ * cudaPointerGetAttributes: device/managed memory is used in place, host
+ * memory is staged through the engine's device buffers.  All work is issued
+ * on the stream set by fg_set_stream (default: the legacy default stream)
+ * and every call returns when its results are available to the caller.
+ *
+ * Status codes (every function returns one):
+ *   FG_OK 0, FG_EINVAL 1 (-> ValueError), FG_ESTALE 2 (stale moments ->
+ *   RuntimeError, summation_engine.py:433-441), FG_ECUDA 3 (CUDA/NCCL error),
+ *   FG_EUNSUPPORTED 4 (a size this build does not support -> ValueError).
+ * fg_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef FASTGAUSS_B200_H
+#define FASTGAUSS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_OK 0
+#define FG_EINVAL 1
+#define FG_ESTALE 2
+#define FG_ECUDA 3
+#define FG_EUNSUPPORTED 4
+
+/* algorithms: summation_engine.py:458-480 */
+#define FG_DFD 1
+#define FG_DFDO 2
+#define FG_DITO 3
+
+/* TraversalCounters (summation_engine.py:81-104) plus exact pair count */
+typedef struct {
+    int64_t pair_visits;
+    int64_t base_cases;
+    int64_t fd_prunes;
+    int64_t hermite_prunes;
+    int64_t local_prunes;
+    int64_t h2l_prunes;
+    int64_t exact_pairs; /* query x reference pairs evaluated exactly */
+} fg_counters;
+
+typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_index.py:144) */
+
+int fg_version(void);
+const char *fg_last_error(void);
+/* stream: a cudaStream_t (NULL = legacy default stream) */
+int fg_set_stream(void *stream);
+int fg_set_device(int device);
+int fg_synchronize(void);
+
+/* ---- exhaustive sums: naive_sum (summation_engine.py:122-154) ---------
+ * queries (m x dim) and references (n x dim) row-major, weights (n,), all
+ * host or device; out (m,) host or device.  nh bandwidths -> out is
+ * (nh x m).  exact_pairs (nullable) receives m*n*nh. */
+int fg_naive_sum(const double *queries, int64_t m, const double *references,
+                 const double *weights, int64_t n, int32_t dim, const double *bandwidths,
+                 int32_t nh, double *out);
+
+/* ---- trees: PointStore (spatial_index.py:47-80) + build_tree (:231-276) --
+ * points (n x dim) host or device; weights NULL -> all ones; rejects n < 1,
+ * dim < 1, non-positive weights, leaf_threshold < 1 (FG_EINVAL).  The
+ * device build reproduces the reference permutation and node ranges. */
+int fg_tree_build(const double *points, const double *weights, int64_t n, int32_t dim,
+                  int32_t leaf_threshold, fg_tree **out);
+int fg_tree_free(fg_tree *tree);
+/* n, dim, number of nodes, sum of weights, number of levels */
+int fg_tree_info(const fg_tree *tree, int64_t *n, int32_t *dim, int64_t *nnodes,
+                 double *total_weight, int32_t *levels);
+/* Node arrays in the reference's PREORDER numbering (Node.index), host
+ * pointers, each nullable: perm (n), start/end/left/right (nnodes, -1 for
+ * no child), lo/hi/center (nnodes x dim), weight/inf_radius (nnodes). */
+int fg_tree_export(const fg_tree *tree, int64_t *perm, int64_t *start, int64_t *end,
+                   double *lo, double *hi, double *center, double *weight,
+                   double *inf_radius, int64_t *left, int64_t *right);
+/* points (n x dim) and weights (n) in tree order, host or device */
+int fg_tree_points(const fg_tree *tree, double *points, double *weights);
+
+/* ---- moments: KdTree.refresh_moments (spatial_index.py:171-197) -------- */
+int fg_moments_refresh(fg_tree *tree, double h, int32_t plimit);
+/* (nnodes x K) in preorder numbering; K = C(dim+plimit-1, dim) */
+int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h,
+                      int32_t *order);
+
+/* ---- runs: dfd_run / dfdo_run / dito_run (summation_engine.py:431-480) --
+ * qtree may equal rtree (monochromatic).  values (m,) host or device, in
+ * ORIGINAL query order.  plimit <= 0 -> default_plimit(dim).  Requires
+ * fresh moments for FG_DITO (else FG_ESTALE).  seconds = device time of the
+ * run (reset + traverse + post, like summation_engine.py:447-452). */
+int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+           int32_t plimit, double *values, fg_counters *counters, double *seconds);
+/* Query-sharded run: only query blocks [block_begin,
+ * block_end) of qtree are processed; values is written only at those
+ * blocks' queries (original order).  fg_query_blocks reports the block count. */
+int fg_query_blocks(fg_tree *qtree, int64_t *nblocks);
+int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+                 int32_t plimit, int64_t block_begin, int64_t block_end, double *values,
+                 fg_counters *counters, double *seconds);
+/* engine knobs (0 keeps the current value): reference-side leaf size used by
+ * the traversal, per-warp stack capacity.  Not part of the reference API. */
+int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap);
+
+/* ---- series algebra (series_expansion.py), batched over `batch` items ---
+ * All arrays host or device, row-major per item.  Used by the Python mirror
+ * of the reference's series functions and by the parity tests. */
+/* accumulate_far_field (:76-92) / accumulate_local_direct (:110-126):
+ * item b owns points [offsets[b], offsets[b+1]) of pts (npts x dim) and w. */
+int fg_series_accumulate(int32_t kind /*0 far, 1 local*/, const double *pts, const double *w,
+                         const int64_t *offsets, int32_t batch, int32_t dim,
+                         const double *centers, int32_t order, double h, double *coeffs);
+/* eval_far_field (:95-107) / eval_local (:129-136): evaluates item b's
+ * expansion (coeffs b x K_stored, prefix `order`) at its points */
+int fg_series_eval(int32_t kind /*0 far, 1 local*/, const double *coeffs, int32_t k_stored,
+                   const double *centers, int32_t batch, int32_t dim, int32_t order,
+                   double h, const double *x, const int64_t *offsets, double *out);
+/* translate_h2h (:139-157) kind 0, translate_l2l (:197-217) kind 1,
+ * translate_h2l (:167-194) kind 2 (src_order = order_src, dest = order) */
+int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
+                        const double *src_centers, const double *dst_centers, int32_t batch,
+                        int32_t dim, int32_t order_src, int32_t order, double h,
+                        double *out);
+/* best_method (error_bounds.py:168-230) on `batch` geometries:
+ * geom rows = (min_sq, max_sq, r_ref, r_query, w_ref, n_query, n_ref, h, maxerr);
+ * out rows = (method 0/2/3/4, order, bound, cost) as doubles. */
+int fg_best_method(const double *geom, int32_t batch, int32_t dim, int32_t plimit,
+                   double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,414 @@
+// fg_api.cu -- the extern "C" boundary (include/fastgauss_b200.h), error
+// state, host/device pointer staging and the multi-index tables.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fg_internal.cuh"
+
+namespace fg {
+
+static thread_local std::string t_last_error;
+static cudaStream_t g_stream = nullptr;
+
+void set_error(const std::string &msg) { t_last_error = msg; }
+cudaStream_t stream() { return g_stream; }
+
+bool is_device_ptr(const void *ptr) {
+    if (!ptr) return false;
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+int to_device(const void *src, size_t bytes, DBuf &stage, const void **dptr) {
+    if (!src) {
+        *dptr = nullptr;
+        return FG_OK;
+    }
+    if (is_device_ptr(src)) {
+        *dptr = src;
+        return FG_OK;
+    }
+    FG_TRY(stage.reserve(bytes));
+    FG_CUDA_TRY(cudaMemcpyAsync(stage.p, src, bytes, cudaMemcpyHostToDevice, stream()));
+    *dptr = stage.p;
+    return FG_OK;
+}
+
+int from_device(void *dst, const void *dsrc, size_t bytes) {
+    if (bytes == 0) return FG_OK;
+    if (is_device_ptr(dst)) {
+        FG_CUDA_TRY(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToDevice, stream()));
+    } else {
+        FG_CUDA_TRY(cudaMemcpyAsync(dst, dsrc, bytes, cudaMemcpyDeviceToHost, stream()));
+    }
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+// ------------------------------------------------------------- tables
+static int64_t binom_i(int n, int k) {
+    if (k < 0 || k > n) return 0;
+    int64_t r = 1;
+    for (int i = 1; i <= k; i++) r = r * (n - k + i) / i;
+    return r;
+}
+
+int iset_count(int dim, int order) { return (int)binom_i(dim + order - 1, dim); }
+
+int default_plimit(int dim) {
+    static const int sched[7] = {1, 8, 8, 6, 4, 4, 2};
+    return dim <= 6 ? sched[dim] : 1;
+}
+
+static double fact_d(int n) {
+    double f = 1.0;
+    for (int i = 2; i <= n; i++) f *= (double)i;
+    return f;
+}
+
+void tail_tables(int dim, int plimit, double *ct, double *cross, double *floor_c) {
+    double fl = INFINITY;
+    ct[0] = 0.0;
+    cross[0] = 0.0;
+    for (int p = 1; p <= plimit; p++) {
+        const double count = (double)binom_i(dim + p - 1, dim - 1);
+        const int q = p / dim, r = p % dim;
+        long double prod = 1.0L;
+        for (int i = 0; i < dim - r; i++) prod *= (long double)fact_d(q);
+        for (int i = 0; i < r; i++) prod *= (long double)fact_d(q + 1);
+        const double denom = std::sqrt((double)prod);
+        ct[p] = count / denom;
+        cross[p] = (double)binom_i(dim + p - 1, dim);
+        if (ct[p] < fl) fl = ct[p];
+    }
+    *floor_c = fl;
+}
+
+// _compositions (kernel_math.py:111-119): leading digit descending
+static void compositions(int total, int dims, std::vector<int> &prefix,
+                         std::vector<std::vector<int>> &out) {
+    if (dims == 1) {
+        prefix.push_back(total);
+        out.push_back(prefix);
+        prefix.pop_back();
+        return;
+    }
+    for (int head = total; head >= 0; head--) {
+        prefix.push_back(head);
+        compositions(total - head, dims - 1, prefix, out);
+        prefix.pop_back();
+    }
+}
+
+static std::mutex g_tab_mu;
+static std::map<std::pair<int, int>, std::unique_ptr<SeriesTables>> g_tables;
+
+const SeriesTables *series_tables(int dim, int order, int *status) {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    auto key = std::make_pair(dim, order);
+    auto it = g_tables.find(key);
+    if (it != g_tables.end()) {
+        *status = FG_OK;
+        return it->second.get();
+    }
+    if (dim < 1 || dim > kMaxDim || order < 1 || order > kMaxOrder ||
+        iset_count(dim, order) > kMaxK) {
+        set_error("series tables: (dim, order) outside the device limits (dim<=8, order<=8, "
+                  "C(dim+order-1, dim)<=256)");
+        *status = FG_EUNSUPPORTED;
+        return nullptr;
+    }
+    auto T = std::make_unique<SeriesTables>();
+    T->dim = dim;
+    T->order = order;
+    std::vector<std::vector<int>> idx;
+    std::vector<int> prefix;
+    for (int deg = 0; deg < order; deg++) compositions(deg, dim, prefix, idx);
+    const int K = (int)idx.size();
+    T->K = K;
+    T->h_digits.assign((size_t)K * kMaxDim, 0);
+    T->h_degrees.resize(K);
+    T->h_fact.resize(K);
+    std::vector<double> inv(K);
+    for (int k = 0; k < K; k++) {
+        int deg = 0;
+        double f = 1.0;
+        for (int d = 0; d < dim; d++) {
+            T->h_digits[(size_t)k * kMaxDim + d] = (uint8_t)idx[k][d];
+            deg += idx[k][d];
+            f *= fact_d(idx[k][d]);
+        }
+        T->h_degrees[k] = deg;
+        T->h_fact[k] = f;
+        inv[k] = 1.0 / f;
+    }
+    T->h_prefix.resize(order + 1);
+    for (int p = 0; p <= order; p++) {
+        int c = 0;
+        while (c < K && T->h_degrees[c] < p) c++;
+        T->h_prefix[p] = c;
+    }
+    std::map<std::vector<int>, int> pos;
+    for (int k = 0; k < K; k++) pos[idx[k]] = k;
+    for (int a = 0; a < K; a++)
+        for (int b = 0; b < K; b++) {
+            if (T->h_degrees[a] + T->h_degrees[b] >= order) continue;
+            std::vector<int> s(dim);
+            for (int d = 0; d < dim; d++) s[d] = idx[a][d] + idx[b][d];
+            T->h_pair_a.push_back(a);
+            T->h_pair_b.push_back(b);
+            T->h_pair_s.push_back(pos[s]);
+        }
+    const int np = (int)T->h_pair_a.size();
+    T->npairs = np;
+    // CSR by s (stable in pair order) and by a
+    std::vector<int> off_s(K + 1, 0), off_a(K + 1, 0);
+    for (int i = 0; i < np; i++) {
+        off_s[T->h_pair_s[i] + 1]++;
+        off_a[T->h_pair_a[i] + 1]++;
+    }
+    for (int k = 0; k < K; k++) {
+        off_s[k + 1] += off_s[k];
+        off_a[k + 1] += off_a[k];
+    }
+    std::vector<int2> ab(np), bs(np);
+    std::vector<int> fill_s(off_s.begin(), off_s.end() - 1), fill_a(off_a.begin(), off_a.end() - 1);
+    for (int i = 0; i < np; i++) {
+        ab[fill_s[T->h_pair_s[i]]++] = make_int2(T->h_pair_a[i], T->h_pair_b[i]);
+        bs[fill_a[T->h_pair_a[i]]++] = make_int2(T->h_pair_b[i], T->h_pair_s[i]);
+    }
+    auto up = [&](DBuf &dst, const void *src, size_t bytes) -> int {
+        FG_TRY(dst.reserve(bytes));
+        FG_CUDA_TRY(cudaMemcpy(dst.p, src, bytes, cudaMemcpyHostToDevice));
+        return FG_OK;
+    };
+    int st = FG_OK;
+    if (!st) st = up(T->digits, T->h_digits.data(), T->h_digits.size());
+    if (!st) st = up(T->inv_fact, inv.data(), sizeof(double) * K);
+    if (!st) st = up(T->fact, T->h_fact.data(), sizeof(double) * K);
+    if (!st) st = up(T->degrees, T->h_degrees.data(), sizeof(int) * K);
+    if (!st) st = up(T->h2h_off, off_s.data(), sizeof(int) * (K + 1));
+    if (!st) st = up(T->h2h_ab, ab.data(), sizeof(int2) * std::max(np, 1));
+    if (!st) st = up(T->l2l_off, off_a.data(), sizeof(int) * (K + 1));
+    if (!st) st = up(T->l2l_bs, bs.data(), sizeof(int2) * std::max(np, 1));
+    *status = st;
+    if (st) return nullptr;
+    const SeriesTables *raw = T.get();
+    g_tables[key] = std::move(T);
+    return raw;
+}
+
+}  // namespace fg
+
+using namespace fg;
+
+// ------------------------------------------------------------ C ABI
+extern "C" {
+
+int fg_version(void) { return 1; }
+
+const char *fg_last_error(void) { return t_last_error.c_str(); }
+
+int fg_set_stream(void *s) {
+    g_stream = reinterpret_cast<cudaStream_t>(s);
+    return FG_OK;
+}
+
+int fg_set_device(int device) {
+    FG_CUDA_TRY(cudaSetDevice(device));
+    return FG_OK;
+}
+
+int fg_synchronize(void) {
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap) {
+    if (ref_leaf > 0) g_ref_leaf = ref_leaf;
+    if (stack_cap > 0) {
+        FG_REQUIRE(stack_cap >= 64, FG_EINVAL, "stack capacity must be >= 64");
+        g_stack_cap = stack_cap;
+    }
+    return FG_OK;
+}
+
+static DBuf g_stage_q, g_stage_r, g_stage_w, g_stage_out;
+
+int fg_naive_sum(const double *queries, int64_t m, const double *references,
+                 const double *weights, int64_t n, int32_t dim, const double *bandwidths,
+                 int32_t nh, double *out) {
+    FG_REQUIRE(queries && references && weights && bandwidths && out, FG_EINVAL,
+               "null pointer");
+    FG_REQUIRE(m >= 1 && n >= 1 && dim >= 1 && nh >= 1, FG_EINVAL, "empty input");
+    for (int k = 0; k < nh; k++)
+        FG_REQUIRE(bandwidths[k] > 0.0, FG_EINVAL, "bandwidth must be positive");
+    const void *dq, *dr, *dw;
+    FG_TRY(to_device(queries, sizeof(double) * m * dim, g_stage_q, &dq));
+    FG_TRY(to_device(references, sizeof(double) * n * dim, g_stage_r, &dr));
+    FG_TRY(to_device(weights, sizeof(double) * n, g_stage_w, &dw));
+    const bool out_dev = is_device_ptr(out);
+    double *dout = out;
+    if (!out_dev) {
+        FG_TRY(g_stage_out.reserve(sizeof(double) * m * nh));
+        dout = g_stage_out.as<double>();
+    }
+    FG_TRY(fg::naive_sum((const double *)dq, m, (const double *)dr, (const double *)dw, n, dim,
+                         bandwidths, nh, dout));
+    if (!out_dev) {
+        FG_CUDA_TRY(cudaMemcpyAsync(out, dout, sizeof(double) * m * nh, cudaMemcpyDeviceToHost,
+                                    stream()));
+    }
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+int fg_tree_build(const double *points, const double *weights, int64_t n, int32_t dim,
+                  int32_t leaf_threshold, fg_tree **out) {
+    FG_REQUIRE(out, FG_EINVAL, "null output handle");
+    *out = nullptr;
+    FG_REQUIRE(points || n == 0, FG_EINVAL, "null points");
+    FG_REQUIRE(n >= 1 && dim >= 1, FG_EINVAL, "points must be a non-empty (N, D) array");
+    FG_REQUIRE(leaf_threshold >= 1, FG_EINVAL, "leaf threshold must be at least 1");
+    DBuf sp, sw;
+    const void *dp, *dw = nullptr;
+    FG_TRY(to_device(points, sizeof(double) * n * dim, sp, &dp));
+    if (weights) FG_TRY(to_device(weights, sizeof(double) * n, sw, &dw));
+    auto *t = new fg_tree();
+    int st = tree_build((const double *)dp, (const double *)dw, n, dim, leaf_threshold, t->t);
+    if (st != FG_OK) {
+        delete t;
+        return st;
+    }
+    *out = t;
+    return FG_OK;
+}
+
+int fg_tree_free(fg_tree *tree) {
+    if (tree) {
+        cudaStreamSynchronize(stream());
+        delete tree;
+    }
+    return FG_OK;
+}
+
+int fg_tree_info(const fg_tree *tree, int64_t *n, int32_t *dim, int64_t *nnodes,
+                 double *total_weight, int32_t *levels) {
+    FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    if (n) *n = tree->t.n;
+    if (dim) *dim = tree->t.dim;
+    if (nnodes) *nnodes = tree->t.nnodes;
+    if (total_weight) *total_weight = tree->t.total_w;
+    if (levels) *levels = tree->t.levels;
+    return FG_OK;
+}
+
+int fg_tree_export(const fg_tree *tree, int64_t *perm, int64_t *start, int64_t *end,
+                   double *lo, double *hi, double *center, double *weight, double *inf_radius,
+                   int64_t *left, int64_t *right) {
+    FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    return tree_export(tree->t, perm, start, end, lo, hi, center, weight, inf_radius, left,
+                       right);
+}
+
+__global__ void unpack_points_kernel(int64_t n, int dim, int stride, const double *pw,
+                                     double *pts, double *w) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (pts)
+        for (int d = 0; d < dim; d++) pts[i * dim + d] = pw[i * stride + d];
+    if (w) w[i] = pw[i * stride + dim];
+}
+
+int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
+    FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    const TreeDev &t = tree->t;
+    DBuf tp, tw;
+    if (points) FG_TRY(tp.reserve(sizeof(double) * t.n * t.dim));
+    if (weights) FG_TRY(tw.reserve(sizeof(double) * t.n));
+    unpack_points_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, stream()>>>(
+        t.n, t.dim, t.stride, t.pw.as<double>(), points ? tp.as<double>() : nullptr,
+        weights ? tw.as<double>() : nullptr);
+    FG_CUDA_TRY(cudaGetLastError());
+    if (points) FG_TRY(from_device(points, tp.p, sizeof(double) * t.n * t.dim));
+    if (weights) FG_TRY(from_device(weights, tw.p, sizeof(double) * t.n));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+int fg_moments_refresh(fg_tree *tree, double h, int32_t plimit) {
+    FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    FG_TRY(moments_refresh(tree->t, h, plimit));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h, int32_t *order) {
+    FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    const TreeDev &t = tree->t;
+    if (K) *K = t.mom_valid ? t.mom_K : 0;
+    if (h) *h = t.mom_valid ? t.mom_h : 0.0;
+    if (order) *order = t.mom_valid ? t.mom_order : 0;
+    if (!out) return FG_OK;
+    return moments_export(t, out);
+}
+
+static int run_impl(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+                    int32_t plimit, int64_t b0, int64_t b1, double *values, fg_counters *counters,
+                    double *seconds) {
+    FG_REQUIRE(qtree && rtree && values, FG_EINVAL, "null argument");
+    const int64_t m = qtree->t.n;
+    const bool out_dev = is_device_ptr(values);
+    double *dout = values;
+    if (!out_dev) {
+        FG_TRY(g_stage_out.reserve(sizeof(double) * m));
+        dout = g_stage_out.as<double>();
+        if (b0 > 0 || (b1 >= 0 && b1 < (qtree->t.n + 31) / 32)) {
+            // partial range: keep the caller's other entries
+            FG_CUDA_TRY(cudaMemcpyAsync(dout, values, sizeof(double) * m,
+                                        cudaMemcpyHostToDevice, stream()));
+        }
+    }
+    FG_TRY(run_traversal(qtree->t, rtree->t, h, eps, mode, plimit, b0, b1, dout, counters,
+                         seconds));
+    if (!out_dev) {
+        FG_CUDA_TRY(cudaMemcpyAsync(values, dout, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                                    stream()));
+    }
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    return FG_OK;
+}
+
+int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode, int32_t plimit,
+           double *values, fg_counters *counters, double *seconds) {
+    return run_impl(qtree, rtree, h, eps, mode, plimit, 0, -1, values, counters, seconds);
+}
+
+int fg_query_blocks(fg_tree *qtree, int64_t *nblocks) {
+    FG_REQUIRE(qtree && nblocks, FG_EINVAL, "null argument");
+    FG_TRY(query_blocks(qtree->t));
+    *nblocks = qtree->t.nqb;
+    return FG_OK;
+}
+
+int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+                 int32_t plimit, int64_t block_begin, int64_t block_end, double *values,
+                 fg_counters *counters, double *seconds) {
+    FG_REQUIRE(block_begin >= 0 && block_end >= block_begin, FG_EINVAL, "bad block range");
+    return run_impl(qtree, rtree, h, eps, mode, plimit, block_begin, block_end, values,
+                    counters, seconds);
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+// fg_internal.cuh -- shared host/device definitions of the B200 engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fastgauss_b200.h"
+
+namespace fg {
+
+constexpr int kMaxDim = 8;      // template-specialised dimensions 1..8
+constexpr int kMaxOrder = 8;    // series order cap on the device (plimit <= 8)
+constexpr int kMaxK = 256;      // coefficient-count cap per expansion
+constexpr double kSqrt2 = 1.4142135623730951;
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+struct Status {
+    int code;
+};
+
+#define FG_CUDA_TRY(expr)                                                        \
+    do {                                                                         \
+        cudaError_t _e = (expr);                                                 \
+        if (_e != cudaSuccess) {                                                 \
+            ::fg::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+            return FG_ECUDA;                                                     \
+        }                                                                        \
+    } while (0)
+
+#define FG_TRY(expr)                  \
+    do {                              \
+        int _s = (expr);              \
+        if (_s != FG_OK) return _s;   \
+    } while (0)
+
+#define FG_REQUIRE(cond, code, msg)   \
+    do {                              \
+        if (!(cond)) {                \
+            ::fg::set_error(msg);     \
+            return code;              \
+        }                             \
+    } while (0)
+
+cudaStream_t stream();
+
+// ------------------------------------------------------- device buffers
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    DBuf() = default;
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    // grow-only (re)allocation; contents are not preserved
+    int reserve(size_t nbytes) {
+        if (nbytes <= bytes) return FG_OK;
+        release();
+        size_t nb = nbytes < 256 ? 256 : nbytes;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e != cudaSuccess) {
+            set_error(std::string("cudaMalloc(") + std::to_string(nb) + "): " +
+                      cudaGetErrorString(e));
+            p = nullptr;
+            return FG_ECUDA;
+        }
+        bytes = nb;
+        return FG_OK;
+    }
+    template <class T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// true when ptr is device (or managed) memory usable by kernels
+bool is_device_ptr(const void *ptr);
+
+// Make `src` (count elements) available on the device: returns src itself
+// when it is device memory, otherwise copies into `stage`.
+int to_device(const void *src, size_t bytes, DBuf &stage, const void **dptr);
+// Copy device data to a destination that may be host or device.
+int from_device(void *dst, const void *dsrc, size_t bytes);
+
+// ------------------------------------------------------- series tables
+// Graded-lex multi-index tables for (dim, order) (kernel_math.py:111-209),
+// resident on the device.  Cached per (dim, order).
+struct SeriesTables {
+    int dim = 0, order = 0, K = 0, npairs = 0;
+    std::vector<uint8_t> h_digits;     // K x dim
+    std::vector<int> h_degrees;        // K
+    std::vector<double> h_fact;        // K
+    std::vector<int> h_prefix;         // order + 1
+    std::vector<int> h_pair_a, h_pair_b, h_pair_s;
+    // device copies
+    DBuf digits;     // uint8 K x kMaxDim (padded)
+    DBuf inv_fact;   // double K
+    DBuf fact;       // double K
+    DBuf degrees;    // int K
+    DBuf h2h_off;    // int K+1: CSR of shift pairs by s
+    DBuf h2h_ab;     // int2 npairs: (a, b) sorted by s
+    DBuf l2l_off;    // int K+1: CSR of shift pairs by a
+    DBuf l2l_bs;     // int2 npairs: (b, s) sorted by a
+};
+const SeriesTables *series_tables(int dim, int order, int *status);
+
+// tail tables (error_bounds.py:73-92): ct[p] = count/denom, cross[p]
+void tail_tables(int dim, int plimit, double *ct, double *cross, double *floor_c);
+int default_plimit(int dim);  // spatial_index.py:39-44
+int iset_count(int dim, int order);
+
+// -------------------------------------------------------------- the tree
+// Node numbering on the device is BFS (level by level); `pre_of_bfs` maps
+// to the reference's preorder numbering for export.
+struct TreeDev {
+    int64_t n = 0;
+    int dim = 0, leaf = 25, stride = 0;  // stride: doubles per packed point
+    int64_t nnodes = 0;
+    int levels = 0;
+    double total_w = 0.0;
+    std::vector<int64_t> level_begin;  // BFS node id range per level
+    DBuf pw;       // n x stride: coords then weight (tree order), padded
+    DBuf perm;     // int64 n: tree position -> original index
+    DBuf node_i;   // int4 nnodes: start, count, left, right (BFS ids, -1 = leaf)
+    DBuf node_box; // double nnodes x 2*dim: lo[dim], hi[dim]
+    DBuf node_c;   // double nnodes x dim: centroid
+    DBuf node_wr;  // double2 nnodes: weight, inf_radius
+    // moments (bandwidth-dependent), K per node, BFS numbering
+    DBuf mom, mom0;
+    int mom_order = 0, mom_K = 0;
+    double mom_h = 0.0, mom0_h = 0.0;
+    bool mom_valid = false, mom0_valid = false;
+    // query blocks (bandwidth-independent): ranges of <= 32 tree-order points
+    bool qb_valid = false;
+    int64_t nqb = 0;
+    DBuf qb_range;  // int2 (start, count)
+    DBuf qb_box;    // double nqb x 2*dim
+    DBuf qb_c;      // double nqb x dim
+    DBuf qb_rad;    // double nqb
+};
+
+}  // namespace fg
+
+struct fg_tree {
+    fg::TreeDev t;
+};
+
+namespace fg {
+// implemented in fg_tree.cu / fg_moments.cu / fg_traverse.cu / fg_naive.cu
+int tree_build(const double *d_points, const double *d_weights, int64_t n, int dim, int leaf,
+               TreeDev &t);
+int tree_export(const TreeDev &t, int64_t *perm, int64_t *start, int64_t *end, double *lo,
+                double *hi, double *center, double *weight, double *inf_radius,
+                int64_t *left, int64_t *right);
+int moments_refresh(TreeDev &t, double h, int plimit);
+int moments_export(const TreeDev &t, double *out);
+int query_blocks(TreeDev &t);
+int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
+                  int64_t b0, int64_t b1, double *d_values, fg_counters *counters,
+                  double *seconds);
+int preorder_map(const TreeDev &t, std::vector<int64_t> &pre);
+int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
+              int dim, const double *hs, int nh, double *d_out);
+extern int g_ref_leaf;
+extern int g_stack_cap;
+}  // namespace fg

@@ -1,0 +1,183 @@
+// fg_moments.cu -- K5: far-field moments per reference node
+// (replaces KdTree.refresh_moments, spatial_index.py:171-197).
+//
+// Direct accumulation at the leaves (accumulate_far_field,
+// series_expansion.py:76-92) and exact H2H shifts bottom-up level by level
+// (translate_h2h + add_far_field, :139-164), one warp per node with lanes
+// owning coefficients.  The first refresh for a given order is kept as a base
+// (h0); later refreshes at other bandwidths apply the exact rescaling law
+// A_a(h) = (h0/h)^{|a|} A_a(h0), pinned by the reference's
+// tests/test_spatial_index.py:147-162, as one elementwise kernel.
+#include <cmath>
+#include <vector>
+
+#include "fg_device.cuh"
+#include "fg_internal.cuh"
+#include "fg_series.cuh"
+
+namespace fg {
+
+template <int D>
+__global__ void moments_leaf_kernel(int64_t node_begin, int64_t node_end,
+                                    const int4 *__restrict__ node_i,
+                                    const double *__restrict__ node_c,
+                                    const double *__restrict__ pw, int p, int K, double sc,
+                                    const uint8_t *__restrict__ digits,
+                                    const double *__restrict__ inv_fact,
+                                    double *__restrict__ mom) {
+    const int64_t node = node_begin + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (node >= node_end) return;
+    const int4 ni = node_i[node];
+    if (ni.z >= 0) return;  // internal: handled by the H2H pass
+    double c[D];
+#pragma unroll
+    for (int d = 0; d < D; d++) c[d] = node_c[node * D + d];
+    accumulate_warp<D>(0, pw, ni.x, (int64_t)ni.x + ni.y, c, p, K, sc, digits, inv_fact,
+                       mom + node * K, true);
+}
+
+// Internal nodes of one level: A = H2H(left) + H2H(right).
+template <int D>
+__global__ void moments_h2h_kernel(int64_t node_begin, int64_t node_end,
+                                   const int4 *__restrict__ node_i,
+                                   const double *__restrict__ node_c, int p, int K, double sc,
+                                   const uint8_t *__restrict__ digits,
+                                   const double *__restrict__ inv_fact,
+                                   const int *__restrict__ off, const int2 *__restrict__ ab,
+                                   double *__restrict__ mom) {
+    extern __shared__ double sh[];  // per warp: 2*K shift values
+    const int lane = threadIdx.x & 31;
+    const int64_t node = node_begin + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    double *shift = sh + (threadIdx.x >> 5) * 2 * K;
+    const bool live = node < node_end;
+    int4 ni = make_int4(0, 0, -1, -1);
+    if (live) ni = node_i[node];
+    const bool internal = live && ni.z >= 0;
+    if (internal) {
+        for (int c = 0; c < 2; c++) {
+            const int64_t ch = c == 0 ? ni.z : ni.w;
+            double pwt[D][2 * kMaxOrder];
+#pragma unroll
+            for (int d = 0; d < D; d++)
+                power_ladder((node_c[ch * D + d] - node_c[node * D + d]) / sc, p - 1, pwt[d]);
+            for (int k = lane; k < K; k += 32)
+                shift[c * K + k] = product<D>(digits_of(digits, k), pwt) * inv_fact[k];
+        }
+    }
+    __syncwarp();
+    if (!internal) return;
+    const double *Al = mom + (int64_t)ni.z * K;
+    const double *Ar = mom + (int64_t)ni.w * K;
+    for (int s = lane; s < K; s += 32) {
+        double l = 0.0, r = 0.0;
+        for (int q = off[s]; q < off[s + 1]; q++) {
+            const int2 pr = ab[q];
+            l += Al[pr.x] * shift[pr.y];
+        }
+        for (int q = off[s]; q < off[s + 1]; q++) {
+            const int2 pr = ab[q];
+            r += Ar[pr.x] * shift[K + pr.y];
+        }
+        mom[node * K + s] = l + r;
+    }
+}
+
+__global__ void moments_rescale_kernel(int64_t total, int K, const double *__restrict__ src,
+                                       const double *__restrict__ fac, double *__restrict__ dst) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    dst[i] = src[i] * fac[i % K];
+}
+
+template <int D>
+static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst) {
+    const int K = T.K, p = T.order;
+    const double sc = kSqrt2 * h;
+    const int warps_per_block = 8;
+    const int64_t nn = t.nnodes;
+    {
+        const unsigned blocks = (unsigned)((nn + warps_per_block - 1) / warps_per_block);
+        moments_leaf_kernel<D><<<blocks, 32 * warps_per_block, 0, stream()>>>(
+            0, nn, t.node_i.as<int4>(), t.node_c.as<double>(), t.pw.as<double>(), p, K, sc,
+            T.digits.as<uint8_t>(), T.inv_fact.as<double>(), dst.as<double>());
+        FG_CUDA_TRY(cudaGetLastError());
+    }
+    for (int lv = t.levels - 1; lv >= 0; lv--) {
+        const int64_t b = t.level_begin[lv], e = t.level_begin[lv + 1];
+        if (e <= b) continue;
+        const unsigned blocks = (unsigned)((e - b + warps_per_block - 1) / warps_per_block);
+        const size_t smem = sizeof(double) * 2 * K * warps_per_block;
+        moments_h2h_kernel<D><<<blocks, 32 * warps_per_block, smem, stream()>>>(
+            b, e, t.node_i.as<int4>(), t.node_c.as<double>(), p, K, sc, T.digits.as<uint8_t>(),
+            T.inv_fact.as<double>(), T.h2h_off.as<int>(), T.h2h_ab.as<int2>(),
+            dst.as<double>());
+        FG_CUDA_TRY(cudaGetLastError());
+    }
+    return FG_OK;
+}
+
+static DBuf g_rescale_fac;
+
+int moments_refresh(TreeDev &t, double h, int plimit) {
+    FG_REQUIRE(h > 0.0 && std::isfinite(h), FG_EINVAL, "bandwidth must be positive");
+    FG_REQUIRE(plimit >= 1, FG_EINVAL, "truncation order must be at least 1");
+    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
+    int st = FG_OK;
+    const SeriesTables *T = series_tables(t.dim, plimit, &st);
+    FG_TRY(st);
+    const int K = T->K;
+    const int64_t total = t.nnodes * K;
+    FG_TRY(t.mom.reserve(sizeof(double) * total));
+    if (t.mom0_valid && t.mom_K == K && t.mom_order == plimit) {
+        // exact rescaling from the base bandwidth
+        std::vector<double> fac(K);
+        const double ratio = t.mom0_h / h;
+        for (int k = 0; k < K; k++) fac[k] = std::pow(ratio, (double)T->h_degrees[k]);
+        FG_TRY(g_rescale_fac.reserve(sizeof(double) * K));
+        FG_CUDA_TRY(cudaMemcpyAsync(g_rescale_fac.p, fac.data(), sizeof(double) * K,
+                                    cudaMemcpyHostToDevice, stream()));
+        moments_rescale_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream()>>>(
+            total, K, t.mom0.as<double>(), g_rescale_fac.as<double>(), t.mom.as<double>());
+        FG_CUDA_TRY(cudaGetLastError());
+        // the host copy of `fac` must outlive the async copy
+        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    } else {
+        FG_TRY(t.mom0.reserve(sizeof(double) * total));
+        switch (t.dim) {
+            case 1: st = moments_direct<1>(t, *T, h, t.mom0); break;
+            case 2: st = moments_direct<2>(t, *T, h, t.mom0); break;
+            case 3: st = moments_direct<3>(t, *T, h, t.mom0); break;
+            case 4: st = moments_direct<4>(t, *T, h, t.mom0); break;
+            case 5: st = moments_direct<5>(t, *T, h, t.mom0); break;
+            case 6: st = moments_direct<6>(t, *T, h, t.mom0); break;
+            case 7: st = moments_direct<7>(t, *T, h, t.mom0); break;
+            default: st = moments_direct<8>(t, *T, h, t.mom0); break;
+        }
+        FG_TRY(st);
+        FG_CUDA_TRY(cudaMemcpyAsync(t.mom.p, t.mom0.p, sizeof(double) * total,
+                                    cudaMemcpyDeviceToDevice, stream()));
+        t.mom0_valid = true;
+        t.mom0_h = h;
+    }
+    t.mom_K = K;
+    t.mom_order = plimit;
+    t.mom_h = h;
+    t.mom_valid = true;
+    return FG_OK;
+}
+
+int moments_export(const TreeDev &t, double *out) {
+    FG_REQUIRE(t.mom_valid, FG_ESTALE, "no moments: call refresh_moments first");
+    const int K = t.mom_K;
+    std::vector<double> m((size_t)t.nnodes * K);
+    FG_CUDA_TRY(cudaMemcpyAsync(m.data(), t.mom.p, sizeof(double) * m.size(),
+                                cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    std::vector<int64_t> pre;
+    FG_TRY(preorder_map(t, pre));
+    for (int64_t v = 0; v < t.nnodes; v++)
+        for (int k = 0; k < K; k++) out[pre[v] * K + k] = m[v * K + k];
+    return FG_OK;
+}
+
+}  // namespace fg

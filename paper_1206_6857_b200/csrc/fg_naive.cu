@@ -1,0 +1,170 @@
+// fg_naive.cu -- K1: exhaustive FP64 Gaussian sums (replaces naive_sum,
+// summation_engine.py:122-154).
+//
+// Layout: queries and references are packed into 16-byte-aligned AoS records
+// (coords, weight, pad).  A CTA owns 256*QPT queries held in registers and
+// streams a slice of the references through shared memory in tiles; every
+// thread reads the same reference record (broadcast LDS), so the inner loop
+// is pure FP64 pipe work: D DADD + D DFMA + 1 DMUL + exp + 1 DFMA per pair.
+// The reference range is split across blockIdx.y so that small M still fills
+// 148 SMs; partial sums are combined in a fixed order (deterministic).
+#include <vector>
+
+#include "fg_device.cuh"
+#include "fg_exp.cuh"
+#include "fg_internal.cuh"
+
+namespace fg {
+
+constexpr int kNaiveThreads = 256;
+constexpr int kNaiveTile = 256;
+
+// Pack row-major (n x dim) coordinates (+ optional weights) into records.
+__global__ void pack_points_kernel(const double *__restrict__ pts, const double *__restrict__ w,
+                                   int64_t n, int dim, int stride, double *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double *o = out + i * stride;
+    for (int d = 0; d < dim; d++) o[d] = pts[i * dim + d];
+    o[dim] = w ? w[i] : 1.0;
+    for (int d = dim + 1; d < stride; d++) o[d] = 0.0;
+}
+
+template <int D, int QPT>
+__global__ void __launch_bounds__(kNaiveThreads)
+naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__ r, int64_t n,
+             int64_t rchunk, double neg_inv, double *__restrict__ part) {
+    constexpr int S = packed_stride(D);
+    __shared__ __align__(16) double tile[kNaiveTile * S];
+    const int64_t q0 = (int64_t)blockIdx.x * kNaiveThreads * QPT;
+    const int64_t r0 = (int64_t)blockIdx.y * rchunk;
+    const int64_t r1 = min(n, r0 + rchunk);
+    double x[QPT][D], acc[QPT];
+#pragma unroll
+    for (int i = 0; i < QPT; i++) {
+        int64_t qi = q0 + threadIdx.x + (int64_t)i * kNaiveThreads;
+        acc[i] = 0.0;
+        if (qi < m) {
+            load_point<D>(q + qi * S, x[i]);
+        } else {
+#pragma unroll
+            for (int d = 0; d < D; d++) x[i][d] = 0.0;
+        }
+    }
+    for (int64_t t0 = r0; t0 < r1; t0 += kNaiveTile) {
+        const int cnt = (int)min((int64_t)kNaiveTile, r1 - t0);
+        __syncthreads();
+        {
+            const double2 *src = reinterpret_cast<const double2 *>(r + t0 * S);
+            double2 *dst = reinterpret_cast<double2 *>(tile);
+            for (int k = threadIdx.x; k < cnt * S / 2; k += kNaiveThreads) dst[k] = __ldg(src + k);
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int j = 0; j < cnt; j++) {
+            double y[D], w;
+            const double2 *t2 = reinterpret_cast<const double2 *>(tile + j * S);
+#pragma unroll
+            for (int k = 0; k < S / 2; k++) {
+                double2 v = t2[k];
+                if (2 * k < D) y[2 * k] = v.x;
+                else if (2 * k == D) w = v.x;
+                if (2 * k + 1 < D) y[2 * k + 1] = v.y;
+                else if (2 * k + 1 == D) w = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < QPT; i++) {
+                double diff = x[i][0] - y[0];
+                double d2 = diff * diff;
+#pragma unroll
+                for (int d = 1; d < D; d++) {
+                    double df = x[i][d] - y[d];
+                    d2 = fma(df, df, d2);
+                }
+                acc[i] = fma(fg_exp(d2 * neg_inv), w, acc[i]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < QPT; i++) {
+        int64_t qi = q0 + threadIdx.x + (int64_t)i * kNaiveThreads;
+        if (qi < m) part[(int64_t)blockIdx.y * m + qi] = acc[i];
+    }
+}
+
+__global__ void reduce_parts_kernel(const double *__restrict__ part, int64_t m, int nsplit,
+                                    double *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double s = 0.0;
+    for (int k = 0; k < nsplit; k++) s += part[(int64_t)k * m + i];
+    out[i] = s;
+}
+
+template <int D>
+static int launch_naive(const double *dq, int64_t m, const double *dr, int64_t n, double h,
+                        double *dpart, int nsplit, int64_t rchunk, int64_t qtiles) {
+    constexpr int QPT = (D <= 4) ? 2 : 1;
+    dim3 grid((unsigned)qtiles, (unsigned)nsplit);
+    naive_kernel<D, QPT><<<grid, kNaiveThreads, 0, stream()>>>(dq, m, dr, n, rchunk,
+                                                               -0.5 / (h * h), dpart);
+    FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
+static DBuf g_naive_q, g_naive_r, g_naive_part;
+
+int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
+              int dim, const double *hs, int nh, double *d_out) {
+    const int S = packed_stride(dim);
+    FG_TRY(g_naive_q.reserve(sizeof(double) * m * S));
+    FG_TRY(g_naive_r.reserve(sizeof(double) * n * S));
+    pack_points_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream()>>>(
+        d_q, nullptr, m, dim, S, g_naive_q.as<double>());
+    pack_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
+        d_r, d_w, n, dim, S, g_naive_r.as<double>());
+    FG_CUDA_TRY(cudaGetLastError());
+    const int qpt = dim <= 4 ? 2 : 1;
+    const int64_t qtiles = (m + kNaiveThreads * qpt - 1) / (kNaiveThreads * qpt);
+    // aim for >= 6 CTAs per SM worth of work; split the reference range
+    int64_t target = 148 * 6;
+    int64_t nsplit = (target + qtiles - 1) / qtiles;
+    int64_t max_split = (n + kNaiveTile - 1) / kNaiveTile;
+    if (nsplit > max_split) nsplit = max_split;
+    if (nsplit < 1) nsplit = 1;
+    if (nsplit > 65535) nsplit = 65535;
+    int64_t rchunk = (n + nsplit - 1) / nsplit;
+    rchunk = (rchunk + kNaiveTile - 1) / kNaiveTile * kNaiveTile;
+    nsplit = (n + rchunk - 1) / rchunk;
+    FG_TRY(g_naive_part.reserve(sizeof(double) * m * nsplit));
+    for (int k = 0; k < nh; k++) {
+        const double h = hs[k];
+        int st = FG_OK;
+        switch (dim) {
+#define FG_NAIVE_CASE(DD)                                                                   \
+    case DD:                                                                                \
+        st = launch_naive<DD>(g_naive_q.as<double>(), m, g_naive_r.as<double>(), n, h,      \
+                              g_naive_part.as<double>(), (int)nsplit, rchunk, qtiles);      \
+        break;
+            FG_NAIVE_CASE(1)
+            FG_NAIVE_CASE(2)
+            FG_NAIVE_CASE(3)
+            FG_NAIVE_CASE(4)
+            FG_NAIVE_CASE(5)
+            FG_NAIVE_CASE(6)
+            FG_NAIVE_CASE(7)
+            FG_NAIVE_CASE(8)
+#undef FG_NAIVE_CASE
+            default:
+                set_error("naive_sum: dimension > 8 is not supported by this build");
+                return FG_EUNSUPPORTED;
+        }
+        FG_TRY(st);
+        reduce_parts_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream()>>>(
+            g_naive_part.as<double>(), m, (int)nsplit, d_out + (int64_t)k * m);
+        FG_CUDA_TRY(cudaGetLastError());
+    }
+    return FG_OK;
+}
+
+}  // namespace fg

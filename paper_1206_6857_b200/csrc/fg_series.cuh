@@ -1,0 +1,203 @@
+// fg_series.cuh -- device restatements of the series algebra
+// (series_expansion.py) and the approximation selector (error_bounds.py).
+//
+// Coefficient vectors are dense over the graded-lex index set of their order
+// (kernel_math.py:122-209); the digit table is uint8 K x kMaxDim (padded).
+// The routines come in two flavours: per-lane (each lane evaluates at its own
+// point: EVALM / EVALL) and lanes-over-coefficients (a warp builds one
+// expansion: accumulate / translate), which keeps every lane busy without
+// shuffles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fg_device.cuh"
+#include "fg_internal.cuh"
+
+namespace fg {
+
+struct TailArgs {
+    double ct[kMaxOrder + 1], cross[kMaxOrder + 1];
+};
+
+// h_0 .. h_L of t (kernel_math.py:42-65)
+__device__ __forceinline__ void hermite_ladder(double t, int L, double *out) {
+    double g = exp(-t * t);
+    out[0] = g;
+    if (L >= 1) out[1] = 2.0 * t * g;
+    for (int n = 1; n < L; n++) out[n + 1] = 2.0 * t * out[n] - 2.0 * n * out[n - 1];
+}
+
+// u^0 .. u^L (kernel_math.py:97-108)
+__device__ __forceinline__ void power_ladder(double u, int L, double *out) {
+    out[0] = 1.0;
+    for (int k = 1; k <= L; k++) out[k] = out[k - 1] * u;
+}
+
+__device__ __forceinline__ uint64_t digits_of(const uint8_t *__restrict__ digits, int k) {
+    return __ldg(reinterpret_cast<const unsigned long long *>(digits) + k);
+}
+
+__device__ __forceinline__ int digit(uint64_t dg, int d) { return (int)((dg >> (8 * d)) & 0xff); }
+
+// prod_d table[d][digit_d] (MultiIndexSet.products, kernel_math.py:169-176)
+template <int D, class Table>
+__device__ __forceinline__ double product(uint64_t dg, const Table &table) {
+    double v = table[0][digit(dg, 0)];
+#pragma unroll
+    for (int d = 1; d < D; d++) v *= table[d][digit(dg, d)];
+    return v;
+}
+
+// EVALM: sum_{k<Kp} A_k prod_d h_{a_d}((x_d - c_d)/sc) (series_expansion.py:95-107)
+template <int D>
+__device__ double eval_far_lane(const double (&x)[D], const double *__restrict__ c,
+                                const double *__restrict__ A, int p, int Kp, double sc,
+                                const uint8_t *__restrict__ digits) {
+    double lad[D][2 * kMaxOrder];
+#pragma unroll
+    for (int d = 0; d < D; d++) hermite_ladder((x[d] - __ldg(c + d)) / sc, p - 1, lad[d]);
+    double acc = 0.0;
+    for (int k = 0; k < Kp; k++) acc += product<D>(digits_of(digits, k), lad) * __ldg(A + k);
+    return acc;
+}
+
+// EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)
+template <int D>
+__device__ double eval_local_lane(const double (&x)[D], const double (&c)[D],
+                                  const double *B, int p, int K, double sc,
+                                  const uint8_t *__restrict__ digits) {
+    double pw[D][2 * kMaxOrder];
+#pragma unroll
+    for (int d = 0; d < D; d++) power_ladder((x[d] - c[d]) / sc, p - 1, pw[d]);
+    double acc = 0.0;
+    for (int k = 0; k < K; k++) acc += product<D>(digits_of(digits, k), pw) * B[k];
+    return acc;
+}
+
+// Warp-cooperative accumulation over a point range (lanes own coefficients):
+// kind 0 = far-field moments A_a = sum_r w_r/a! ((x_r-c)/sc)^a (:76-92),
+// kind 1 = direct local B_b = sum_r w_r/b! h_b((x_r-c)/sc)       (:110-126).
+// Adds inv_fact-scaled sums into out[k] for k < Kp (out may alias shared mem).
+template <int D>
+__device__ void accumulate_warp(int kind, const double *__restrict__ pw_pts, int64_t r0,
+                                int64_t r1, const double (&c)[D], int p, int Kp, double sc,
+                                const uint8_t *__restrict__ digits,
+                                const double *__restrict__ inv_fact, double *out,
+                                bool overwrite) {
+    constexpr int S = packed_stride(D);
+    const int lane = threadIdx.x & 31;
+    double acc[kMaxK / 32];
+    uint64_t dg[kMaxK / 32];
+#pragma unroll
+    for (int j = 0; j < kMaxK / 32; j++) {
+        acc[j] = 0.0;
+        int k = lane + 32 * j;
+        dg[j] = k < Kp ? digits_of(digits, k) : 0;
+    }
+    double tab[D][2 * kMaxOrder];
+    for (int64_t r = r0; r < r1; r++) {
+        double y[D], w;
+        load_point_w<D>(pw_pts + r * S, y, w);
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            double u = (y[d] - c[d]) / sc;
+            if (kind == 0) power_ladder(u, p - 1, tab[d]);
+            else hermite_ladder(u, p - 1, tab[d]);
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxK / 32; j++) {
+            if (32 * j < Kp) acc[j] += w * product<D>(dg[j], tab);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxK / 32; j++) {
+        int k = lane + 32 * j;
+        if (k < Kp) {
+            double v = acc[j] * __ldg(inv_fact + k);
+            if (overwrite) out[k] = v;
+            else out[k] += v;
+        }
+    }
+}
+
+// H2L (series_expansion.py:167-194): source order ps (Ks coefficients),
+// destination order pd (Kd coefficients); lanes own destination coefficients
+// and add into out[b] for b < Kd.
+template <int D>
+__device__ void h2l_warp_add(const double *__restrict__ A, const double *__restrict__ src_c,
+                             const double (&dst_c)[D], int ps, int Ks, int pd, int Kd,
+                             double sc, const uint8_t *__restrict__ digits,
+                             const double *__restrict__ inv_fact, const int *__restrict__ degrees,
+                             double *out) {
+    const int lane = threadIdx.x & 31;
+    double lad[D][2 * kMaxOrder];
+#pragma unroll
+    for (int d = 0; d < D; d++)
+        hermite_ladder((dst_c[d] - __ldg(src_c + d)) / sc, (pd - 1) + (ps - 1), lad[d]);
+    for (int b = lane; b < Kd; b += 32) {
+        const uint64_t db = digits_of(digits, b);
+        double acc = 0.0;
+        for (int a = 0; a < Ks; a++) {
+            const uint64_t s = db + digits_of(digits, a);  // per-byte digit sums (< 2*8)
+            acc += product<D>(s, lad) * __ldg(A + a);
+        }
+        const double sign = (__ldg(degrees + b) % 2 == 0) ? 1.0 : -1.0;
+        out[b] += sign * __ldg(inv_fact + b) * acc;
+    }
+}
+
+// best_method (error_bounds.py:168-230).  ct/cross indexed by p (1..plimit).
+// method: 0 exhaustive, 2 hermite, 3 local, 4 h2l.
+__device__ __forceinline__ void best_method_dev(double min_sq, double r_ref, double r_query,
+                                                double w_ref, double n_query, double n_ref,
+                                                int dim, double h, double maxerr, int plimit,
+                                                const double *ct, const double *cross,
+                                                int &method, int &order, double &bound,
+                                                double &cost) {
+    const double base = w_ref * exp(-0.25 * min_sq / (h * h));
+    const double rr = r_ref, rq = r_query, sq = kSqrt2 * rq, sr = kSqrt2 * rr;
+    int p_h = 0, p_l = 0, p_t = 0;
+    double e_h = CUDART_INF, e_l = CUDART_INF, e_t = CUDART_INF;
+    if (base == 0.0) {
+        p_h = p_l = p_t = 1;
+        e_h = e_l = e_t = 0.0;
+    } else {
+        double x_r = rr, x_q = rq, x_sr = sr, x_sq = 1.0;
+        for (int p = 1; p <= plimit; p++) {
+            const double c = ct[p];
+            if (!p_h) {
+                double err = base * c * x_r;
+                if (err <= maxerr) { p_h = p; e_h = err; }
+            }
+            if (!p_l) {
+                double err = base * c * x_q;
+                if (err <= maxerr) { p_l = p; e_l = err; }
+            }
+            if (!p_t) {
+                double step = sq > 1.0 ? x_sq : 1.0;
+                double err = base * c * (x_q + x_sr * cross[p] * step);
+                if (err <= maxerr) { p_t = p; e_t = err; }
+            }
+            if (p_h && p_l && p_t) break;
+            x_r *= rr;
+            x_q *= rq;
+            x_sr *= sr;
+            x_sq *= sq;
+        }
+    }
+    const double d = (double)dim;
+    double c_h = CUDART_INF, c_l = CUDART_INF, c_t = CUDART_INF;
+    if (p_h) c_h = n_query * pow(d, (double)(p_h + 1));
+    if (p_l) c_l = n_ref * pow(d, (double)(p_l + 1));
+    if (p_t) c_t = pow(d, (double)(2 * p_t + 1));
+    const double c_x = d * n_query * n_ref;
+    double c = fmin(fmin(c_h, c_l), fmin(c_t, c_x));
+    if (c == c_h) { method = 2; order = p_h; bound = e_h; cost = c_h; return; }
+    if (c == c_l) { method = 3; order = p_l; bound = e_l; cost = c_l; return; }
+    if (c == c_t) { method = 4; order = p_t; bound = e_t; cost = c_t; return; }
+    method = 0; order = 0; bound = 0.0; cost = c_x;
+}
+
+}  // namespace fg

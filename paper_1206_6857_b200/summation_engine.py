@@ -1,0 +1,212 @@
+"""Gaussian summation on the B200 (mirror of summation_engine.py).
+
+``naive_sum`` runs the exhaustive FP64 kernel (fg_naive.cu);
+``dfd_run``/``dfdo_run``/``dito_run`` run the fused traversal kernel
+(fg_traverse.cu) with the reference's three mode flags
+(summation_engine.py:458-480).  Results come back in original query order
+as float64 NumPy arrays (or in a caller-provided CUDA tensor via ``out=``).
+Every run guarantees max_q |G_est - G| / G <= epsilon.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .spatial_index import KdTree, default_plimit
+
+_ALGORITHMS = ("naive", "dfd", "dfdo", "dito")
+
+
+@dataclass
+class RunConfig:
+    """summation_engine.py:57-78."""
+
+    bandwidth: float
+    epsilon: float = 0.01
+    algorithm: str = "dito"
+    plimit: int | None = None
+    leaf_threshold: int = 25
+
+    def __post_init__(self):
+        if self.bandwidth <= 0.0:
+            raise ValueError("bandwidth must be positive")
+        if self.epsilon < 0.0:
+            raise ValueError("epsilon must be non-negative")
+        if self.algorithm not in _ALGORITHMS:
+            raise ValueError(f"unknown algorithm {self.algorithm!r}")
+
+
+@dataclass
+class TraversalCounters:
+    """summation_engine.py:81-104, plus the number of exactly evaluated pairs."""
+
+    pair_visits: int = 0
+    base_cases: int = 0
+    fd_prunes: int = 0
+    hermite_prunes: int = 0
+    local_prunes: int = 0
+    h2l_prunes: int = 0
+    exact_pairs: int = 0
+
+    @property
+    def prunes(self) -> int:
+        return self.fd_prunes + self.hermite_prunes + self.local_prunes + self.h2l_prunes
+
+    def as_dict(self) -> dict:
+        return {
+            "pair_visits": self.pair_visits,
+            "base_cases": self.base_cases,
+            "fd_prunes": self.fd_prunes,
+            "hermite_prunes": self.hermite_prunes,
+            "local_prunes": self.local_prunes,
+            "h2l_prunes": self.h2l_prunes,
+        }
+
+    @classmethod
+    def _from_c(cls, c: _lib.fg_counters) -> "TraversalCounters":
+        return cls(c.pair_visits, c.base_cases, c.fd_prunes, c.hermite_prunes, c.local_prunes,
+                   c.h2l_prunes, c.exact_pairs)
+
+
+@dataclass
+class ResultVector:
+    """summation_engine.py:107-119."""
+
+    values: np.ndarray
+    seconds: float
+    counters: TraversalCounters = field(default_factory=TraversalCounters)
+    audit: list | None = None
+
+
+def naive_sum(queries, references, weights, h, out=None) -> ResultVector:
+    """Exact FP64 sums G(x_q) = sum_r w_r exp(-|x_q - x_r|^2 / 2h^2) on the GPU.
+
+    summation_engine.py:122-154.  ``h`` may be a scalar or a sequence of
+    bandwidths (then ``values`` has shape (len(h), M)).  Inputs may be NumPy
+    arrays or CUDA tensors; ``out`` may be a CUDA tensor to keep the result
+    on the device.
+    """
+    t0 = time.perf_counter()
+    q = _lib.as_f64(queries)
+    if q.ndim == 1:
+        q = q.reshape(1, -1)
+    r = _lib.as_f64(references)
+    if r.ndim == 1:
+        r = r.reshape(-1, q.shape[1])
+    w = _lib.as_f64(weights).reshape(-1)
+    m, dim = q.shape
+    n = r.shape[0]
+    if r.shape[1] != dim or w.shape[0] != n:
+        raise ValueError("shape mismatch between queries, references and weights")
+    hs = np.atleast_1d(np.asarray(h, dtype=float))
+    if np.any(hs <= 0.0):
+        raise ValueError("bandwidth must be positive")
+    vals = out if out is not None else np.empty((hs.shape[0], m))
+    _lib.call("fg_naive_sum", _lib.ptr(q), m, _lib.ptr(r), _lib.ptr(w), n, dim,
+              _lib.ptr(hs), hs.shape[0], _lib.ptr(vals))
+    if out is None and np.ndim(h) == 0:
+        vals = vals[0]
+    counters = TraversalCounters(exact_pairs=int(m) * int(n) * int(hs.shape[0]))
+    return ResultVector(vals, time.perf_counter() - t0, counters)
+
+
+def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: str,
+                        audit: bool, out=None, block_range=None) -> ResultVector:
+    """summation_engine.py:431-455 on the device."""
+    if audit:
+        raise NotImplementedError(
+            "the device engine does not record an audit ledger (SURVEY 8(f) item 3)")
+    plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
+    if mode == "dito" and (rtree.moments_bandwidth != config.bandwidth or
+                           rtree.moments_order is None or rtree.moments_order < plimit):
+        raise RuntimeError("reference moments missing or stale; call refresh_moments "
+                           "for this bandwidth first")
+    vals = out if out is not None else np.empty(qtree.n)
+    cnt = _lib.fg_counters()
+    secs = ctypes.c_double()
+    if block_range is None:
+        _lib.call("fg_run", qtree.handle, rtree.handle, float(config.bandwidth),
+                  float(config.epsilon), _lib.MODES[mode], int(plimit), _lib.ptr(vals),
+                  ctypes.byref(cnt), ctypes.byref(secs))
+    else:
+        b0, b1 = block_range
+        _lib.call("fg_run_range", qtree.handle, rtree.handle, float(config.bandwidth),
+                  float(config.epsilon), _lib.MODES[mode], int(plimit), int(b0), int(b1),
+                  _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
+    if out is None:
+        qtree.q_est = vals[qtree.perm]
+    return ResultVector(vals, secs.value, TraversalCounters._from_c(cnt), None)
+
+
+def dfd_run(config: RunConfig, qtree: KdTree, rtree: KdTree, audit: bool = False,
+            out=None) -> ResultVector:
+    """Finite-difference dual-tree summation (no tokens, no series)."""
+    return _run_tree_algorithm(config, qtree, rtree, "dfd", audit, out)
+
+
+def dfdo_run(config: RunConfig, qtree: KdTree, rtree: KdTree, audit: bool = False,
+             out=None) -> ResultVector:
+    """Finite-difference dual-tree summation with error tokens."""
+    return _run_tree_algorithm(config, qtree, rtree, "dfdo", audit, out)
+
+
+def dito_run(config: RunConfig, qtree: KdTree, rtree: KdTree, audit: bool = False,
+             out=None) -> ResultVector:
+    """Series-accelerated dual-tree summation with error tokens.
+
+    Requires ``rtree.refresh_moments(bandwidth, plimit)`` for this bandwidth.
+    """
+    return _run_tree_algorithm(config, qtree, rtree, "dito", audit, out)
+
+
+def query_block_count(qtree: KdTree) -> int:
+    """Number of 32-point query blocks (the unit of query sharding)."""
+    nb = ctypes.c_int64()
+    _lib.call("fg_query_blocks", qtree.handle, ctypes.byref(nb))
+    return nb.value
+
+
+def run_blocks(config: RunConfig, qtree: KdTree, rtree: KdTree, block_begin: int,
+               block_end: int, out=None) -> ResultVector:
+    """Run ``config.algorithm`` on query blocks [block_begin, block_end) only."""
+    vals = out if out is not None else np.zeros(qtree.n)
+    return _run_tree_algorithm(config, qtree, rtree, config.algorithm, False, vals,
+                               (block_begin, block_end))
+
+
+def dito_post(qtree: KdTree) -> None:
+    """Push node-level estimates and local polynomials of the host mirror
+    state down to the points (summation_engine.py:253-281).
+
+    The device engine applies this pass inside each run; this function serves
+    callers that populate the mirror state (``reset_query_state`` fields)
+    themselves.  Shifts and evaluations run on the device.
+    """
+    from .series_expansion import add_local, eval_local, translate_l2l
+
+    if qtree.q_est is None:
+        raise RuntimeError("query state not initialised; call reset_query_state first")
+    pts = qtree.points
+    stack = [qtree.root]
+    while stack:
+        node = stack.pop()
+        if node.is_leaf:
+            if node.est != 0.0:
+                qtree.q_est[node.start:node.end] += node.est
+            if node.local_used:
+                qtree.q_est[node.start:node.end] += eval_local(node.local,
+                                                               pts[node.start:node.end])
+            continue
+        for child in (node.left, node.right):
+            child.est += node.est
+            if node.local_used:
+                add_local(child.local, translate_l2l(node.local, child.center))
+                child.local_used = True
+        node.est = 0.0
+        stack.append(node.right)
+        stack.append(node.left)

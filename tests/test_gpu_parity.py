@@ -1,0 +1,274 @@
+"""GPU parity: the B200 engine vs the CPU oracle and the reference golden vectors.
+
+Bars: exhaustive <= 1e-12 relative per query; tree permutation
+and node ranges identical; moments <= 1e-10 of each node's largest
+coefficient; series functions <= 1e-12; every tree run within eps of the
+exhaustive sums, within 2*eps of the reference's own DITO, and <= 1e-12 at
+eps = 0.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fg():
+    import paper_1206_6857_b200 as fg
+
+    return fg
+
+
+def rel(a, b):
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    return float(np.max(np.abs(a - b) / np.abs(b))) if a.size else 0.0
+
+
+# ------------------------------------------------------------ exhaustive
+@pytest.mark.parametrize("D", [1, 2, 3, 5, 7, 8])
+def test_naive_random(fg, oracle, D):
+    rng = np.random.default_rng(D)
+    q = rng.random((700, D))
+    r = rng.random((1300, D))
+    w = rng.uniform(0.5, 2.0, 1300)
+    for h in (0.05, 0.3, 2.0):
+        got = fg.naive_sum(q, r, w, h).values
+        exp = oracle.naive_sum(q, r, w, h, threads=0)
+        assert rel(got, exp) <= 1e-12
+
+
+def test_naive_multi_bandwidth_and_1d_query(fg, oracle):
+    rng = np.random.default_rng(3)
+    r = rng.random((500, 3))
+    w = np.ones(500)
+    got = fg.naive_sum(r[:7], r, w, [0.1, 0.4]).values
+    assert got.shape == (2, 7)
+    for j, h in enumerate((0.1, 0.4)):
+        assert rel(got[j], oracle.naive_sum(r[:7], r, w, h)) <= 1e-12
+    one = fg.naive_sum(r[0], r, w, 0.1).values
+    assert one.shape == (1,)
+
+
+def test_naive_golden_config1(fg):
+    from paper_1206_6857_b200.configs import config
+
+    wl = config(1)
+    g = golden("config1.npz")
+    got = fg.naive_sum(wl.queries, wl.references, wl.weights, 0.05).values
+    assert rel(got, g["naive"]) <= 1e-12
+
+
+@pytest.mark.parametrize("i", [2, 3, 4, 5])
+def test_naive_golden_subsamples(fg, i):
+    from paper_1206_6857_b200.configs import config
+
+    g = golden(f"sub_C{i}.npz")
+    wl = config(i, scale=float(g["scale"]))
+    qs = wl.references[g["query_index"]]
+    got = fg.naive_sum(qs, wl.references, wl.weights, list(g["bandwidths"])).values
+    assert rel(got, g["naive"]) <= 1e-12
+
+
+def test_kernel_known_answer(fg):
+    # tests/test_kernel_math.py:66-72
+    h = 0.7
+    v = fg.naive_sum(np.array([[np.sqrt(2.0) * h]]), np.zeros((1, 1)), np.ones(1), h).values
+    assert abs(v[0] - 0.36787944117144233) <= 1e-14
+    assert fg.naive_sum(np.zeros((1, 1)), np.zeros((1, 1)), np.ones(1), h).values[0] == 1.0
+
+
+# ------------------------------------------------------------------ trees
+@pytest.mark.parametrize("name", ["uniform3", "dup", "ident", "small", "leaf1",
+                                  "C2", "C3", "C4", "C5"])
+def test_tree_matches_reference(fg, name):
+    g = golden(f"tree_{name}.npz")
+    t = fg.build_tree(fg.PointStore(g["points"], g["weights"]), int(g["leaf"]))
+    a = t.arrays()
+    for key in ("perm", "start", "end", "left", "right"):
+        np.testing.assert_array_equal(a[key], g[key], err_msg=key)
+    np.testing.assert_array_equal(a["lo"], g["lo"])
+    np.testing.assert_array_equal(a["hi"], g["hi"])
+    np.testing.assert_allclose(a["center"], g["center"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(a["inf_radius"], g["inf_radius"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(a["weight"], g["weight"], rtol=1e-12)
+    np.testing.assert_array_equal(t.points, g["points"][g["perm"]])
+
+
+def test_tree_validation(fg):
+    with pytest.raises(ValueError):
+        fg.PointStore(np.empty((0, 2)))
+    with pytest.raises(ValueError):
+        fg.PointStore(np.ones((3, 2)), np.array([1.0, 0.0, 2.0]))
+    with pytest.raises(ValueError):
+        fg.build_tree(fg.PointStore(np.ones((3, 2))), 0)
+
+
+def test_tree_node_model(fg):
+    # tests/test_spatial_index.py:46-83 invariants on the host mirror
+    rng = np.random.default_rng(1)
+    pts = rng.random((1000, 3))
+    w = rng.uniform(0.5, 2.0, 1000)
+    tree = fg.build_tree(fg.PointStore(pts, w), 20)
+    covered = np.zeros(1000, dtype=int)
+    for leaf in tree.leaves:
+        assert leaf.count <= 20
+        covered[leaf.start:leaf.end] += 1
+    assert np.all(covered == 1)
+    np.testing.assert_allclose(tree.points, pts[tree.perm])
+    np.testing.assert_allclose(tree.weights, w[tree.perm])
+    for node in tree.nodes:
+        inside = tree.points[node.start:node.end]
+        np.testing.assert_allclose(node.center, inside.mean(axis=0), rtol=1e-12)
+        assert np.abs(inside - node.center).max() <= node.inf_radius * (1 + 1e-12)
+
+
+@pytest.mark.parametrize("D", [2, 3, 5])
+def test_moments_match_reference(fg, D):
+    g = golden(f"moments_D{D}.npz")
+    t = fg.build_tree(fg.PointStore(g["points"], g["weights"]), int(g["leaf"]))
+    for h, ref in zip(g["bandwidths"], g["moments"]):
+        t.refresh_moments(float(h), int(g["plimit"]))
+        m = t.moments_array()
+        scale = np.abs(ref).max(axis=1, keepdims=True) + 1e-30
+        assert np.max(np.abs(m - ref) / scale) <= 1e-10
+
+
+def test_moments_rescaling_law(fg):
+    # tests/test_spatial_index.py:147-162
+    rng = np.random.default_rng(5)
+    tree = fg.build_tree(fg.PointStore(rng.random((40, 2))), 10)
+    tree.refresh_moments(0.3, 4)
+    base = tree.root.moments.coeffs.copy()
+    deg = np.array([sum(a) for a in fg.kernel_math.enumerate_multi_indices(2, 4)], float)
+    for c in (np.sqrt(2.0), 2.0):
+        tree.refresh_moments(c * 0.3, 4)
+        np.testing.assert_allclose(tree.root.moments.coeffs, base * c ** (-deg),
+                                   rtol=1e-10, atol=1e-14)
+
+
+# ----------------------------------------------------------------- series
+def test_series_functions_match_reference(fg):
+    g = golden("series.npz")
+    for k in range(int(g["count"])):
+        D, p, h = g[f"c{k}_meta"]
+        D, p = int(D), int(p)
+        pts, w, x = g[f"c{k}_pts"], g[f"c{k}_w"], g[f"c{k}_x"]
+        c, c2, cq = g[f"c{k}_c"], g[f"c{k}_c2"], g[f"c{k}_cq"]
+        far = fg.accumulate_far_field(pts, w, c, p, h)
+        np.testing.assert_allclose(far.coeffs, g[f"c{k}_far"], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(fg.eval_far_field(far, x), g[f"c{k}_evalm"], rtol=1e-12,
+                                   atol=1e-15)
+        loc = fg.accumulate_local_direct(pts, w, cq, p, h)
+        np.testing.assert_allclose(loc.coeffs, g[f"c{k}_loc"], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(fg.eval_local(loc, x), g[f"c{k}_evall"], rtol=1e-12,
+                                   atol=1e-15)
+        np.testing.assert_allclose(fg.translate_h2h(far, c2).coeffs, g[f"c{k}_h2h"],
+                                   rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(fg.translate_h2l(far, cq, p).coeffs, g[f"c{k}_h2l"],
+                                   rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(fg.translate_l2l(loc, c2).coeffs, g[f"c{k}_l2l"],
+                                   rtol=1e-12, atol=1e-15)
+
+
+def test_best_method_matches_reference(fg):
+    from paper_1206_6857_b200.error_bounds import best_method_batch
+
+    g = golden("bounds.npz")
+    codes = {0: "exhaustive", 2: "hermite", 3: "local", 4: "h2l"}
+    rows = g["rows"]
+    for D in np.unique(rows[:, 7]):
+        for pl in np.unique(rows[:, 10]):
+            sel = rows[(rows[:, 7] == D) & (rows[:, 10] == pl)]
+            if not len(sel):
+                continue
+            geoms = [fg.NodePairGeometry(r[0], r[1], r[2], r[3], r[4], int(r[5]), int(r[6]),
+                                         int(D), r[8]) for r in sel]
+            got = best_method_batch(geoms, sel[:, 9], int(pl))
+            for ch, r in zip(got, sel):
+                assert ch.method.value == codes[int(r[11])]
+                assert (ch.order or 0) == int(r[12])
+                assert ch.bound == pytest.approx(r[13], rel=1e-12, abs=1e-300)
+                assert ch.cost == pytest.approx(r[14], rel=1e-12)
+
+
+# ------------------------------------------------------------------- runs
+@pytest.mark.parametrize("name", ["mono_D1", "mono_D2", "mono_D3", "mono_D5", "mono_D7",
+                                  "bi_D3"])
+def test_runs_eps_contract(fg, name):
+    g = golden(f"run_{name}.npz")
+    pts, w, qs = g["points"], g["weights"], g["queries"]
+    rt = fg.build_tree(fg.PointStore(pts, w), 25)
+    qt = rt if int(g["mono"]) else fg.build_tree(fg.PointStore(qs), 25)
+    D = pts.shape[1]
+    for j, h in enumerate(g["bandwidths"]):
+        h = float(h)
+        naive = g["naive"][j]
+        rt.refresh_moments(h, fg.default_plimit(D))
+        for eps in (0.01, 0.001, 0.0):
+            for alg, run in (("dfd", fg.dfd_run), ("dfdo", fg.dfdo_run), ("dito", fg.dito_run)):
+                res = run(fg.RunConfig(bandwidth=h, epsilon=eps), qt, rt)
+                err = rel(res.values, naive)
+                bar = eps if eps > 0 else 1e-12
+                assert err <= bar, (alg, h, eps, err)
+                ref_vals = g[f"{alg}_{eps}_values"][j]
+                assert rel(res.values, ref_vals) <= 2 * eps + 1e-12, (alg, h, eps)
+
+
+def test_config1_full(fg):
+    from paper_1206_6857_b200.configs import config
+
+    g = golden("config1.npz")
+    wl = config(1)
+    rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
+    qt = fg.build_tree(fg.PointStore(wl.queries), 25)
+    rt.refresh_moments(0.05, fg.default_plimit(2))
+    res = fg.dito_run(fg.RunConfig(bandwidth=0.05, epsilon=0.01), qt, rt)
+    assert rel(res.values, g["naive"]) <= 0.01
+    assert rel(res.values, g["dito"]) <= 0.02
+    assert res.counters.exact_pairs < 1e8
+
+
+def test_stale_moments_raise(fg):
+    rng = np.random.default_rng(2)
+    t = fg.build_tree(fg.PointStore(rng.random((300, 2))), 25)
+    with pytest.raises(RuntimeError):
+        fg.dito_run(fg.RunConfig(bandwidth=0.1), t, t)
+    t.refresh_moments(0.2, 8)
+    with pytest.raises(RuntimeError):
+        fg.dito_run(fg.RunConfig(bandwidth=0.1), t, t)
+    fg.dito_run(fg.RunConfig(bandwidth=0.2), t, t)
+
+
+@pytest.mark.parametrize("case", ["identical", "single", "tiny_h", "huge_h", "dup_clusters",
+                                  "D8", "far_queries"])
+def test_edge_cases(fg, oracle, case):
+    rng = np.random.default_rng(11)
+    qs = None
+    if case == "identical":
+        pts, h = np.tile([0.3, 0.7], (500, 1)), 0.1
+    elif case == "single":
+        pts, h = np.array([[0.5, 0.5, 0.5]]), 0.2
+    elif case == "tiny_h":
+        pts, h = rng.random((3000, 3)), 1e-4
+    elif case == "huge_h":
+        pts, h = rng.random((3000, 3)), 1e3
+    elif case == "dup_clusters":
+        pts, h = np.repeat(rng.random((50, 2)), 40, axis=0), 0.05
+    elif case == "D8":
+        pts, h = rng.random((2000, 8)), 0.5
+    else:
+        pts, h = rng.random((2000, 2)), 0.05
+        qs = rng.random((300, 2)) + 3.0
+    w = rng.uniform(0.5, 1.5, pts.shape[0])
+    rt = fg.build_tree(fg.PointStore(pts, w), 25)
+    qt = rt if qs is None else fg.build_tree(fg.PointStore(qs), 25)
+    qpts = pts if qs is None else qs
+    exact = oracle.naive_sum(qpts, pts, w, h, threads=0)
+    rt.refresh_moments(h, fg.default_plimit(pts.shape[1]))
+    for eps in (0.01, 0.0):
+        res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=eps), qt, rt)
+        assert oracle.max_rel_error(res.values, exact) <= max(eps, 1e-12)
