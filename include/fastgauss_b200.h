@@ -55,6 +55,10 @@ typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_inde
 
 int fg_version(void);
 const char *fg_last_error(void);
+/* diagnostics: number of kernels this library has launched so far, and a
+ * measured FP64 FMA throughput (TFLOP/s) on the current device */
+int fg_launch_count(int64_t *count);
+int fg_fp64_peak(double *tflops);
 /* stream: a cudaStream_t (NULL = legacy default stream) */
 int fg_set_stream(void *stream);
 int fg_set_device(int device);
@@ -100,13 +104,15 @@ int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h,
  * run (reset + traverse + post, like summation_engine.py:447-452). */
 int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
            int32_t plimit, double *values, fg_counters *counters, double *seconds);
-/* Query-sharded run: only query blocks [block_begin,
- * block_end) of qtree are processed; values is written only at those
- * blocks' queries (original order).  fg_query_blocks reports the block count. */
+/* Query-sharded run: only query blocks block_begin,
+ * block_begin + block_stride, ... (< block_end) of qtree are processed;
+ * values is written only at those blocks' queries (original order).  A
+ * query block is 32 consecutive tree-order points; fg_query_blocks reports
+ * the block count. */
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks);
 int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
-                 int32_t plimit, int64_t block_begin, int64_t block_end, double *values,
-                 fg_counters *counters, double *seconds);
+                 int32_t plimit, int64_t block_begin, int64_t block_end, int64_t block_stride,
+                 double *values, fg_counters *counters, double *seconds);
 /* engine knobs (0 keeps the current value): reference-side leaf size used by
  * the traversal, per-warp stack capacity.  Not part of the reference API. */
 int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap);

@@ -2,6 +2,7 @@
 // state, host/device pointer staging and the multi-index tables.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -18,6 +19,38 @@ static thread_local std::string t_last_error;
 static cudaStream_t g_stream = nullptr;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void pool_init() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done_dev = dev;
+}
+
+// FP64 FMA throughput probe: independent DFMA chains per thread, no memory
+// traffic in the loop (the roofline denominator for the pair kernels).
+__global__ void dfma_peak_kernel(double *out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+    double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+    for (int i = 0; i < iters; i++) {
+        x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+        x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
 cudaStream_t stream() { return g_stream; }
 
 bool is_device_ptr(const void *ptr) {
@@ -219,6 +252,42 @@ extern "C" {
 
 int fg_version(void) { return 1; }
 
+int fg_launch_count(int64_t *count) {
+    FG_REQUIRE(count, FG_EINVAL, "null pointer");
+    *count = (int64_t)g_launches.load();
+    return FG_OK;
+}
+
+int fg_fp64_peak(double *tflops) {
+    FG_REQUIRE(tflops, FG_EINVAL, "null pointer");
+    int dev = 0, sms = 0;
+    FG_CUDA_TRY(cudaGetDevice(&dev));
+    FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf sink;
+    FG_TRY(sink.reserve(sizeof(double)));
+    const int threads = 256, blocks = sms * 8, iters = 1 << 14;
+    cudaEvent_t e0, e1;
+    FG_CUDA_TRY(cudaEventCreate(&e0));
+    FG_CUDA_TRY(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {
+        cudaEventRecord(e0, stream());
+        count_launch();
+        dfma_peak_kernel<<<blocks, threads, 0, stream()>>>(sink.as<double>(), iters, 0.999999,
+                                                           1e-7);
+        cudaEventRecord(e1, stream());
+        FG_CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    return FG_OK;
+}
+
 const char *fg_last_error(void) { return t_last_error.c_str(); }
 
 int fg_set_stream(void *s) {
@@ -338,6 +407,7 @@ int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
     DBuf tp, tw;
     if (points) FG_TRY(tp.reserve(sizeof(double) * t.n * t.dim));
     if (weights) FG_TRY(tw.reserve(sizeof(double) * t.n));
+    count_launch();
     unpack_points_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, stream()>>>(
         t.n, t.dim, t.stride, t.pw.as<double>(), points ? tp.as<double>() : nullptr,
         weights ? tw.as<double>() : nullptr);
@@ -366,8 +436,8 @@ int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h, i
 }
 
 static int run_impl(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
-                    int32_t plimit, int64_t b0, int64_t b1, double *values, fg_counters *counters,
-                    double *seconds) {
+                    int32_t plimit, int64_t b0, int64_t b1, int64_t stride, double *values,
+                    fg_counters *counters, double *seconds) {
     FG_REQUIRE(qtree && rtree && values, FG_EINVAL, "null argument");
     const int64_t m = qtree->t.n;
     const bool out_dev = is_device_ptr(values);
@@ -375,14 +445,14 @@ static int run_impl(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_
     if (!out_dev) {
         FG_TRY(g_stage_out.reserve(sizeof(double) * m));
         dout = g_stage_out.as<double>();
-        if (b0 > 0 || (b1 >= 0 && b1 < (qtree->t.n + 31) / 32)) {
+        if (b0 > 0 || stride > 1 || (b1 >= 0 && b1 < (qtree->t.n + 31) / 32)) {
             // partial range: keep the caller's other entries
             FG_CUDA_TRY(cudaMemcpyAsync(dout, values, sizeof(double) * m,
                                         cudaMemcpyHostToDevice, stream()));
         }
     }
-    FG_TRY(run_traversal(qtree->t, rtree->t, h, eps, mode, plimit, b0, b1, dout, counters,
-                         seconds));
+    FG_TRY(run_traversal(qtree->t, rtree->t, h, eps, mode, plimit, b0, b1, stride, dout,
+                         counters, seconds));
     if (!out_dev) {
         FG_CUDA_TRY(cudaMemcpyAsync(values, dout, sizeof(double) * m, cudaMemcpyDeviceToHost,
                                     stream()));
@@ -393,7 +463,7 @@ static int run_impl(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_
 
 int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode, int32_t plimit,
            double *values, fg_counters *counters, double *seconds) {
-    return run_impl(qtree, rtree, h, eps, mode, plimit, 0, -1, values, counters, seconds);
+    return run_impl(qtree, rtree, h, eps, mode, plimit, 0, -1, 1, values, counters, seconds);
 }
 
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks) {
@@ -404,11 +474,12 @@ int fg_query_blocks(fg_tree *qtree, int64_t *nblocks) {
 }
 
 int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
-                 int32_t plimit, int64_t block_begin, int64_t block_end, double *values,
-                 fg_counters *counters, double *seconds) {
+                 int32_t plimit, int64_t block_begin, int64_t block_end, int64_t block_stride,
+                 double *values, fg_counters *counters, double *seconds) {
     FG_REQUIRE(block_begin >= 0 && block_end >= block_begin, FG_EINVAL, "bad block range");
-    return run_impl(qtree, rtree, h, eps, mode, plimit, block_begin, block_end, values,
-                    counters, seconds);
+    FG_REQUIRE(block_stride >= 1, FG_EINVAL, "block stride must be >= 1");
+    return run_impl(qtree, rtree, h, eps, mode, plimit, block_begin, block_end, block_stride,
+                    values, counters, seconds);
 }
 
 }  // extern "C"

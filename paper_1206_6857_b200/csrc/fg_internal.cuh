@@ -46,6 +46,10 @@ struct Status {
     } while (0)
 
 cudaStream_t stream();
+// keep freed pool memory cached (release threshold = max) on the current device
+void pool_init();
+// every kernel launch of the library bumps this (fg_launch_count)
+void count_launch();
 
 // ------------------------------------------------------- device buffers
 struct DBuf {
@@ -55,8 +59,10 @@ struct DBuf {
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
     ~DBuf() { release(); }
+    // Stream-ordered allocation from the device's memory pool (kept warm, see
+    // pool_init), so per-sweep trees and scratch cost no cudaMalloc/cudaFree.
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, stream());
         p = nullptr;
         bytes = 0;
     }
@@ -64,8 +70,9 @@ struct DBuf {
     int reserve(size_t nbytes) {
         if (nbytes <= bytes) return FG_OK;
         release();
+        pool_init();
         size_t nb = nbytes < 256 ? 256 : nbytes;
-        cudaError_t e = cudaMalloc(&p, nb);
+        cudaError_t e = cudaMallocAsync(&p, nb, stream());
         if (e != cudaSuccess) {
             set_error(std::string("cudaMalloc(") + std::to_string(nb) + "): " +
                       cudaGetErrorString(e));
@@ -162,7 +169,7 @@ int moments_refresh(TreeDev &t, double h, int plimit);
 int moments_export(const TreeDev &t, double *out);
 int query_blocks(TreeDev &t);
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
-                  int64_t b0, int64_t b1, double *d_values, fg_counters *counters,
+                  int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
                   double *seconds);
 int preorder_map(const TreeDev &t, std::vector<int64_t> &pre);
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,

@@ -97,6 +97,7 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     const int64_t nn = t.nnodes;
     {
         const unsigned blocks = (unsigned)((nn + warps_per_block - 1) / warps_per_block);
+        count_launch();
         moments_leaf_kernel<D><<<blocks, 32 * warps_per_block, 0, stream()>>>(
             0, nn, t.node_i.as<int4>(), t.node_c.as<double>(), t.pw.as<double>(), p, K, sc,
             T.digits.as<uint8_t>(), T.inv_fact.as<double>(), dst.as<double>());
@@ -107,6 +108,7 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
         if (e <= b) continue;
         const unsigned blocks = (unsigned)((e - b + warps_per_block - 1) / warps_per_block);
         const size_t smem = sizeof(double) * 2 * K * warps_per_block;
+        count_launch();
         moments_h2h_kernel<D><<<blocks, 32 * warps_per_block, smem, stream()>>>(
             b, e, t.node_i.as<int4>(), t.node_c.as<double>(), p, K, sc, T.digits.as<uint8_t>(),
             T.inv_fact.as<double>(), T.h2h_off.as<int>(), T.h2h_ab.as<int2>(),
@@ -136,6 +138,7 @@ int moments_refresh(TreeDev &t, double h, int plimit) {
         FG_TRY(g_rescale_fac.reserve(sizeof(double) * K));
         FG_CUDA_TRY(cudaMemcpyAsync(g_rescale_fac.p, fac.data(), sizeof(double) * K,
                                     cudaMemcpyHostToDevice, stream()));
+        count_launch();
         moments_rescale_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream()>>>(
             total, K, t.mom0.as<double>(), g_rescale_fac.as<double>(), t.mom.as<double>());
         FG_CUDA_TRY(cudaGetLastError());

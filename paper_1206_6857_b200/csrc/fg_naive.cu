@@ -106,6 +106,7 @@ static int launch_naive(const double *dq, int64_t m, const double *dr, int64_t n
                         double *dpart, int nsplit, int64_t rchunk, int64_t qtiles) {
     constexpr int QPT = (D <= 4) ? 2 : 1;
     dim3 grid((unsigned)qtiles, (unsigned)nsplit);
+    count_launch();
     naive_kernel<D, QPT><<<grid, kNaiveThreads, 0, stream()>>>(dq, m, dr, n, rchunk,
                                                                -0.5 / (h * h), dpart);
     FG_CUDA_TRY(cudaGetLastError());
@@ -119,8 +120,10 @@ int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w
     const int S = packed_stride(dim);
     FG_TRY(g_naive_q.reserve(sizeof(double) * m * S));
     FG_TRY(g_naive_r.reserve(sizeof(double) * n * S));
+    count_launch();
     pack_points_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream()>>>(
         d_q, nullptr, m, dim, S, g_naive_q.as<double>());
+    count_launch();
     pack_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
         d_r, d_w, n, dim, S, g_naive_r.as<double>());
     FG_CUDA_TRY(cudaGetLastError());
@@ -160,6 +163,7 @@ int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w
                 return FG_EUNSUPPORTED;
         }
         FG_TRY(st);
+        count_launch();
         reduce_parts_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream()>>>(
             g_naive_part.as<double>(), m, (int)nsplit, d_out + (int64_t)k * m);
         FG_CUDA_TRY(cudaGetLastError());

@@ -189,11 +189,13 @@ int fg_series_accumulate(int32_t kind, const double *pts, const double *w,
     const int S = packed_stride(dim);
     FG_TRY(g_s_pw.reserve(sizeof(double) * (npts > 0 ? npts : 1) * S));
     if (npts > 0) {
+        count_launch();
         pack_rows_kernel<<<(unsigned)((npts + 255) / 256), 256, 0, stream()>>>(
             (const double *)dp, (const double *)dw, npts, dim, S, g_s_pw.as<double>());
     }
     FG_TRY(g_s_out.reserve(sizeof(double) * batch * T->K));
     const unsigned blocks = (unsigned)((batch * 32 + 127) / 128);
+    count_launch();
     FG_DISPATCH_D(dim, (accumulate_batch_kernel<DD><<<blocks, 128, 0, stream()>>>(
                            kind, g_s_pw.as<double>(), (const int64_t *)doff, batch,
                            (const double *)dc, order, T->K, kSqrt2 * h,
@@ -229,6 +231,7 @@ int fg_series_eval(int32_t kind, const double *coeffs, int32_t k_stored, const d
     FG_TRY(to_device(offsets, sizeof(int64_t) * (batch + 1), s4, &doff));
     FG_TRY(g_s_out.reserve(sizeof(double) * (npts > 0 ? npts : 1)));
     const unsigned blocks = (unsigned)((batch * 32 + 127) / 128);
+    count_launch();
     FG_DISPATCH_D(dim, (eval_batch_kernel<DD><<<blocks, 128, 0, stream()>>>(
                            kind, (const double *)dco, k_stored, (const double *)dc, batch,
                            order, T->K, kSqrt2 * h, (const double *)dx, (const int64_t *)doff,
@@ -264,6 +267,7 @@ int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
     const size_t smem = sizeof(double) * warps * (Td->K > Ts->K ? Td->K : Ts->K);
     const int *off = kind == 0 ? Td->h2h_off.as<int>() : Td->l2l_off.as<int>();
     const int2 *pr = kind == 0 ? Td->h2h_ab.as<int2>() : Td->l2l_bs.as<int2>();
+    count_launch();
     FG_DISPATCH_D(dim, (translate_batch_kernel<DD><<<blocks, 32 * warps, smem, stream()>>>(
                            kind, (const double *)dco, k_stored, (const double *)dsc,
                            (const double *)ddc, batch, order_src, Ts->K, order, Td->K,
@@ -284,6 +288,7 @@ int fg_best_method(const double *geom, int32_t batch, int32_t dim, int32_t plimi
     DBuf s1;
     FG_TRY(to_device(geom, sizeof(double) * batch * 9, s1, &dg));
     FG_TRY(g_s_out.reserve(sizeof(double) * batch * 4));
+    count_launch();
     best_method_kernel<<<(batch + 127) / 128, 128, 0, stream()>>>(
         (const double *)dg, batch, dim, plimit, T, g_s_out.as<double>());
     FG_CUDA_TRY(cudaGetLastError());

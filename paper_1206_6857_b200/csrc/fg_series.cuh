@@ -148,6 +148,79 @@ __device__ void h2l_warp_add(const double *__restrict__ A, const double *__restr
     }
 }
 
+// Smallest feasible order of each series method (the order scan of
+// error_bounds.py:196-225).  p == 0 marks an infeasible method.
+__device__ __forceinline__ void feasible_orders(double min_sq, double r_ref, double r_query,
+                                                double w_ref, double h, double maxerr,
+                                                int plimit, const double *ct,
+                                                const double *cross, int &p_h, int &p_l,
+                                                int &p_t, double &e_h, double &e_l,
+                                                double &e_t) {
+    const double base = w_ref * exp(-0.25 * min_sq / (h * h));
+    const double rr = r_ref, rq = r_query, sq = kSqrt2 * rq, sr = kSqrt2 * rr;
+    p_h = p_l = p_t = 0;
+    e_h = e_l = e_t = CUDART_INF;
+    if (base == 0.0) {
+        p_h = p_l = p_t = 1;
+        e_h = e_l = e_t = 0.0;
+        return;
+    }
+    double x_r = rr, x_q = rq, x_sr = sr, x_sq = 1.0;
+    for (int p = 1; p <= plimit; p++) {
+        const double c = ct[p];
+        if (!p_h) {
+            double err = base * c * x_r;
+            if (err <= maxerr) { p_h = p; e_h = err; }
+        }
+        if (!p_l) {
+            double err = base * c * x_q;
+            if (err <= maxerr) { p_l = p; e_l = err; }
+        }
+        if (!p_t) {
+            double step = sq > 1.0 ? x_sq : 1.0;
+            double err = base * c * (x_q + x_sr * cross[p] * step);
+            if (err <= maxerr) { p_t = p; e_t = err; }
+        }
+        if (p_h && p_l && p_t) break;
+        x_r *= rr;
+        x_q *= rq;
+        x_sr *= sr;
+        x_sq *= sq;
+    }
+}
+
+// Method selection for the traversal kernel: the same feasibility rule as
+// best_method, with costs in warp-instruction units of THIS engine instead of
+// the reference's sequential-CPU costs (error_bounds.py:217-221).  A warp owns
+// a block of <= 32 queries, one per lane, so
+//   exhaustive ~ N_R (2D + 20)        (lanes evaluate 32 pairs per step)
+//   Hermite    ~ 32 D + K_p (D + 1)   (per-lane ladders + one K_p product sum)
+//   local      ~ N_R (32 D + ceil(K_p/32)(D + 1))
+//   H2L        ~ 32 D + ceil(K_p/32) K_p (D + 1)
+// Any feasible method keeps the error guarantee; only speed depends on this.
+__device__ __forceinline__ void select_method_gpu(double min_sq, double r_ref, double r_query,
+                                                  double w_ref, double n_ref, int dim,
+                                                  double h, double maxerr, int plimit,
+                                                  const double *ct, const double *cross,
+                                                  const int *kp, int &method, int &order,
+                                                  double &bound) {
+    int p_h, p_l, p_t;
+    double e_h, e_l, e_t;
+    feasible_orders(min_sq, r_ref, r_query, w_ref, h, maxerr, plimit, ct, cross, p_h, p_l, p_t,
+                    e_h, e_l, e_t);
+    const double d = (double)dim;
+    double c_h = CUDART_INF, c_l = CUDART_INF, c_t = CUDART_INF;
+    if (p_h) c_h = 32.0 * d + kp[p_h] * (d + 1.0);
+    if (p_l) c_l = n_ref * (32.0 * d + ((kp[p_l] + 31) / 32) * (d + 1.0));
+    if (p_t) c_t = 32.0 * d + ((kp[p_t] + 31) / 32) * (double)kp[p_t] * (d + 1.0);
+    const double c_x = n_ref * (2.0 * d + 20.0);
+    const double c = fmin(fmin(c_h, c_l), fmin(c_t, c_x));
+    if (c == c_h) { method = 2; order = p_h; bound = e_h; return; }
+    if (c == c_l) { method = 3; order = p_l; bound = e_l; return; }
+    if (c == c_t) { method = 4; order = p_t; bound = e_t; return; }
+    method = 0; order = 0; bound = 0.0;
+}
+
 // best_method (error_bounds.py:168-230).  ct/cross indexed by p (1..plimit).
 // method: 0 exhaustive, 2 hermite, 3 local, 4 h2l.
 __device__ __forceinline__ void best_method_dev(double min_sq, double r_ref, double r_query,

@@ -66,7 +66,7 @@ struct TravArgs {
     const double *qb_c;
     const double *qb_rad;
     const int64_t *q_perm;
-    long long b0, b1;
+    long long b0, b1, stride;
     double *out;
     // scalars
     double h, neg_inv, inv_h, sc, eps, total_w, floor_c;
@@ -139,7 +139,7 @@ traverse_kernel(const TravArgs A) {
 
     for (;;) {
         long long b = 0;
-        if (lane == 0) b = (long long)atomicAdd(A.work, 1ULL) + A.b0;
+        if (lane == 0) b = (long long)atomicAdd(A.work, 1ULL) * A.stride + A.b0;
         b = __shfl_sync(kFull, b, 0);
         if (b >= A.b1) break;
 
@@ -162,8 +162,7 @@ traverse_kernel(const TravArgs A) {
         double pt_est = 0.0, pt_mass = 0.0;                  // per point
         double node_est = 0.0, node_mass = 0.0, tokens = 0.0; // per block (uniform)
         bool local_used = false;
-        unsigned long long c_vis = 0, c_base = 0, c_fd = 0, c_dh = 0, c_dl = 0, c_h2l = 0,
-                           c_pairs = 0;
+        unsigned c_vis = 0, c_base = 0, c_fd = 0, c_dh = 0, c_dl = 0, c_h2l = 0, c_pairs = 0;
         if (A.use_series)
             for (int k = lane; k < A.K; k += 32) loc[k] = 0.0;
 
@@ -240,9 +239,8 @@ traverse_kernel(const TravArgs A) {
                         possible *= pw;
                     }
                     if (possible <= maxerr) {
-                        double cost;
-                        best_method_dev(mn, r_ref, r_qu, WR, (double)qn, (double)ni.y, D, A.h,
-                                        maxerr, A.plimit, A.ct, A.cross, meth, p, bound, cost);
+                        select_method_gpu(mn, r_ref, r_qu, WR, (double)ni.y, D, A.h, maxerr,
+                                          A.plimit, A.ct, A.cross, A.kp, meth, p, bound);
                     }
                 }
                 const bool cand = cand0 && meth != 0;
@@ -362,7 +360,7 @@ traverse_kernel(const TravArgs A) {
                 pt_mass += contrib;
                 if (A.use_tokens) tokens += wri;
                 c_base++;
-                c_pairs += (unsigned long long)qn * (unsigned long long)rc;
+                c_pairs += (unsigned)(qn * rc);
             }
         }
 
@@ -374,13 +372,13 @@ traverse_kernel(const TravArgs A) {
         }
         if (valid) A.out[A.q_perm[qs + lane]] = val;
         if (lane == 0) {
-            atomicAdd(A.counters + 0, c_vis);
-            atomicAdd(A.counters + 1, c_base);
-            atomicAdd(A.counters + 2, c_fd);
-            atomicAdd(A.counters + 3, c_dh);
-            atomicAdd(A.counters + 4, c_dl);
-            atomicAdd(A.counters + 5, c_h2l);
-            atomicAdd(A.counters + 6, c_pairs);
+            atomicAdd(A.counters + 0, (unsigned long long)c_vis);
+            atomicAdd(A.counters + 1, (unsigned long long)c_base);
+            atomicAdd(A.counters + 2, (unsigned long long)c_fd);
+            atomicAdd(A.counters + 3, (unsigned long long)c_dh);
+            atomicAdd(A.counters + 4, (unsigned long long)c_dl);
+            atomicAdd(A.counters + 5, (unsigned long long)c_h2l);
+            atomicAdd(A.counters + 6, (unsigned long long)c_pairs);
         }
         __syncwarp();
     }
@@ -436,6 +434,7 @@ int query_blocks(TreeDev &t) {
     const unsigned blocks = (unsigned)((nqb * 32 + 255) / 256);
 #define FG_QB(DD)                                                                           \
     case DD:                                                                                \
+        count_launch();                                                                     \
         query_blocks_kernel<DD><<<blocks, 256, 0, stream()>>>(                              \
             t.n, nqb, t.pw.as<double>(), t.qb_range.as<int2>(), t.qb_box.as<double>(),      \
             t.qb_c.as<double>(), t.qb_rad.as<double>());                                    \
@@ -485,6 +484,7 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks, cudaEvent_
     A.st_node = g_scr.st_node.as<int>();
     A.st_f = g_scr.st_f.as<double>();
     FG_CUDA_TRY(cudaEventRecord(e0, stream()));
+    count_launch();
     kern<<<(unsigned)grid, kTravThreads, smem, stream()>>>(A);
     FG_CUDA_TRY(cudaGetLastError());
     FG_CUDA_TRY(cudaEventRecord(e1, stream()));
@@ -492,7 +492,7 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks, cudaEvent_
 }
 
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
-                  int64_t b0, int64_t b1, double *d_values, fg_counters *counters,
+                  int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
                   double *seconds) {
     FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
     FG_REQUIRE(eps >= 0.0, FG_EINVAL, "epsilon must be non-negative");
@@ -525,6 +525,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     A.q_perm = q.perm.as<int64_t>();
     A.b0 = b0;
     A.b1 = b1;
+    A.stride = stride < 1 ? 1 : stride;
     A.out = d_values;
     A.h = h;
     A.neg_inv = -0.5 / (h * h);
@@ -568,7 +569,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     FG_CUDA_TRY(cudaEventCreate(&e0));
     FG_CUDA_TRY(cudaEventCreate(&e1));
     int st = FG_OK;
-    const int64_t nb = b1 - b0;
+    const int64_t nb = b1 > b0 ? (b1 - b0 + A.stride - 1) / A.stride : 0;
     if (nb > 0) {
         switch (D) {
             case 1: st = launch_traverse<1>(A, smem, nb, e0, e1); break;

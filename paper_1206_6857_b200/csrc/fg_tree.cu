@@ -456,27 +456,33 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
         const double *x = B.x[cur & 1].as<double>();
         const double *w = B.w[cur & 1].as<double>();
         const int *idx = B.idx[cur & 1].as<int>();
+        count_launch();
         fill_chunks_kernel<<<(na + 127) / 128, 128, 0, stream()>>>(
             na, act, t.node_i.as<int4>(), nch, choff, B.chunk_slot.as<int>(),
             B.chunk_begin.as<int>());
+        count_launch();
         stats_partial_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
             n, x, w, act, t.node_i.as<int4>(), B.chunk_slot.as<int>(), B.chunk_begin.as<int>(),
             B.part.as<double>());
         const int wblocks = (na * 32 + 255) / 256;
+        count_launch();
         node_stats_kernel<D><<<wblocks, 256, 0, stream()>>>(
             na, leaf, act, t.node_i.as<int4>(), nch, choff, B.part.as<double>(),
             t.node_box.as<double>(), t.node_c.as<double>(), t.node_wr.as<double2>(),
             B.split_dim.as<int>(), B.split_mid.as<double>());
+        count_launch();
         radius_count_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
             n, x, act, t.node_i.as<int4>(), B.chunk_slot.as<int>(), B.chunk_begin.as<int>(),
             t.node_c.as<double>(), B.split_dim.as<int>(), B.split_mid.as<double>(),
             B.part2.as<double>(), B.lcnt.as<int>());
+        count_launch();
         node_decide_kernel<<<wblocks, 256, 0, stream()>>>(
             na, act, t.node_i.as<int4>(), nch, choff, B.part2.as<double>(), B.lcnt.as<int>(),
             B.loff.as<int>(), t.node_wr.as<double2>(), B.split_dim.as<int>(),
             B.nleft.as<int>(), B.flag.as<int>());
         FG_CUDA_TRY(cudaGetLastError());
         FG_TRY(scan_ints(B.flag.as<int>(), B.rank.as<int>(), na, B));
+        count_launch();
         scatter_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
             n, x, w, idx, B.x[(cur + 1) & 1].as<double>(), B.w[(cur + 1) & 1].as<double>(),
             B.idx[(cur + 1) & 1].as<int>(), B.xf.as<double>(), B.wf.as<double>(),
@@ -484,11 +490,13 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
             B.chunk_begin.as<int>(), B.split_dim.as<int>(), B.split_mid.as<double>(),
             B.nleft.as<int>(), B.loff.as<int>());
         FG_CUDA_TRY(cudaMemsetAsync(nch_next, 0, sizeof(int) * 2 * na, stream()));
+        count_launch();
         make_children_kernel<<<(na + 127) / 128, 128, 0, stream()>>>(
             na, next_base, act, t.node_i.as<int4>(), B.flag.as<int>(), B.rank.as<int>(),
             B.nleft.as<int>(), act_next, nch_next);
         FG_CUDA_TRY(cudaGetLastError());
         FG_TRY(scan_ints(nch_next, choff_next, 2 * na, B));
+        count_launch();
         totals_kernel<<<1, 1, 0, stream()>>>(na, B.flag.as<int>(), B.rank.as<int>(), nch_next,
                                              choff_next, B.totals.as<int>());
         FG_CUDA_TRY(cudaMemcpyAsync(h_tot, B.totals.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
@@ -515,6 +523,7 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     // final packing
     FG_TRY(t.pw.reserve(sizeof(double) * n * packed_stride(D)));
     FG_TRY(t.perm.reserve(sizeof(int64_t) * n));
+    count_launch();
     pack_tree_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
         n, B.xf.as<double>(), B.wf.as<double>(), B.idxf.as<int>(), t.pw.as<double>(),
         t.perm.as<int64_t>());
@@ -566,6 +575,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_TRY(t.node_c.reserve(sizeof(double) * nmax * dim));
     FG_TRY(t.node_wr.reserve(sizeof(double2) * nmax));
     FG_CUDA_TRY(cudaMemsetAsync(B.bad.p, 0, sizeof(int), stream()));
+    count_launch();
     init_soa_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
         d_points, d_weights, n, dim, B.x[0].as<double>(), B.w[0].as<double>(),
         B.idx[0].as<int>(), B.bad.as<int>());

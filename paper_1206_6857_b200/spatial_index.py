@@ -272,6 +272,24 @@ def build_tree(store: PointStore, leaf_threshold: int = 25) -> KdTree:
     return KdTree(h.value, store, leaf_threshold)
 
 
+def build_tree_device(points, weights=None, leaf_threshold: int = 25) -> KdTree:
+    """build_tree for inputs already resident on the GPU (CUDA tensors, float64).
+
+    Validation (non-empty, positive weights, finite coordinates) runs on the
+    device; the host mirror (``points``/``nodes``...) is still available lazily.
+    """
+    if leaf_threshold < 1:
+        raise ValueError("leaf threshold must be at least 1")
+    pts = _lib.as_f64(points)
+    if pts.ndim != 2 or pts.shape[0] == 0:
+        raise ValueError("points must be a non-empty (N, D) array")
+    w = None if weights is None else _lib.as_f64(weights).reshape(-1)
+    h = ctypes.c_void_p()
+    _lib.call("fg_tree_build", _lib.ptr(pts), _lib.ptr(w), pts.shape[0], pts.shape[1],
+              int(leaf_threshold), ctypes.byref(h))
+    return KdTree(h.value, None, leaf_threshold)
+
+
 def min_sq_dist(a_lo, a_hi, b_lo, b_hi) -> float:
     gap = np.maximum(np.asarray(a_lo) - b_hi, np.asarray(b_lo) - a_hi)
     gap = np.maximum(gap, 0.0)

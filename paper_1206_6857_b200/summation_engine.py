@@ -134,10 +134,10 @@ def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: s
                   float(config.epsilon), _lib.MODES[mode], int(plimit), _lib.ptr(vals),
                   ctypes.byref(cnt), ctypes.byref(secs))
     else:
-        b0, b1 = block_range
+        b0, b1, stride = block_range
         _lib.call("fg_run_range", qtree.handle, rtree.handle, float(config.bandwidth),
                   float(config.epsilon), _lib.MODES[mode], int(plimit), int(b0), int(b1),
-                  _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
+                  int(stride), _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
     if out is None:
         qtree.q_est = vals[qtree.perm]
     return ResultVector(vals, secs.value, TraversalCounters._from_c(cnt), None)
@@ -172,11 +172,13 @@ def query_block_count(qtree: KdTree) -> int:
 
 
 def run_blocks(config: RunConfig, qtree: KdTree, rtree: KdTree, block_begin: int,
-               block_end: int, out=None) -> ResultVector:
-    """Run ``config.algorithm`` on query blocks [block_begin, block_end) only."""
+               block_end: int, block_stride: int = 1, out=None) -> ResultVector:
+    """Run ``config.algorithm`` on query blocks block_begin, block_begin +
+    block_stride, ... (< block_end) only; other entries of ``out`` are kept."""
     vals = out if out is not None else np.zeros(qtree.n)
-    return _run_tree_algorithm(config, qtree, rtree, config.algorithm, False, vals,
-                               (block_begin, block_end))
+    res = _run_tree_algorithm(config, qtree, rtree, config.algorithm, False, vals,
+                              (block_begin, block_end, block_stride))
+    return res
 
 
 def dito_post(qtree: KdTree) -> None:
