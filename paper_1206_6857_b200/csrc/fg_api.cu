@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -307,6 +308,7 @@ int fg_synchronize(void) {
 
 int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap) {
     if (ref_leaf > 0) g_ref_leaf = ref_leaf;
+    if (const char *m = getenv("FG_QBLOCK_MODE")) g_qblock_mode = atoi(m);
     if (stack_cap > 0) {
         FG_REQUIRE(stack_cap >= 64, FG_EINVAL, "stack capacity must be >= 64");
         g_stack_cap = stack_cap;

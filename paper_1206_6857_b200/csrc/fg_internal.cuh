@@ -175,5 +175,6 @@ int preorder_map(const TreeDev &t, std::vector<int64_t> &pre);
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
               int dim, const double *hs, int nh, double *d_out);
 extern int g_ref_leaf;
+extern int g_qblock_mode;
 extern int g_stack_cap;
 }  // namespace fg

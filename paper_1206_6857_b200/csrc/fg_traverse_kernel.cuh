@@ -1,0 +1,382 @@
+// fg_traverse_kernel.cuh -- the fused traversal kernel (see fg_traverse.cu for
+// the design notes).  Kept in its own header so the launch code and the kernel
+// body evolve separately.
+#pragma once
+
+#include "fg_device.cuh"
+#include "fg_exp.cuh"
+#include "fg_internal.cuh"
+#include "fg_series.cuh"
+
+namespace fg {
+
+constexpr int kTravThreads = 128;
+constexpr int kTravWarps = kTravThreads / 32;
+// Relative safety margin on the running mass bound: the frontier sum is kept
+// incrementally, so it carries <= (#updates) ulps of drift relative to G_min.
+constexpr double kMassSafety = 1.0 - 1e-10;
+
+struct TravArgs {
+    // reference tree (BFS numbering)
+    const double *r_pw;
+    const int4 *r_ni;
+    const double *r_box;
+    const double *r_c;
+    const double2 *r_wr;
+    const double *r_mom;
+    int mom_K;
+    // query blocks
+    const double *q_pw;
+    const int2 *qb_range;
+    const double *qb_box;
+    const double *qb_c;
+    const double *qb_rad;
+    const int64_t *q_perm;
+    long long b0, b1, stride;
+    double *out;
+    // scalars
+    double h, neg_inv, inv_h, sc, eps, total_w, floor_c;
+    int use_tokens, use_series, plimit, K, ref_leaf;
+    double ct[kMaxOrder + 1], cross[kMaxOrder + 1];
+    int kp[kMaxOrder + 1];  // coefficient count for order p
+    const uint8_t *digits;
+    const double *inv_fact;
+    const int *degrees;
+    // per-warp scratch: frontier stack and deferred series list
+    int *st_node;
+    double *st_f;
+    int2 *ser_list;
+    int stack_cap;
+    unsigned long long *work;
+    unsigned long long *counters;  // 7 counters
+    unsigned long long *dbg;       // optional per-block (cycles, steps, visits, pairs)
+    int no_eager;                  // experiment: credit base cases with K_lo only
+};
+
+// Admit candidates in lane order under the token rule.  Unconditional
+// candidates (req <= 0) bank their surplus first; the rest are taken greedily
+// in lane order while the balance covers them.  Never lets tokens go negative.
+__device__ __forceinline__ unsigned admit(bool cand, double req, double &tokens) {
+    const int lane = threadIdx.x & 31;
+    const unsigned un = __ballot_sync(kFull, cand && req <= 0.0);
+    tokens += warp_sum(((un >> lane) & 1u) ? -req : 0.0);
+    unsigned pos = __ballot_sync(kFull, cand && req > 0.0 && req <= tokens);
+    unsigned adm = un;
+    while (pos) {
+        const int i = __ffs(pos) - 1;
+        pos &= pos - 1;
+        const double ri = __shfl_sync(kFull, req, i);
+        if (tokens >= ri) {
+            tokens -= ri;
+            adm |= 1u << i;
+        }
+    }
+    return adm;
+}
+
+// _required_tokens (summation_engine.py:157-173)
+__device__ __forceinline__ double required_tokens(double wr, double err, double eps,
+                                                  double gmin, double total_w) {
+    if (err <= 0.0) return -wr;
+    const double den = eps * gmin;
+    return den > 0.0 ? total_w * err / den - wr : CUDART_INF;
+}
+
+// Box bounds of (query block box in shared memory, reference node) and both
+// kernel bounds (summation_engine.py:315-328).
+template <int D>
+__device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq, int node,
+                                             double &klo, double &khi, double &mn) {
+    const double *rbox = A.r_box + (int64_t)node * 2 * D;
+    double mx = 0.0;
+    mn = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double qlo = sq[d], qhi = sq[D + d];
+        const double rlo = __ldg(rbox + d), rhi = __ldg(rbox + D + d);
+        const double a = qlo - rhi, b = rlo - qhi;
+        const double g = a > b ? a : b;
+        if (g > 0.0) mn += g * g;
+        const double s1 = qhi - rlo, s2 = rhi - qlo;
+        const double s = s1 > s2 ? s1 : s2;
+        mx += s * s;
+    }
+    khi = exp(mn * A.neg_inv);
+    klo = exp(mx * A.neg_inv);
+}
+
+// Exact contribution of reference points [rs, rs+rc) to this lane's query
+// (_leaf_kernel_block, summation_engine.py:206-218): all lanes read the same
+// record (broadcast), two independent exp chains per step.
+template <int D>
+__device__ __forceinline__ double base_case(const double (&x)[D],
+                                            const double *__restrict__ rp, int rc,
+                                            double neg_inv) {
+    constexpr int S = packed_stride(D);
+    double acc0 = 0.0, acc1 = 0.0;
+    int j = 0;
+    for (; j + 1 < rc; j += 2) {
+        double y0[D], y1[D], w0, w1;
+        load_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        load_point_w<D>(rp + (int64_t)(j + 1) * S, y1, w1);
+        const double e0 = x[0] - y0[0], e1 = x[0] - y1[0];
+        double d0 = e0 * e0, d1 = e1 * e1;
+#pragma unroll
+        for (int d = 1; d < D; d++) {
+            const double f0 = x[d] - y0[d], f1 = x[d] - y1[d];
+            d0 = fma(f0, f0, d0);
+            d1 = fma(f1, f1, d1);
+        }
+        acc0 = fma(fg_exp(d0 * neg_inv), w0, acc0);
+        acc1 = fma(fg_exp(d1 * neg_inv), w1, acc1);
+    }
+    if (j < rc) {
+        double y0[D], w0;
+        load_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        const double e0 = x[0] - y0[0];
+        double d0 = e0 * e0;
+#pragma unroll
+        for (int d = 1; d < D; d++) {
+            const double f0 = x[d] - y0[d];
+            d0 = fma(f0, f0, d0);
+        }
+        acc0 = fma(fg_exp(d0 * neg_inv), w0, acc0);
+    }
+    return acc0 + acc1;
+}
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(kTravThreads, MINB)
+traverse_kernel(const TravArgs A) {
+    constexpr int S = packed_stride(D);
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * kTravWarps + wib;
+    // per-warp shared memory: query box (lo, hi), centroid, local coefficients
+    double *sq = smem + wib * (3 * D + A.K);
+    double *sqc = sq + 2 * D;
+    double *loc = sq + 3 * D;
+    int *sn = A.st_node + gw * A.stack_cap;
+    double *skl = A.st_f + gw * A.stack_cap * 3;
+    double *skh = skl + A.stack_cap;
+    double *smn = skh + A.stack_cap;
+    int2 *sl = A.ser_list + gw * A.stack_cap;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    for (;;) {
+        long long b = 0;
+        if (lane == 0) b = (long long)atomicAdd(A.work, 1ULL) * A.stride + A.b0;
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= A.b1) break;
+
+        const long long t_start = clock64();
+        unsigned steps = 0;
+        const int2 rg = A.qb_range[b];
+        const int qs = rg.x, qn = rg.y;
+        const bool valid = lane < qn;
+        if (lane < 2 * D) sq[lane] = A.qb_box[b * 2 * D + lane];
+        if (lane < D) sqc[lane] = A.qb_c[b * D + lane];
+        if (A.use_series)
+            for (int k = lane; k < A.K; k += 32) loc[k] = 0.0;
+        __syncwarp();
+        double x[D];
+        if (valid) load_point<D>(A.q_pw + (int64_t)(qs + lane) * S, x);
+        else {
+#pragma unroll
+            for (int d = 0; d < D; d++) x[d] = sqc[d];
+        }
+        double pt_est = 0.0, pt_mass = 0.0;                    // per point
+        double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
+        unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0;
+        int nser = 0;
+
+        // root entry
+        double fsum;  // sum over the frontier of W_R * K_lo
+        int sp = 1;
+        {
+            double klo, khi, mn;
+            entry_bounds<D>(A, sq, 0, klo, khi, mn);
+            if (lane == 0) {
+                sn[0] = 0;
+                skl[0] = klo;
+                skh[0] = khi;
+                smn[0] = mn;
+            }
+            fsum = A.r_wr[0].x * klo;
+        }
+        __syncwarp();
+
+        while (sp > 0) {
+            const int nb = min(sp, 32);
+            steps++;
+            const int base = sp - nb;
+            sp = base;
+            const bool act = lane < nb;
+            int node = 0;
+            double klo = 0.0, khi = 0.0, mn = 0.0;
+            int4 ni = make_int4(0, 0, -1, -1);
+            double2 wr = make_double2(0.0, 0.0);
+            if (act) {
+                node = sn[base + lane];
+                klo = skl[base + lane];
+                khi = skh[base + lane];
+                mn = smn[base + lane];
+                ni = A.r_ni[node];
+                wr = A.r_wr[node];
+            }
+            __syncwarp();
+            const double WR = wr.x;
+            c_vis += nb;
+            const double batch_sum = warp_sum(act ? WR * klo : 0.0);
+            const double pmin = warp_min(valid ? pt_mass : CUDART_INF);
+            const double gmin = (pmin + node_mass + fsum) * kMassSafety;
+
+            // ---- finite-difference prune (summation_engine.py:327-351)
+            const double fd_err = 0.5 * WR * (khi - klo);
+            const double req = required_tokens(WR, fd_err, A.eps, gmin, A.total_w);
+            unsigned fd_mask;
+            if (A.use_tokens) fd_mask = admit(act, req, tokens);
+            else fd_mask = __ballot_sync(kFull, act && req <= 0.0);
+            const bool fd = (fd_mask >> lane) & 1u;
+            c_fd += __popc(fd_mask);
+            double settled = 0.0, est_add = 0.0;
+            if (fd) {
+                const double dl = WR * klo, du = WR * khi - WR;
+                settled = dl;
+                est_add = 0.5 * (dl + du + WR);
+            }
+
+            // ---- series prunes (summation_engine.py:352-399); the evaluation
+            // itself is deferred to the end of the block (it never feeds a bound)
+            unsigned ser_mask = 0;
+            if (A.use_series && nser + 32 <= A.stack_cap) {
+                int meth = 0, p = 0;
+                double bound = 0.0;
+                if (act && !fd) {
+                    const double maxerr = A.eps * (WR + tokens) * gmin / A.total_w;
+                    const double r_ref = wr.y * A.inv_h;
+                    const double r_qu = A.qb_rad[b] * A.inv_h;
+                    const double rmin = r_ref < r_qu ? r_ref : r_qu;
+                    double possible = sqrt(khi) * WR * A.floor_c;
+                    if (rmin < 1.0) {
+                        double pw = 1.0;
+                        for (int k = 0; k < A.plimit; k++) pw *= rmin;
+                        possible *= pw;
+                    }
+                    if (possible <= maxerr)
+                        select_method_gpu(mn, r_ref, r_qu, WR, (double)ni.y, D, A.h, maxerr,
+                                          A.plimit, A.ct, A.cross, A.kp, meth, p, bound);
+                }
+                const bool cand = meth != 0;
+                const double sreq = cand ? required_tokens(WR, bound, A.eps, gmin, A.total_w)
+                                         : CUDART_INF;
+                ser_mask = admit(cand, sreq, tokens);
+                if ((ser_mask >> lane) & 1u) {
+                    settled = WR * klo;
+                    sl[nser + __popc(ser_mask & lt_mask)] = make_int2(node, p | (meth << 8));
+                }
+                nser += __popc(ser_mask);
+            }
+            node_mass += warp_sum(settled);
+            node_est += warp_sum(est_add);
+
+            // ---- descend or evaluate exactly (summation_engine.py:400-426)
+            const bool rem = act && !fd && !((ser_mask >> lane) & 1u);
+            const bool leafy = ni.z < 0 || ni.y <= A.ref_leaf;
+            unsigned split_mask = __ballot_sync(kFull, rem && !leafy);
+            unsigned base_mask = __ballot_sync(kFull, rem && leafy);
+            if (sp + 2 * __popc(split_mask) > A.stack_cap) {
+                // frontier capacity reached: settle these exactly (always admissible)
+                base_mask |= split_mask;
+                split_mask = 0;
+            }
+            double child_sum = 0.0;
+            if ((split_mask >> lane) & 1u) {
+                const int pos = sp + 2 * __popc(split_mask & lt_mask);
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    const int ch = c == 0 ? ni.z : ni.w;
+                    double cl, chh, cm;
+                    entry_bounds<D>(A, sq, ch, cl, chh, cm);
+                    sn[pos + c] = ch;
+                    skl[pos + c] = cl;
+                    skh[pos + c] = chh;
+                    smn[pos + c] = cm;
+                    child_sum += A.r_wr[ch].x * cl;
+                }
+            }
+            sp += 2 * __popc(split_mask);
+            fsum = fsum - batch_sum + warp_sum(child_sum);
+            if (fsum < 0.0) fsum = 0.0;
+
+            // ---- exhaustive base cases, eager (dito_base, :221-250)
+            for (unsigned m = base_mask; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const int rs = __shfl_sync(kFull, ni.x, i);
+                const int rc = __shfl_sync(kFull, ni.y, i);
+                const double wri = __shfl_sync(kFull, WR, i);
+                const double contrib = base_case<D>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv);
+                pt_est += contrib;
+                if (A.no_eager) node_mass += wri * __shfl_sync(kFull, klo, i);
+                else pt_mass += contrib;
+                if (A.use_tokens) tokens += wri;
+                c_base++;
+                c_pairs += (unsigned)(qn * rc);
+            }
+        }
+
+        // ---- deferred series contributions, then the post pass (dito_post, :253-281)
+        unsigned c_dh = 0, c_dl = 0, c_h2l = 0;
+        bool local_used = false;
+        if (nser > 0) {
+            double qc[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) qc[d] = sqc[d];
+            for (int i = 0; i < nser; i++) {
+                const int2 e = sl[i];
+                const int meth = e.y >> 8, p = e.y & 0xff;
+                if (meth == 2) {
+                    pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)e.x * D,
+                                               A.r_mom + (int64_t)e.x * A.mom_K, p, A.kp[p], A.sc,
+                                               A.digits);
+                    c_dh++;
+                } else if (meth == 3) {
+                    const int4 ni = A.r_ni[e.x];
+                    accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], A.sc,
+                                       A.digits, A.inv_fact, loc, false);
+                    local_used = true;
+                    c_dl++;
+                } else {
+                    h2l_warp_add<D>(A.r_mom + (int64_t)e.x * A.mom_K, A.r_c + (int64_t)e.x * D, qc,
+                                    p, A.kp[p], p, A.kp[p], A.sc, A.digits, A.inv_fact, A.degrees,
+                                    loc);
+                    local_used = true;
+                    c_h2l++;
+                }
+                __syncwarp();
+            }
+            if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, A.sc, A.digits);
+        }
+        const double val = pt_est + node_est;
+        if (valid) A.out[A.q_perm[qs + lane]] = val;
+        if (lane == 0 && A.dbg) {
+            A.dbg[4 * b + 0] = (unsigned long long)(clock64() - t_start);
+            A.dbg[4 * b + 1] = steps;
+            A.dbg[4 * b + 2] = c_vis;
+            A.dbg[4 * b + 3] = c_pairs;
+        }
+        if (lane == 0) {
+            atomicAdd(A.counters + 0, (unsigned long long)c_vis);
+            atomicAdd(A.counters + 1, (unsigned long long)c_base);
+            atomicAdd(A.counters + 2, (unsigned long long)c_fd);
+            atomicAdd(A.counters + 3, (unsigned long long)c_dh);
+            atomicAdd(A.counters + 4, (unsigned long long)c_dl);
+            atomicAdd(A.counters + 5, (unsigned long long)c_h2l);
+            atomicAdd(A.counters + 6, (unsigned long long)c_pairs);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace fg
