@@ -63,6 +63,82 @@ __device__ double eval_far_lane(const double (&x)[D], const double *__restrict__
     return acc;
 }
 
+// ---- compile-time graded-lex tables (kernel_math.py:111-136) ----------------
+__host__ __device__ constexpr int glex_count(int D, int P) {
+    // C(D+P-1, D)
+    long long r = 1;
+    for (int i = 1; i <= D; i++) r = r * (P - 1 + i) / i;
+    return (int)r;
+}
+
+__host__ __device__ constexpr int default_plimit_c(int D) {
+    return D == 1 ? 8 : D == 2 ? 8 : D == 3 ? 6 : D == 4 ? 4 : D == 5 ? 4 : D == 6 ? 2 : 1;
+}
+
+template <int D, int P>
+struct GLex {
+    static constexpr int K = glex_count(D, P);
+    int dig[K][D];
+    int prefix[P + 1];
+    constexpr GLex() : dig{}, prefix{} {
+        int k = 0;
+        for (int g = 0; g < P; g++) {
+            prefix[g] = k;
+            int a[D] = {};
+            a[0] = g;
+            for (;;) {
+                for (int d = 0; d < D; d++) dig[k][d] = a[d];
+                k++;
+                // previous composition in lexicographically descending order
+                int j = D - 2;
+                while (j >= 0 && a[j] == 0) j--;
+                if (j < 0) break;
+                int rest = 1;
+                for (int t = j + 1; t < D; t++) rest += a[t];
+                a[j] -= 1;
+                a[j + 1] = rest;
+                for (int t = j + 2; t < D; t++) a[t] = 0;
+            }
+        }
+        prefix[P] = k;
+    }
+};
+
+// EVALM with a compile-time index set: the ladders live in registers and every
+// product indexes them with constants.  Evaluates the order-p prefix (p <= P).
+template <int D, int P>
+__device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
+                                                 const double *__restrict__ c,
+                                                 const double *__restrict__ A, int p,
+                                                 double inv_sc) {
+    constexpr GLex<D, P> G;
+    double lad[D][P];
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double t = (x[d] - __ldg(c + d)) * inv_sc;
+        const double g = exp(-t * t);
+        lad[d][0] = g;
+        if (P > 1) lad[d][1] = 2.0 * t * g;
+#pragma unroll
+        for (int n = 1; n + 1 < P; n++) lad[d][n + 1] = 2.0 * t * lad[d][n] - 2.0 * n * lad[d][n - 1];
+    }
+    int kmax = G.K;  // coefficients of the order-p prefix
+#pragma unroll
+    for (int q = 1; q < P; q++)
+        if (q == p) kmax = G.prefix[q];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < G.K; k++) {
+        if (k < kmax) {
+            double v = lad[0][G.dig[k][0]];
+#pragma unroll
+            for (int d = 1; d < D; d++) v *= lad[d][G.dig[k][d]];
+            acc = fma(v, __ldg(A + k), acc);
+        }
+    }
+    return acc;
+}
+
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)
 template <int D>
 __device__ double eval_local_lane(const double (&x)[D], const double (&c)[D],

@@ -108,10 +108,10 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
 // Exact contribution of reference points [rs, rs+rc) to this lane's query
 // (_leaf_kernel_block, summation_engine.py:206-218): all lanes read the same
 // record (broadcast), two independent exp chains per step.
-template <int D>
+template <int D, bool CHECKED>
 __device__ __forceinline__ double base_case(const double (&x)[D],
                                             const double *__restrict__ rp, int rc,
-                                            double neg_inv) {
+                                            double neg_inv, const double *s_tab) {
     constexpr int S = packed_stride(D);
     double acc0 = 0.0, acc1 = 0.0;
     int j = 0;
@@ -127,8 +127,13 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             d0 = fma(f0, f0, d0);
             d1 = fma(f1, f1, d1);
         }
-        acc0 = fma(fg_exp(d0 * neg_inv), w0, acc0);
-        acc1 = fma(fg_exp(d1 * neg_inv), w1, acc1);
+        if (CHECKED) {
+            acc0 = fma(fg_exp_fast(d0 * neg_inv, s_tab), w0, acc0);
+            acc1 = fma(fg_exp_fast(d1 * neg_inv, s_tab), w1, acc1);
+        } else {
+            acc0 = fma(fg_exp_normal(d0 * neg_inv, s_tab), w0, acc0);
+            acc1 = fma(fg_exp_normal(d1 * neg_inv, s_tab), w1, acc1);
+        }
     }
     if (j < rc) {
         double y0[D], w0;
@@ -140,7 +145,8 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             const double f0 = x[d] - y0[d];
             d0 = fma(f0, f0, d0);
         }
-        acc0 = fma(fg_exp(d0 * neg_inv), w0, acc0);
+        acc0 = fma(CHECKED ? fg_exp_fast(d0 * neg_inv, s_tab) : fg_exp_normal(d0 * neg_inv, s_tab),
+                   w0, acc0);
     }
     return acc0 + acc1;
 }
@@ -150,6 +156,9 @@ __global__ void __launch_bounds__(kTravThreads, MINB)
 traverse_kernel(const TravArgs A) {
     constexpr int S = packed_stride(D);
     extern __shared__ double smem[];
+    __shared__ double s_tab[64];
+    exp_table_init(s_tab);
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kTravWarps + wib;
@@ -316,7 +325,13 @@ traverse_kernel(const TravArgs A) {
                 const int rs = __shfl_sync(kFull, ni.x, i);
                 const int rc = __shfl_sync(kFull, ni.y, i);
                 const double wri = __shfl_sync(kFull, WR, i);
-                const double contrib = base_case<D>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv);
+                // every pair of this item has K >= K_lo: skip the exp range test
+                // when K_lo is a normal number
+                const double kli = __shfl_sync(kFull, klo, i);
+                const double contrib =
+                    kli >= 2.3e-308
+                        ? base_case<D, false>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv, s_tab)
+                        : base_case<D, true>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv, s_tab);
                 pt_est += contrib;
                 if (A.no_eager) node_mass += wri * __shfl_sync(kFull, klo, i);
                 else pt_mass += contrib;
@@ -337,9 +352,15 @@ traverse_kernel(const TravArgs A) {
                 const int2 e = sl[i];
                 const int meth = e.y >> 8, p = e.y & 0xff;
                 if (meth == 2) {
-                    pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)e.x * D,
-                                               A.r_mom + (int64_t)e.x * A.mom_K, p, A.kp[p], A.sc,
-                                               A.digits);
+                    constexpr int PF = default_plimit_c(D);
+                    if (A.plimit == PF)
+                        pt_est += eval_far_fixed<D, PF>(x, A.r_c + (int64_t)e.x * D,
+                                                        A.r_mom + (int64_t)e.x * A.mom_K, p,
+                                                        1.0 / A.sc);
+                    else
+                        pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)e.x * D,
+                                                   A.r_mom + (int64_t)e.x * A.mom_K, p, A.kp[p],
+                                                   A.sc, A.digits);
                     c_dh++;
                 } else if (meth == 3) {
                     const int4 ni = A.r_ni[e.x];
