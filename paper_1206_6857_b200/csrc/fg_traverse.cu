@@ -264,7 +264,8 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         }
         A.floor_c = floor_c;
     }
-    smem = sizeof(double) * (3 * D + A.K) * kTravWarps;
+    // per warp: query box + centroid + local coefficients, then 2 x 32 staged points
+    smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 64 * packed_stride(D)) * kTravWarps;
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
     FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * 8));
     FG_CUDA_TRY(cudaMemsetAsync(g_scr.work.p, 0, sizeof(unsigned long long), stream()));

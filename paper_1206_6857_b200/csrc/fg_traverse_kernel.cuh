@@ -3,6 +3,8 @@
 // body evolve separately.
 #pragma once
 
+#include <cuda_pipeline.h>
+
 #include "fg_device.cuh"
 #include "fg_exp.cuh"
 #include "fg_internal.cuh"
@@ -108,6 +110,38 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
 // Exact contribution of reference points [rs, rs+rc) to this lane's query
 // (_leaf_kernel_block, summation_engine.py:206-218): all lanes read the same
 // record (broadcast), two independent exp chains per step.
+// Copy the points of base item `i` (lanes' (ni_x, ni_y) = start, count <= 32)
+// into a shared-memory buffer with cp.async; one commit group per call.
+template <int D>
+__device__ __forceinline__ void stage_points(const double *__restrict__ pw, int ni_x, int ni_y,
+                                             int i, double *buf) {
+    constexpr int S = packed_stride(D);
+    const int lane = threadIdx.x & 31;
+    const int rs = __shfl_sync(kFull, ni_x, i);
+    const int rc = __shfl_sync(kFull, ni_y, i);
+    if (lane < rc) {
+        const double *src = pw + (int64_t)(rs + lane) * S;
+        double *dst = buf + lane * S;
+#pragma unroll
+        for (int q = 0; q < S / 2; q++) __pipeline_memcpy_async(dst + 2 * q, src + 2 * q, 16);
+    }
+    __pipeline_commit();
+}
+
+template <int D>
+__device__ __forceinline__ void read_point_w(const double *rec, double (&x)[D], double &w) {
+    constexpr int S = packed_stride(D);
+    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+    for (int k = 0; k < S / 2; k++) {
+        const double2 v = r2[k];
+        if (2 * k < D) x[2 * k] = v.x;
+        else if (2 * k == D) w = v.x;
+        if (2 * k + 1 < D) x[2 * k + 1] = v.y;
+        else if (2 * k + 1 == D) w = v.y;
+    }
+}
+
 template <int D, bool CHECKED>
 __device__ __forceinline__ double base_case(const double (&x)[D],
                                             const double *__restrict__ rp, int rc,
@@ -117,8 +151,8 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
     int j = 0;
     for (; j + 1 < rc; j += 2) {
         double y0[D], y1[D], w0, w1;
-        load_point_w<D>(rp + (int64_t)j * S, y0, w0);
-        load_point_w<D>(rp + (int64_t)(j + 1) * S, y1, w1);
+        read_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        read_point_w<D>(rp + (int64_t)(j + 1) * S, y1, w1);
         const double e0 = x[0] - y0[0], e1 = x[0] - y1[0];
         double d0 = e0 * e0, d1 = e1 * e1;
 #pragma unroll
@@ -137,7 +171,7 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
     }
     if (j < rc) {
         double y0[D], w0;
-        load_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        read_point_w<D>(rp + (int64_t)j * S, y0, w0);
         const double e0 = x[0] - y0[0];
         double d0 = e0 * e0;
 #pragma unroll
@@ -163,9 +197,12 @@ traverse_kernel(const TravArgs A) {
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kTravWarps + wib;
     // per-warp shared memory: query box (lo, hi), centroid, local coefficients
-    double *sq = smem + wib * (3 * D + A.K);
+    // and a double buffer of 2 x 32 staged reference points
+    const int head = (3 * D + A.K + 1) & ~1;
+    double *sq = smem + wib * (head + 64 * S);
     double *sqc = sq + 2 * D;
     double *loc = sq + 3 * D;
+    double *sbuf = sq + head;
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;
@@ -319,7 +356,14 @@ traverse_kernel(const TravArgs A) {
             fsum = fsum - batch_sum + warp_sum(child_sum);
             if (fsum < 0.0) fsum = 0.0;
 
-            // ---- exhaustive base cases, eager (dito_base, :221-250)
+            // ---- exhaustive base cases, eager (dito_base, :221-250).  Reference
+            // leaves of <= 32 points are staged into shared memory with cp.async,
+            // double-buffered so the next item's points load while this one computes.
+            const unsigned small_mask = __ballot_sync(kFull, ni.y <= 32) & base_mask;
+            int bi = 0;
+            if (small_mask) {
+                stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(small_mask) - 1, sbuf);
+            }
             for (unsigned m = base_mask; m; m &= m - 1) {
                 const int i = __ffs(m) - 1;
                 const int rs = __shfl_sync(kFull, ni.x, i);
@@ -328,12 +372,27 @@ traverse_kernel(const TravArgs A) {
                 // every pair of this item has K >= K_lo: skip the exp range test
                 // when K_lo is a normal number
                 const double kli = __shfl_sync(kFull, klo, i);
-                const double contrib =
-                    kli >= 2.3e-308
-                        ? base_case<D, false>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv, s_tab)
-                        : base_case<D, true>(x, A.r_pw + (int64_t)rs * S, rc, A.neg_inv, s_tab);
+                double contrib;
+                if ((small_mask >> i) & 1u) {
+                    const unsigned rest = small_mask & ~((2u << i) - 1u);
+                    if (rest) {
+                        stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1, sbuf + (bi ^ 1) * 32 * S);
+                        __pipeline_wait_prior(1);
+                    } else {
+                        __pipeline_wait_prior(0);
+                    }
+                    __syncwarp();
+                    const double *bp = sbuf + bi * 32 * S;
+                    contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, A.neg_inv, s_tab)
+                                              : base_case<D, true>(x, bp, rc, A.neg_inv, s_tab);
+                    __syncwarp();
+                    bi ^= 1;
+                } else {
+                    const double *rp = A.r_pw + (int64_t)rs * S;
+                    contrib = base_case<D, true>(x, rp, rc, A.neg_inv, s_tab);
+                }
                 pt_est += contrib;
-                if (A.no_eager) node_mass += wri * __shfl_sync(kFull, klo, i);
+                if (A.no_eager) node_mass += wri * kli;
                 else pt_mass += contrib;
                 if (A.use_tokens) tokens += wri;
                 c_base++;
