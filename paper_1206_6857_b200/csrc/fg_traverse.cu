@@ -244,6 +244,10 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     A.plimit = plimit;
     A.ref_leaf = g_ref_leaf;
     A.stack_cap = g_stack_cap;
+    {
+        const char *env = getenv("FG_BFS_CAP");
+        A.bfs_cap = env ? atoi(env) : g_stack_cap / 4;
+    }
     size_t smem = 0;
     if (series) {
         int st = FG_OK;

@@ -49,6 +49,7 @@ struct TravArgs {
     double *st_f;
     int2 *ser_list;
     int stack_cap;
+    int bfs_cap;  // breadth-first while the frontier holds <= bfs_cap entries
     unsigned long long *work;
     unsigned long long *counters;  // 7 counters
     unsigned long long *dbg;       // optional per-block (cycles, steps, visits, pairs)
@@ -239,7 +240,13 @@ traverse_kernel(const TravArgs A) {
 
         // root entry
         double fsum;  // sum over the frontier of W_R * K_lo
-        int sp = 1;
+        // Frontier: circular buffer [head, head + cnt) of capacity stack_cap.
+        // Breadth-first (pop the oldest entries) while it holds fewer than
+        // bfs_cap entries, so the frontier's K_lo bound tightens everywhere
+        // before any region is explored to the leaves; depth-first (pop the
+        // newest) beyond that, which bounds its size.
+        int head = 0, cnt = 1;
+        const int cap = A.stack_cap;
         {
             double klo, khi, mn;
             entry_bounds<D>(A, sq, 0, klo, khi, mn);
@@ -253,21 +260,30 @@ traverse_kernel(const TravArgs A) {
         }
         __syncwarp();
 
-        while (sp > 0) {
-            const int nb = min(sp, 32);
+        while (cnt > 0) {
+            const int nb = min(cnt, 32);
             steps++;
-            const int base = sp - nb;
-            sp = base;
+            int base;
+            if (cnt <= A.bfs_cap) {
+                base = head;
+                head = head + nb >= cap ? head + nb - cap : head + nb;
+            } else {
+                base = head + cnt - nb;
+                if (base >= cap) base -= cap;
+            }
+            cnt -= nb;
             const bool act = lane < nb;
             int node = 0;
             double klo = 0.0, khi = 0.0, mn = 0.0;
             int4 ni = make_int4(0, 0, -1, -1);
             double2 wr = make_double2(0.0, 0.0);
             if (act) {
-                node = sn[base + lane];
-                klo = skl[base + lane];
-                khi = skh[base + lane];
-                mn = smn[base + lane];
+                int slot = base + lane;
+                if (slot >= cap) slot -= cap;
+                node = sn[slot];
+                klo = skl[slot];
+                khi = skh[slot];
+                mn = smn[slot];
                 ni = A.r_ni[node];
                 wr = A.r_wr[node];
             }
@@ -332,27 +348,30 @@ traverse_kernel(const TravArgs A) {
             const bool leafy = ni.z < 0 || ni.y <= A.ref_leaf;
             unsigned split_mask = __ballot_sync(kFull, rem && !leafy);
             unsigned base_mask = __ballot_sync(kFull, rem && leafy);
-            if (sp + 2 * __popc(split_mask) > A.stack_cap) {
+            if (cnt + 2 * __popc(split_mask) > cap) {
                 // frontier capacity reached: settle these exactly (always admissible)
                 base_mask |= split_mask;
                 split_mask = 0;
             }
             double child_sum = 0.0;
             if ((split_mask >> lane) & 1u) {
-                const int pos = sp + 2 * __popc(split_mask & lt_mask);
+                const int pos = head + cnt + 2 * __popc(split_mask & lt_mask);
 #pragma unroll
                 for (int c = 0; c < 2; c++) {
                     const int ch = c == 0 ? ni.z : ni.w;
                     double cl, chh, cm;
                     entry_bounds<D>(A, sq, ch, cl, chh, cm);
-                    sn[pos + c] = ch;
-                    skl[pos + c] = cl;
-                    skh[pos + c] = chh;
-                    smn[pos + c] = cm;
+                    int slot = pos + c;
+                    if (slot >= cap) slot -= cap;
+                    if (slot >= cap) slot -= cap;
+                    sn[slot] = ch;
+                    skl[slot] = cl;
+                    skh[slot] = chh;
+                    smn[slot] = cm;
                     child_sum += A.r_wr[ch].x * cl;
                 }
             }
-            sp += 2 * __popc(split_mask);
+            cnt += 2 * __popc(split_mask);
             fsum = fsum - batch_sum + warp_sum(child_sum);
             if (fsum < 0.0) fsum = 0.0;
 
