@@ -422,8 +422,10 @@ int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
 
 int fg_moments_refresh(fg_tree *tree, double h, int32_t plimit) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    // stream-ordered: later engine calls on the same stream see the moments;
+    // errors of the asynchronous work surface at the next synchronising call
     FG_TRY(moments_refresh(tree->t, h, plimit));
-    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    FG_CUDA_TRY(cudaGetLastError());
     return FG_OK;
 }
 

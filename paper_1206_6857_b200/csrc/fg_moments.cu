@@ -82,6 +82,11 @@ __global__ void moments_h2h_kernel(int64_t node_begin, int64_t node_end,
     }
 }
 
+__global__ void rescale_factors_kernel(int K, double ratio, const int *__restrict__ degrees,
+                                       double *__restrict__ fac) {
+    for (int k = threadIdx.x; k < K; k += blockDim.x) fac[k] = pow(ratio, (double)degrees[k]);
+}
+
 __global__ void moments_rescale_kernel(int64_t total, int K, const double *__restrict__ src,
                                        const double *__restrict__ fac, double *__restrict__ dst) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -131,19 +136,15 @@ int moments_refresh(TreeDev &t, double h, int plimit) {
     const int64_t total = t.nnodes * K;
     FG_TRY(t.mom.reserve(sizeof(double) * total));
     if (t.mom0_valid && t.mom_K == K && t.mom_order == plimit) {
-        // exact rescaling from the base bandwidth
-        std::vector<double> fac(K);
-        const double ratio = t.mom0_h / h;
-        for (int k = 0; k < K; k++) fac[k] = std::pow(ratio, (double)T->h_degrees[k]);
+        // exact rescaling from the base bandwidth: (h0/h)^{|a|} per coefficient
         FG_TRY(g_rescale_fac.reserve(sizeof(double) * K));
-        FG_CUDA_TRY(cudaMemcpyAsync(g_rescale_fac.p, fac.data(), sizeof(double) * K,
-                                    cudaMemcpyHostToDevice, stream()));
+        count_launch();
+        rescale_factors_kernel<<<1, 256, 0, stream()>>>(K, t.mom0_h / h, T->degrees.as<int>(),
+                                                        g_rescale_fac.as<double>());
         count_launch();
         moments_rescale_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream()>>>(
             total, K, t.mom0.as<double>(), g_rescale_fac.as<double>(), t.mom.as<double>());
         FG_CUDA_TRY(cudaGetLastError());
-        // the host copy of `fac` must outlive the async copy
-        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     } else {
         FG_TRY(t.mom0.reserve(sizeof(double) * total));
         switch (t.dim) {

@@ -148,14 +148,13 @@ int query_blocks(TreeDev &t) {
 
 // ---------------------------------------------------------------- launch
 struct TravScratch {
-    DBuf st_node, st_f, ser, work, counters, dbg;
+    DBuf st_node, st_f, ser, work, counters, dbg, prime;
     int grid = 0, cap = 0;
 };
 static TravScratch g_scr;
 
 template <int D>
-static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks, cudaEvent_t e0,
-                           cudaEvent_t e1) {
+static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     auto kern = traverse_kernel<D, 4>;
     if (D == 3) {
         const char *env = getenv("FG_TRAV_MINB");
@@ -165,15 +164,26 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks, cudaEvent_
         if (mb == 8) kern = traverse_kernel<D, 8>;
         if (mb == 1) kern = traverse_kernel<D, 1>;
     }
-    if (smem > 48 * 1024)
-        FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-    int dev = 0, sms = 0, occ = 0;
+    // resident-grid size, cached per (kernel, shared memory size)
+    static thread_local const void *c_kern = nullptr;
+    static thread_local size_t c_smem = 0;
+    static thread_local int c_dev = -1, c_full = 0;
+    int dev = 0;
     FG_CUDA_TRY(cudaGetDevice(&dev));
-    FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTravThreads, smem));
-    if (occ < 1) occ = 1;
-    int64_t grid = (int64_t)sms * occ;
+    if (c_kern != (const void *)kern || c_smem != smem || c_dev != dev) {
+        if (smem > 48 * 1024)
+            FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+        int sms = 0, occ = 0;
+        FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        FG_CUDA_TRY(
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTravThreads, smem));
+        c_full = sms * (occ < 1 ? 1 : occ);
+        c_kern = (const void *)kern;
+        c_smem = smem;
+        c_dev = dev;
+    }
+    int64_t grid = c_full;
     const int64_t need = (nblocks + kTravWarps - 1) / kTravWarps;
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
@@ -189,13 +199,32 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks, cudaEvent_
     A.st_node = g_scr.st_node.as<int>();
     A.st_f = g_scr.st_f.as<double>();
     A.ser_list = g_scr.ser.as<int2>();
-    FG_CUDA_TRY(cudaEventRecord(e0, stream()));
+    FG_CUDA_TRY(cudaMemsetAsync(A.work, 0, sizeof(unsigned long long), stream()));
     count_launch();
     kern<<<(unsigned)grid, kTravThreads, smem, stream()>>>(A);
     FG_CUDA_TRY(cudaGetLastError());
-    FG_CUDA_TRY(cudaEventRecord(e1, stream()));
     return FG_OK;
 }
+
+static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
+    switch (D) {
+        case 1: return launch_traverse<1>(A, smem, nb);
+        case 2: return launch_traverse<2>(A, smem, nb);
+        case 3: return launch_traverse<3>(A, smem, nb);
+        case 4: return launch_traverse<4>(A, smem, nb);
+        case 5: return launch_traverse<5>(A, smem, nb);
+        case 6: return launch_traverse<6>(A, smem, nb);
+        case 7: return launch_traverse<7>(A, smem, nb);
+        case 8: return launch_traverse<8>(A, smem, nb);
+        default: return FG_EUNSUPPORTED;
+    }
+}
+
+// Priming pass: a coarse run at eps1 gives estimates with
+// |est - G| <= eps1 G, hence G >= est / (1 + eps1) for every query.  The
+// per-block minimum of that bound primes the mass lower bound of the real run
+// (used as max(accumulated, primed)).  0 disables.
+double g_prime_eps = 0.0;
 
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
                   int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
@@ -272,7 +301,6 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 64 * packed_stride(D)) * kTravWarps;
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
     FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * 8));
-    FG_CUDA_TRY(cudaMemsetAsync(g_scr.work.p, 0, sizeof(unsigned long long), stream()));
     FG_CUDA_TRY(cudaMemsetAsync(g_scr.counters.p, 0, sizeof(unsigned long long) * 8, stream()));
     A.work = g_scr.work.as<unsigned long long>();
     A.no_eager = getenv("FG_NO_EAGER") ? 1 : 0;
@@ -282,31 +310,36 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         A.dbg = g_scr.dbg.as<unsigned long long>();
     }
     A.counters = g_scr.counters.as<unsigned long long>();
-    cudaEvent_t e0, e1;
-    FG_CUDA_TRY(cudaEventCreate(&e0));
-    FG_CUDA_TRY(cudaEventCreate(&e1));
+    // timing events and the pinned counter buffer are created once per thread
+    static thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
+    static thread_local unsigned long long *cnt = nullptr;
+    if (!e0) {
+        FG_CUDA_TRY(cudaEventCreate(&e0));
+        FG_CUDA_TRY(cudaEventCreate(&e1));
+        FG_CUDA_TRY(cudaMallocHost(&cnt, sizeof(unsigned long long) * 8));
+    }
     int st = FG_OK;
     const int64_t nb = b1 > b0 ? (b1 - b0 + A.stride - 1) / A.stride : 0;
-    if (nb > 0) {
-        switch (D) {
-            case 1: st = launch_traverse<1>(A, smem, nb, e0, e1); break;
-            case 2: st = launch_traverse<2>(A, smem, nb, e0, e1); break;
-            case 3: st = launch_traverse<3>(A, smem, nb, e0, e1); break;
-            case 4: st = launch_traverse<4>(A, smem, nb, e0, e1); break;
-            case 5: st = launch_traverse<5>(A, smem, nb, e0, e1); break;
-            case 6: st = launch_traverse<6>(A, smem, nb, e0, e1); break;
-            case 7: st = launch_traverse<7>(A, smem, nb, e0, e1); break;
-            case 8: st = launch_traverse<8>(A, smem, nb, e0, e1); break;
-            default: st = FG_EUNSUPPORTED;
+    double prime_eps = g_prime_eps;
+    if (const char *env = getenv("FG_PRIME_EPS")) prime_eps = atof(env);
+    cudaEventRecord(e0, stream());
+    if (nb > 0 && prime_eps > eps && eps > 0.0) {
+        st = g_scr.prime.reserve(sizeof(double) * q.nqb);
+        if (st == FG_OK) {
+            TravArgs A1 = A;
+            A1.eps = prime_eps;
+            A1.prime_out = g_scr.prime.as<double>();
+            A1.prime_scale = kMassSafety / (1.0 + prime_eps);
+            st = launch_dispatch(D, A1, smem, nb);
+            A.prime_in = g_scr.prime.as<double>();
         }
-    } else {
-        cudaEventRecord(e0, stream());
-        cudaEventRecord(e1, stream());
     }
+    if (st == FG_OK && nb > 0) st = launch_dispatch(D, A, smem, nb);
+    cudaEventRecord(e1, stream());
     const char *dbg_path = getenv("FG_DEBUG_BLOCKS");
-    unsigned long long cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < 8; k++) cnt[k] = 0;
     if (st == FG_OK) {
-        cudaError_t e = cudaMemcpyAsync(cnt, g_scr.counters.p, sizeof(cnt),
+        cudaError_t e = cudaMemcpyAsync(cnt, g_scr.counters.p, sizeof(unsigned long long) * 8,
                                         cudaMemcpyDeviceToHost, stream());
         if (e == cudaSuccess) e = cudaStreamSynchronize(stream());
         if (e != cudaSuccess) {
@@ -319,8 +352,6 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         cudaEventElapsedTime(&ms, e0, e1);
         *seconds = ms * 1e-3;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     FG_TRY(st);
     if (dbg_path && A.dbg) {
         std::vector<unsigned long long> hd(4 * q.nqb);

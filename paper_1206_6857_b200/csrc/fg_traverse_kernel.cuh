@@ -54,6 +54,9 @@ struct TravArgs {
     unsigned long long *counters;  // 7 counters
     unsigned long long *dbg;       // optional per-block (cycles, steps, visits, pairs)
     int no_eager;                  // experiment: credit base cases with K_lo only
+    const double *prime_in;        // per-block primed lower bound on G (or null)
+    double *prime_out;             // coarse pass: write per-block bound instead of values
+    double prime_scale;            // safety / (1 + eps1)
 };
 
 // Admit candidates in lane order under the token rule.  Unconditional
@@ -233,6 +236,9 @@ traverse_kernel(const TravArgs A) {
 #pragma unroll
             for (int d = 0; d < D; d++) x[d] = sqc[d];
         }
+        // primed lower bound on G over the block (a coarse pass's estimates
+        // divided by 1 + its epsilon); used as max(accumulated, primed) only
+        const double gprime = A.prime_in ? A.prime_in[b] : 0.0;
         double pt_est = 0.0, pt_mass = 0.0;                    // per point
         double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0;
@@ -292,7 +298,7 @@ traverse_kernel(const TravArgs A) {
             c_vis += nb;
             const double batch_sum = warp_sum(act ? WR * klo : 0.0);
             const double pmin = warp_min(valid ? pt_mass : CUDART_INF);
-            const double gmin = (pmin + node_mass + fsum) * kMassSafety;
+            const double gmin = fmax((pmin + node_mass + fsum) * kMassSafety, gprime);
 
             // ---- finite-difference prune (summation_engine.py:327-351)
             const double fd_err = 0.5 * WR * (khi - klo);
@@ -458,7 +464,13 @@ traverse_kernel(const TravArgs A) {
             if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, A.sc, A.digits);
         }
         const double val = pt_est + node_est;
-        if (valid) A.out[A.q_perm[qs + lane]] = val;
+        if (A.prime_out) {
+            // |val - G| <= eps1 G  =>  G >= val / (1 + eps1) for every query
+            const double m = warp_min(valid ? val : CUDART_INF);
+            if (lane == 0) A.prime_out[b] = m * A.prime_scale;
+        } else if (valid) {
+            A.out[A.q_perm[qs + lane]] = val;
+        }
         if (lane == 0 && A.dbg) {
             A.dbg[4 * b + 0] = (unsigned long long)(clock64() - t_start);
             A.dbg[4 * b + 1] = steps;

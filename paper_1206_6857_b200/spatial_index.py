@@ -127,7 +127,25 @@ class KdTree:
         self._moments = None
         self.q_mass_lo = None
         self.q_mass_hi = None
-        self.q_est = None
+        self._q_est = None
+        self._run_values = None
+
+    @property
+    def q_est(self):
+        """Per-point estimates in tree order (the reference's q_est), built lazily
+        from the last run's values."""
+        if self._q_est is None and self._run_values is not None:
+            self._q_est = np.asarray(self._run_values)[self.perm]
+        return self._q_est
+
+    @q_est.setter
+    def q_est(self, value):
+        self._q_est = value
+        self._run_values = None
+
+    def _set_run_values(self, values):
+        self._run_values = values
+        self._q_est = None
 
     def __del__(self):
         h = getattr(self, "_h", None)

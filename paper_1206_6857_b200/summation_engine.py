@@ -139,7 +139,7 @@ def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: s
                   float(config.epsilon), _lib.MODES[mode], int(plimit), int(b0), int(b1),
                   int(stride), _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
     if out is None:
-        qtree.q_est = vals[qtree.perm]
+        qtree._set_run_values(vals)
     return ResultVector(vals, secs.value, TraversalCounters._from_c(cnt), None)
 
 
