@@ -151,8 +151,36 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
                                             const double *__restrict__ rp, int rc,
                                             double neg_inv, const double *s_tab) {
     constexpr int S = packed_stride(D);
-    double acc0 = 0.0, acc1 = 0.0;
+    constexpr int U = CHECKED ? 2 : 4;  // independent exp chains per step
+    double acc[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) acc[u] = 0.0;
     int j = 0;
+    for (; j + U - 1 < rc; j += U) {
+        double y[U][D], w[U], d2[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) read_point_w<D>(rp + (int64_t)(j + u) * S, y[u], w[u]);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const double e = x[0] - y[u][0];
+            d2[u] = e * e;
+        }
+#pragma unroll
+        for (int d = 1; d < D; d++)
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const double f = x[d] - y[u][d];
+                d2[u] = fma(f, f, d2[u]);
+            }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            acc[u] = fma(CHECKED ? fg_exp_fast(d2[u] * neg_inv, s_tab)
+                                 : fg_exp_normal(d2[u] * neg_inv, s_tab),
+                         w[u], acc[u]);
+    }
+    double acc0 = acc[0], acc1 = acc[1];
+#pragma unroll
+    for (int u = 2; u < U; u++) acc0 += acc[u];
     for (; j + 1 < rc; j += 2) {
         double y0[D], y1[D], w0, w1;
         read_point_w<D>(rp + (int64_t)j * S, y0, w0);
@@ -165,13 +193,10 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             d0 = fma(f0, f0, d0);
             d1 = fma(f1, f1, d1);
         }
-        if (CHECKED) {
-            acc0 = fma(fg_exp_fast(d0 * neg_inv, s_tab), w0, acc0);
-            acc1 = fma(fg_exp_fast(d1 * neg_inv, s_tab), w1, acc1);
-        } else {
-            acc0 = fma(fg_exp_normal(d0 * neg_inv, s_tab), w0, acc0);
-            acc1 = fma(fg_exp_normal(d1 * neg_inv, s_tab), w1, acc1);
-        }
+        acc0 = fma(CHECKED ? fg_exp_fast(d0 * neg_inv, s_tab) : fg_exp_normal(d0 * neg_inv, s_tab),
+                   w0, acc0);
+        acc1 = fma(CHECKED ? fg_exp_fast(d1 * neg_inv, s_tab) : fg_exp_normal(d1 * neg_inv, s_tab),
+                   w1, acc1);
     }
     if (j < rc) {
         double y0[D], w0;
