@@ -81,18 +81,18 @@ __device__ __forceinline__ unsigned admit(bool cand, double req, double &tokens)
 }
 
 // _required_tokens (summation_engine.py:157-173)
-__device__ __forceinline__ double required_tokens(double wr, double err, double eps,
-                                                  double gmin, double total_w) {
+// scale = W / (eps G_min), or +inf when eps G_min <= 0 (no inexact prune)
+__device__ __forceinline__ double required_tokens(double wr, double err, double scale) {
     if (err <= 0.0) return -wr;
-    const double den = eps * gmin;
-    return den > 0.0 ? total_w * err / den - wr : CUDART_INF;
+    return scale < CUDART_INF ? err * scale - wr : CUDART_INF;
 }
 
 // Box bounds of (query block box in shared memory, reference node) and both
 // kernel bounds (summation_engine.py:315-328).
 template <int D>
 __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq, int node,
-                                             double &klo, double &khi, double &mn) {
+                                             double &klo, double &khi, double &mn,
+                                             const double *s_tab) {
     const double *rbox = A.r_box + (int64_t)node * 2 * D;
     double mx = 0.0;
     mn = 0.0;
@@ -107,8 +107,8 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
         const double s = s1 > s2 ? s1 : s2;
         mx += s * s;
     }
-    khi = exp(mn * A.neg_inv);
-    klo = exp(mx * A.neg_inv);
+    khi = fg_exp_fast(mn * A.neg_inv, s_tab);
+    klo = fg_exp_fast(mx * A.neg_inv, s_tab);
 }
 
 // Exact contribution of reference points [rs, rs+rc) to this lane's query
@@ -280,7 +280,7 @@ traverse_kernel(const TravArgs A) {
         const int cap = A.stack_cap;
         {
             double klo, khi, mn;
-            entry_bounds<D>(A, sq, 0, klo, khi, mn);
+            entry_bounds<D>(A, sq, 0, klo, khi, mn, s_tab);
             if (lane == 0) {
                 sn[0] = 0;
                 skl[0] = klo;
@@ -327,7 +327,11 @@ traverse_kernel(const TravArgs A) {
 
             // ---- finite-difference prune (summation_engine.py:327-351)
             const double fd_err = 0.5 * WR * (khi - klo);
-            const double req = required_tokens(WR, fd_err, A.eps, gmin, A.total_w);
+            // W / (eps G_min): one uniform division per step instead of one per entry
+            const double den = A.eps * gmin;
+            const double tok_scale = den > 0.0 ? A.total_w / den : CUDART_INF;
+            const double err_scale = den / A.total_w;  // eps G_min / W
+            const double req = required_tokens(WR, fd_err, tok_scale);
             unsigned fd_mask;
             if (A.use_tokens) fd_mask = admit(act, req, tokens);
             else fd_mask = __ballot_sync(kFull, act && req <= 0.0);
@@ -347,7 +351,7 @@ traverse_kernel(const TravArgs A) {
                 int meth = 0, p = 0;
                 double bound = 0.0;
                 if (act && !fd) {
-                    const double maxerr = A.eps * (WR + tokens) * gmin / A.total_w;
+                    const double maxerr = (WR + tokens) * err_scale;
                     const double r_ref = wr.y * A.inv_h;
                     const double r_qu = A.qb_rad[b] * A.inv_h;
                     const double rmin = r_ref < r_qu ? r_ref : r_qu;
@@ -362,7 +366,7 @@ traverse_kernel(const TravArgs A) {
                                           A.plimit, A.ct, A.cross, A.kp, meth, p, bound);
                 }
                 const bool cand = meth != 0;
-                const double sreq = cand ? required_tokens(WR, bound, A.eps, gmin, A.total_w)
+                const double sreq = cand ? required_tokens(WR, bound, tok_scale)
                                          : CUDART_INF;
                 ser_mask = admit(cand, sreq, tokens);
                 if ((ser_mask >> lane) & 1u) {
@@ -387,11 +391,11 @@ traverse_kernel(const TravArgs A) {
             double child_sum = 0.0;
             if ((split_mask >> lane) & 1u) {
                 const int pos = head + cnt + 2 * __popc(split_mask & lt_mask);
-#pragma unroll
+#pragma unroll 1
                 for (int c = 0; c < 2; c++) {
                     const int ch = c == 0 ? ni.z : ni.w;
                     double cl, chh, cm;
-                    entry_bounds<D>(A, sq, ch, cl, chh, cm);
+                    entry_bounds<D>(A, sq, ch, cl, chh, cm, s_tab);
                     int slot = pos + c;
                     if (slot >= cap) slot -= cap;
                     if (slot >= cap) slot -= cap;
