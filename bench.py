@@ -121,6 +121,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic():
+    """dram read+write bytes per launch of the dominant kernel, from the
+    committed `ncu --set full` summary (profiles/, one C2 h=0.1126 launch of
+    this same bench command).  Null when no summary is present."""
+    import glob
+    import re
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traverse_kernel_full.txt")))
+    if not files:
+        return None
+    txt = open(files[-1]).read()
+    tot = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        m = re.search(key + r"\s+([\d.]+)\s+(\w*byte)", txt)
+        if not m:
+            return None
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[m.group(2)]
+        tot += float(m.group(1)) * scale
+    return {"bytes_per_launch": tot, "source": os.path.basename(files[-1]),
+            "launch": "C2 bandwidth index 6 (h=0.1126)"}
+
+
 # ------------------------------------------------------------ CPU side
 def cpu_sample(wl, target_seconds, threads):
     """Bounded sample of the workload on the host with the oracle port of the
@@ -208,7 +230,7 @@ def run_ours(args):
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200 import _lib
     from paper_1206_6857_b200.spatial_index import build_tree_device
-    from paper_1206_6857_b200.summation_engine import query_block_count, run_blocks
+    from paper_1206_6857_b200.distributed import run_sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -235,21 +257,19 @@ def run_ours(args):
     def step(record=True):
         vals_d.zero_()
         tree = build_tree_device(pts_d, w_d, 25)
-        nb = query_block_count(tree)
         for j, h in enumerate(wl.bandwidths):
             tree.refresh_moments(h, pl)
             cfg = fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, algorithm="dito")
             if world == 1:
                 res = fg.dito_run(cfg, tree, tree, out=vals_d[j])
             else:
-                res = run_blocks(cfg, tree, tree, rank, nb, world, out=vals_d[j])
+                # this rank's query blocks, then the gather (NCCL all-reduce over
+                # disjoint supports) -- inside the timed step
+                res = run_sharded(cfg, tree, tree, vals_d[j], rank, world)
             if record:
                 stats["kernel_s"] += res.seconds
                 stats["pairs"] += res.counters.exact_pairs
                 stats["visits"] += res.counters.pair_visits
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(vals_d)
         del tree
 
     with torch.cuda.stream(stream):
@@ -288,7 +308,8 @@ def run_ours(args):
     peak_tf = float(peak[0])
     achieved_tf = stats["pairs"] * F_OF_D[D] / stats["kernel_s"] / 1e12 if stats["kernel_s"] else 0.0
     roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak_tf if peak_tf else None, "traffic": None,
+                "frac": achieved_tf / peak_tf if peak_tf else None,
+                "traffic": profiled_traffic(),
                 "kernel": "traverse_kernel<3> (fused traversal + exact base cases)",
                 "flops_per_pair": F_OF_D[D],
                 "kernel_share_of_step": stats["kernel_s"] / total if total else None,

@@ -1,0 +1,105 @@
+"""Callers of the hot path: the parity metric, the LSCV score
+that Config 4 measures, and least-squares cross-validation bandwidth selection,
+all running their kernel sums on the device engine.
+
+Restates cli_harness.py:101-157 (select_bandwidth + score) and :216-226
+(max_rel_error).  The score arithmetic on the two sums is O(n) host work, as in
+the reference; the sums themselves are device runs.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .spatial_index import KdTree, PointStore, build_tree
+from .summation_engine import RunConfig, dfd_run, dfdo_run, dito_run
+
+
+def max_rel_error(estimates, exact) -> float:
+    """max_q |est - exact| / exact, exact zeros must be matched (cli_harness.py:216-226)."""
+    exact = np.asarray(exact, dtype=float)
+    estimates = np.asarray(estimates, dtype=float)
+    err = np.zeros_like(exact)
+    pos = exact > 0.0
+    err[pos] = np.abs(estimates[pos] - exact[pos]) / exact[pos]
+    if np.any(~pos & (estimates != 0.0)):
+        return float("inf")
+    return float(err.max()) if err.size else 0.0
+
+
+_RUNS = {"dfd": dfd_run, "dfdo": dfdo_run, "dito": dito_run}
+
+
+def lscv_score(tree: KdTree, h: float, epsilon: float = 1e-3, algorithm: str = "dfd") -> float:
+    """LSCV score of a Gaussian KDE with unit weights (cli_harness.py:128-137):
+
+        (2 pi 2h^2)^(-D/2) sum G_{sqrt2 h} / n^2
+          - 2 (2 pi h^2)^(-D/2) (sum G_h - n) / (n (n-1))
+
+    from two monochromatic device runs (the self term is removed by `- n`).
+    """
+    n, dim = tree.n, tree.dim
+    run = _RUNS[algorithm]
+    vals = []
+    for hh in (math.sqrt(2.0) * h, h):
+        if algorithm == "dito":
+            tree.refresh_moments(hh, _default_plimit(dim))
+        vals.append(run(RunConfig(bandwidth=hh, epsilon=epsilon, algorithm=algorithm),
+                        tree, tree).values)
+    conv, near = vals
+    norm_conv = (2.0 * math.pi * 2.0 * h * h) ** (-0.5 * dim)
+    norm_near = (2.0 * math.pi * h * h) ** (-0.5 * dim)
+    integral_sq = norm_conv * float(conv.sum()) / (n * n)
+    leave_one_out = norm_near * 2.0 * float(near.sum() - n) / (n * (n - 1))
+    return integral_sq - leave_one_out
+
+
+def _default_plimit(dim):
+    from .spatial_index import default_plimit
+
+    return default_plimit(dim)
+
+
+def select_bandwidth(points, seed: int = 0, epsilon: float = 1e-3, max_points: int = 2000,
+                     algorithm: str = "dfd") -> float:
+    """LSCV bandwidth: 14-point geometric grid over [1e-3, 0.5] x diameter, then a
+    golden-section search in log h down to width 0.02 (cli_harness.py:101-157)."""
+    points = np.asarray(points, dtype=float)
+    if points.ndim == 1:
+        points = points.reshape(-1, 1)
+    if points.shape[0] < 2:
+        raise ValueError("bandwidth selection needs at least two points")
+    lo = points.min(axis=0)
+    hi = points.max(axis=0)
+    if np.all(hi == lo):
+        raise ValueError("all points identical; no finite bandwidth minimizes LSCV")
+    if points.shape[0] > max_points:
+        idx = np.random.default_rng(seed).choice(points.shape[0], max_points, replace=False)
+        points = points[idx]
+    scale = float(np.linalg.norm(hi - lo))
+    tree = build_tree(PointStore(points))
+
+    def score(h):
+        return lscv_score(tree, h, epsilon, algorithm)
+
+    grid = np.geomspace(1e-3 * scale, 0.5 * scale, 14)
+    scores = [score(h) for h in grid]
+    best = int(np.argmin(scores))
+    a = math.log(grid[max(best - 1, 0)])
+    b = math.log(grid[min(best + 1, len(grid) - 1)])
+    invphi = 0.5 * (math.sqrt(5.0) - 1.0)
+    c = b - invphi * (b - a)
+    d = a + invphi * (b - a)
+    fc, fd = score(math.exp(c)), score(math.exp(d))
+    while b - a > 0.02:
+        if fc < fd:
+            b, d, fd = d, c, fc
+            c = b - invphi * (b - a)
+            fc = score(math.exp(c))
+        else:
+            a, c, fc = c, d, fd
+            d = a + invphi * (b - a)
+            fd = score(math.exp(d))
+    return math.exp(0.5 * (a + b))

@@ -216,12 +216,48 @@ def make_bounds():
                         floor=np.array(floor))
 
 
+def make_lscv():
+    """LSCV selection (cli_harness.py:101-157) and exact scores on seeded data."""
+    from fastgauss.cli_harness import select_bandwidth
+
+    rng = np.random.default_rng(12)
+    rec = {}
+    for D, n in ((2, 1500), (3, 1200)):
+        means = rng.uniform(0, 1, (3, D))
+        pts = means[rng.integers(0, 3, n)] + 0.08 * rng.standard_normal((n, D))
+        h_sel = select_bandwidth(pts, seed=0)
+        hs = np.geomspace(0.01, 0.3, 5)
+        exact = []
+        for h in hs:
+            conv = fg.naive_sum(pts, pts, np.ones(n), np.sqrt(2.0) * h).values
+            near = fg.naive_sum(pts, pts, np.ones(n), h).values
+            nc = (2 * np.pi * 2 * h * h) ** (-0.5 * D)
+            nn = (2 * np.pi * h * h) ** (-0.5 * D)
+            exact.append([nc * conv.sum() / n ** 2, 2 * nn * (near.sum() - n) / (n * (n - 1))])
+        rec[f"D{D}_points"] = pts
+        rec[f"D{D}_h_select"] = np.float64(h_sel)
+        rec[f"D{D}_hs"] = hs
+        rec[f"D{D}_terms"] = np.array(exact)
+    np.savez_compressed(os.path.join(HERE, "lscv.npz"), **rec)
+
+
 if __name__ == "__main__":
-    print("trees", make_trees())
-    make_moments()
-    make_series()
-    make_bounds()
-    make_runs()
-    make_subsamples()
-    make_c1()
+    which = sys.argv[1:] or ["trees", "moments", "series", "bounds", "runs", "subsamples",
+                             "c1", "lscv"]
+    if "trees" in which:
+        print("trees", make_trees())
+    if "moments" in which:
+        make_moments()
+    if "series" in which:
+        make_series()
+    if "bounds" in which:
+        make_bounds()
+    if "runs" in which:
+        make_runs()
+    if "subsamples" in which:
+        make_subsamples()
+    if "c1" in which:
+        make_c1()
+    if "lscv" in which:
+        make_lscv()
     print("done")

@@ -272,3 +272,52 @@ def test_edge_cases(fg, oracle, case):
     for eps in (0.01, 0.0):
         res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=eps), qt, rt)
         assert oracle.max_rel_error(res.values, exact) <= max(eps, 1e-12)
+
+
+def test_query_sharding_reproduces_full_run(fg):
+    """Round-robin block shards (paper_1206_6857_b200.distributed), run one after
+    another on one GPU, sum to exactly the unsharded result (each block is
+    processed identically whichever rank owns it)."""
+    import torch
+
+    from paper_1206_6857_b200.distributed import shard_blocks
+    from paper_1206_6857_b200.summation_engine import query_block_count, run_blocks
+
+    rng = np.random.default_rng(21)
+    pts = rng.random((20000, 3))
+    w = rng.uniform(0.5, 1.5, 20000)
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    h = 0.05
+    t.refresh_moments(h, fg.default_plimit(3))
+    cfg = fg.RunConfig(bandwidth=h, epsilon=0.01)
+    full = fg.dito_run(cfg, t, t).values
+    nb = query_block_count(t)
+    for world in (2, 3, 8):
+        acc = torch.zeros(20000, dtype=torch.float64, device="cuda")
+        visits = 0
+        for rank in range(world):
+            part = torch.zeros(20000, dtype=torch.float64, device="cuda")
+            b0, b1, s = shard_blocks(nb, rank, world)
+            visits += run_blocks(cfg, t, t, b0, b1, s, out=part).counters.pair_visits
+            assert torch.count_nonzero(acc * part) == 0  # disjoint supports
+            acc += part
+        np.testing.assert_array_equal(acc.cpu().numpy(), full)
+
+
+@pytest.mark.parametrize("D", [2, 3])
+def test_lscv_score_and_selection(fg, D):
+    """cli_harness.py:101-157 callers of the hot path: the LSCV score from two
+    device runs is within the eps contract of the exact score, and the
+    bandwidth search lands where the reference's select_bandwidth did."""
+    from paper_1206_6857_b200.harness import lscv_score, select_bandwidth
+
+    g = golden("lscv.npz")
+    pts = g[f"D{D}_points"]
+    tree = fg.build_tree(fg.PointStore(pts), 25)
+    for h, (t1, t2) in zip(g[f"D{D}_hs"], g[f"D{D}_terms"]):
+        for alg, eps in (("dfd", 1e-3), ("dito", 1e-3), ("dfd", 0.0)):
+            s = lscv_score(tree, float(h), eps, alg)
+            # each sum is within eps relative, so each term is too
+            assert abs(s - (t1 - t2)) <= eps * (abs(t1) + abs(t2)) + 1e-12 * (t1 + t2)
+    h_sel = select_bandwidth(pts, seed=0)
+    assert abs(np.log(h_sel / float(g[f"D{D}_h_select"]))) <= 0.05

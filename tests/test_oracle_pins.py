@@ -177,3 +177,17 @@ def test_config1_golden(oracle):
     sub = slice(0, 500)
     naive = oracle.naive_sum(wl.queries[sub], wl.references, wl.weights, 0.05)
     assert rel(naive, g["naive"][sub]) <= 1e-13
+
+
+def test_lscv_exact_terms(oracle):
+    g = golden("lscv.npz")
+    for D in (2, 3):
+        pts = g[f"D{D}_points"]
+        n = pts.shape[0]
+        for h, (t1, t2) in zip(g[f"D{D}_hs"], g[f"D{D}_terms"]):
+            conv = oracle.naive_sum(pts, pts, np.ones(n), np.sqrt(2.0) * h, threads=0)
+            near = oracle.naive_sum(pts, pts, np.ones(n), h, threads=0)
+            nc = (2 * np.pi * 2 * h * h) ** (-0.5 * D)
+            nn = (2 * np.pi * h * h) ** (-0.5 * D)
+            assert nc * conv.sum() / n ** 2 == pytest.approx(t1, rel=1e-12)
+            assert 2 * nn * (near.sum() - n) / (n * (n - 1)) == pytest.approx(t2, rel=1e-12)
