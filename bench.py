@@ -210,7 +210,8 @@ def run_reference(args):
               f"reference tree (bichromatic restatement of the monochromatic sums), "
               f"tree build + refresh + DFS DITO")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))), "host_only": True,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; SURVEY Appendix C)",

@@ -139,6 +139,57 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
     return acc;
 }
 
+// Graded-lex position of a 3-digit index (for the factorised D = 3 EVALM).
+template <int P>
+struct GLexIndex3 {
+    int idx[P][P][P];
+    constexpr GLexIndex3() : idx{} {
+        constexpr GLex<3, P> G{};
+        for (int a = 0; a < P; a++)
+            for (int b = 0; b < P; b++)
+                for (int c = 0; c < P; c++) idx[a][b][c] = -1;
+        for (int k = 0; k < G.K; k++) idx[G.dig[k][0]][G.dig[k][1]][G.dig[k][2]] = k;
+    }
+};
+
+// EVALM for D = 3, factorised: sum_a L0[a] sum_b L1[b] sum_c A_abc L2[c], which
+// takes K + C(P+1,2) + P FMAs instead of 3K multiplies (56 + 21 + 6 vs 168 at
+// P = 6).  Terms of degree >= p are masked (coefficient 0).
+template <int P, class ExpF>
+__device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
+                                                  const double *__restrict__ c,
+                                                  const double *__restrict__ A, int p,
+                                                  double inv_sc, ExpF expf) {
+    constexpr GLexIndex3<P> I{};
+    double lad[3][P];
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        const double t = (x[d] - __ldg(c + d)) * inv_sc;
+        const double g = expf(-t * t);
+        lad[d][0] = g;
+        if (P > 1) lad[d][1] = 2.0 * t * g;
+#pragma unroll
+        for (int n = 1; n + 1 < P; n++) lad[d][n + 1] = 2.0 * t * lad[d][n] - 2.0 * n * lad[d][n - 1];
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int a = 0; a < P; a++) {
+        double t1 = 0.0;
+#pragma unroll
+        for (int b = 0; a + b < P; b++) {
+            double t2 = 0.0;
+#pragma unroll
+            for (int cc = 0; a + b + cc < P; cc++) {
+                const double coef = (a + b + cc < p) ? __ldg(A + I.idx[a][b][cc]) : 0.0;
+                t2 = fma(coef, lad[2][cc], t2);
+            }
+            t1 = fma(t2, lad[1][b], t1);
+        }
+        acc = fma(t1, lad[0][a], acc);
+    }
+    return acc;
+}
+
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)
 template <int D>
 __device__ double eval_local_lane(const double (&x)[D], const double (&c)[D],

@@ -466,11 +466,17 @@ traverse_kernel(const TravArgs A) {
                 const int meth = e.y >> 8, p = e.y & 0xff;
                 if (meth == 2) {
                     constexpr int PF = default_plimit_c(D);
-                    if (A.plimit == PF)
-                        pt_est += eval_far_fixed<D, PF>(x, A.r_c + (int64_t)e.x * D,
-                                                        A.r_mom + (int64_t)e.x * A.mom_K, p,
-                                                        1.0 / A.sc);
-                    else
+                    if (A.plimit == PF) {
+                        if constexpr (D == 3) {
+                            pt_est += eval_far_fixed3<PF>(
+                                x, A.r_c + (int64_t)e.x * D, A.r_mom + (int64_t)e.x * A.mom_K, p,
+                                1.0 / A.sc, [&](double v) { return fg_exp_fast(v, s_tab); });
+                        } else {
+                            pt_est += eval_far_fixed<D, PF>(x, A.r_c + (int64_t)e.x * D,
+                                                            A.r_mom + (int64_t)e.x * A.mom_K, p,
+                                                            1.0 / A.sc);
+                        }
+                    } else
                         pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)e.x * D,
                                                    A.r_mom + (int64_t)e.x * A.mom_K, p, A.kp[p],
                                                    A.sc, A.digits);
