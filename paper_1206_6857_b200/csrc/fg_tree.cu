@@ -10,10 +10,16 @@
 // one-sided.  The stable per-chunk partition therefore reproduces the
 // reference's permutation and node ranges exactly.
 //
+// The whole build is ONE cooperative launch: a resident grid walks all levels,
+// separating the phases of a level (chunk statistics, node combine, radius and
+// left counts, split decision, grid-wide scans, stable scatter, child
+// allocation) with grid-wide barriers.  No host round trip per level.
+//
 // Points live as SoA coordinate planes (ping-pong) during the build; a node's
 // points are copied to the final tree-order arrays when it becomes a leaf.
 // Node ids are allocated level by level (BFS), so each level is a contiguous
 // id range, which the bottom-up moment pass uses.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -22,25 +28,55 @@
 #include "fg_device.cuh"
 #include "fg_internal.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace fg {
 
-constexpr int kChunk = 2048;
+// A chunk is processed by one warp (8 points per lane): deep levels hold many
+// tiny nodes, and warp-level reductions need no block barriers.
+constexpr int kChunk = 256;
 constexpr int kBuildThreads = 256;
 constexpr int kPerThread = kChunk / kBuildThreads;  // 8
+constexpr int kMaxLevels = 1024;
+
+// control block (device): level state written by one thread between barriers
+enum { kNa = 0, kNchunks = 1, kNextBase = 2, kLevels = 3, kOverflow = 4, kCtl = 8 };
 
 struct BuildBufs {
     DBuf x[2], w[2], idx[2];   // SoA coords (dim planes of n), weights, original index
     DBuf xf, wf, idxf;         // final (tree order)
     DBuf act[2];               // active node ids per level
-    DBuf nch, choff;           // chunks per active slot, exclusive offsets
+    DBuf nch, choff;           // chunks per active slot, exclusive offsets (2 halves)
     DBuf chunk_slot, chunk_begin;
     DBuf part;                 // per-chunk partial stats (3*dim+1 doubles)
     DBuf part2;                // per-chunk radius partial
     DBuf lcnt, loff;           // per-chunk left counts / left offsets within node
-    DBuf split_dim, split_mid, nleft, flag, rank;
-    DBuf totals;               // int2: (nsplit, nchunks_next)
-    DBuf scan_tmp;
+    DBuf split_dim, split_mid, nleft, flag, rank, sval;
+    DBuf blk;                  // per-CTA scan totals
+    DBuf ctl, level_begin;
     DBuf bad;                  // validation flag
+};
+
+struct BuildArgs {
+    int64_t n, nmax;
+    int leaf;
+    double *x[2], *w[2];
+    int *idx[2];
+    double *xf, *wf;
+    int *idxf;
+    int *act[2];
+    int *nch, *choff;  // each 2 * nmax (halves by level parity)
+    int *chunk_slot, *chunk_begin;
+    double *part, *part2;
+    int *lcnt, *loff;
+    int *split_dim;
+    double *split_mid;
+    int *nleft, *flag, *rank;
+    unsigned long long *blk, *sval;
+    int *ctl, *level_begin;
+    int4 *node_i;
+    double *node_box, *node_c;
+    double2 *node_wr;
 };
 
 // -------------------------------------------------------------- kernels
@@ -59,21 +95,6 @@ __global__ void init_soa_kernel(const double *__restrict__ pts, const double *__
     if (!(wi > 0.0)) atomicOr(bad, 1);
     wo[i] = wi;
     idx[i] = (int)i;
-}
-
-// chunk list for the active slots
-__global__ void fill_chunks_kernel(int na, const int *__restrict__ act,
-                                   const int4 *__restrict__ node_i, const int *__restrict__ nch,
-                                   const int *__restrict__ choff, int *__restrict__ chunk_slot,
-                                   int *__restrict__ chunk_begin) {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= na) return;
-    int4 ni = node_i[act[s]];
-    int o = choff[s];
-    for (int k = 0; k < nch[s]; k++) {
-        chunk_slot[o + k] = s;
-        chunk_begin[o + k] = ni.x + k * kChunk;
-    }
 }
 
 template <int D>
@@ -116,294 +137,10 @@ __device__ __forceinline__ void block_reduce_stats(double (&lo)[D], double (&hi)
         }
         ws = warp_sum(ws);
     }
-}
-
-template <int D>
-__global__ void __launch_bounds__(kBuildThreads)
-stats_partial_kernel(int64_t n, const double *__restrict__ x, const double *__restrict__ w,
-                     const int *__restrict__ act, const int4 *__restrict__ node_i,
-                     const int *__restrict__ chunk_slot, const int *__restrict__ chunk_begin,
-                     double *__restrict__ part) {
-    __shared__ double sh[(kBuildThreads / 32) * (3 * D + 1)];
-    const int c = blockIdx.x;
-    const int4 ni = node_i[act[chunk_slot[c]]];
-    const int cb = chunk_begin[c];
-    const int ce = min(cb + kChunk, ni.x + ni.y);
-    double lo[D], hi[D], sm[D], ws = 0.0;
-#pragma unroll
-    for (int d = 0; d < D; d++) {
-        lo[d] = CUDART_INF;
-        hi[d] = -CUDART_INF;
-        sm[d] = 0.0;
-    }
-    for (int i = cb + threadIdx.x; i < ce; i += kBuildThreads) {
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            double v = x[(int64_t)d * n + i];
-            lo[d] = fmin(lo[d], v);
-            hi[d] = fmax(hi[d], v);
-            sm[d] += v;
-        }
-        ws += w[i];
-    }
-    block_reduce_stats<D>(lo, hi, sm, ws, sh);
-    if (threadIdx.x == 0) {
-        double *p = part + (int64_t)c * (3 * D + 1);
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            p[d] = lo[d];
-            p[D + d] = hi[d];
-            p[2 * D + d] = sm[d];
-        }
-        p[3 * D] = ws;
-    }
-}
-
-// warp per active slot: combine chunk partials, choose the split
-template <int D>
-__global__ void node_stats_kernel(int na, int leaf, const int *__restrict__ act,
-                                  int4 *__restrict__ node_i, const int *__restrict__ nch,
-                                  const int *__restrict__ choff, const double *__restrict__ part,
-                                  double *__restrict__ node_box, double *__restrict__ node_c,
-                                  double2 *__restrict__ node_wr, int *__restrict__ split_dim,
-                                  double *__restrict__ split_mid) {
-    const int lane = threadIdx.x & 31;
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (s >= na) return;
-    const int node = act[s];
-    const int4 ni = node_i[node];
-    double lo[D], hi[D], sm[D], ws = 0.0;
-#pragma unroll
-    for (int d = 0; d < D; d++) {
-        lo[d] = CUDART_INF;
-        hi[d] = -CUDART_INF;
-        sm[d] = 0.0;
-    }
-    const int c0 = choff[s], c1 = c0 + nch[s];
-    for (int c = c0 + lane; c < c1; c += 32) {
-        const double *p = part + (int64_t)c * (3 * D + 1);
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            lo[d] = fmin(lo[d], p[d]);
-            hi[d] = fmax(hi[d], p[D + d]);
-            sm[d] += p[2 * D + d];
-        }
-        ws += p[3 * D];
-    }
-#pragma unroll
-    for (int d = 0; d < D; d++) {
-        lo[d] = warp_min(lo[d]);
-        hi[d] = warp_max(hi[d]);
-        sm[d] = warp_sum(sm[d]);
-    }
-    ws = warp_sum(ws);
-    if (lane == 0) {
-        const double cnt = (double)ni.y;
-        int sd = 0;
-        double best = hi[0] - lo[0];
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            node_box[(int64_t)node * 2 * D + d] = lo[d];
-            node_box[(int64_t)node * 2 * D + D + d] = hi[d];
-            node_c[(int64_t)node * D + d] = sm[d] / cnt;
-            double wd = hi[d] - lo[d];
-            if (d > 0 && wd > best) {
-                best = wd;
-                sd = d;
-            }
-        }
-        node_wr[node] = make_double2(ws, 0.0);
-        const bool leafy = ni.y <= leaf || best == 0.0;
-        split_dim[s] = leafy ? -1 : sd;
-        split_mid[s] = 0.5 * (lo[sd] + hi[sd]);
-    }
-}
-
-// per chunk: inf-norm radius partial and left count
-template <int D>
-__global__ void __launch_bounds__(kBuildThreads)
-radius_count_kernel(int64_t n, const double *__restrict__ x, const int *__restrict__ act,
-                    const int4 *__restrict__ node_i, const int *__restrict__ chunk_slot,
-                    const int *__restrict__ chunk_begin, const double *__restrict__ node_c,
-                    const int *__restrict__ split_dim, const double *__restrict__ split_mid,
-                    double *__restrict__ part2, int *__restrict__ lcnt) {
-    __shared__ double shr[kBuildThreads / 32];
-    __shared__ int shc[kBuildThreads / 32];
-    const int c = blockIdx.x;
-    const int s = chunk_slot[c];
-    const int node = act[s];
-    const int4 ni = node_i[node];
-    const int cb = chunk_begin[c];
-    const int ce = min(cb + kChunk, ni.x + ni.y);
-    const int sd = split_dim[s];
-    const double mid = split_mid[s];
-    double ctr[D];
-#pragma unroll
-    for (int d = 0; d < D; d++) ctr[d] = node_c[(int64_t)node * D + d];
-    double rad = 0.0;
-    int cnt = 0;
-    for (int i = cb + threadIdx.x; i < ce; i += kBuildThreads) {
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            double v = x[(int64_t)d * n + i];
-            rad = fmax(rad, fabs(v - ctr[d]));
-        }
-        if (sd >= 0) cnt += x[(int64_t)sd * n + i] < mid ? 1 : 0;
-    }
-    rad = warp_max(rad);
-    cnt = warp_sum(cnt);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) {
-        shr[wid] = rad;
-        shc[wid] = cnt;
-    }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double r = 0.0;
-        int t = 0;
-        for (int k = 0; k < kBuildThreads / 32; k++) {
-            r = fmax(r, shr[k]);
-            t += shc[k];
-        }
-        part2[c] = r;
-        lcnt[c] = t;
-    }
 }
 
-// warp per slot: radius, left count, per-chunk left offsets, final leaf test
-__global__ void node_decide_kernel(int na, const int *__restrict__ act,
-                                   const int4 *__restrict__ node_i, const int *__restrict__ nch,
-                                   const int *__restrict__ choff, const double *__restrict__ part2,
-                                   const int *__restrict__ lcnt, int *__restrict__ loff,
-                                   double2 *__restrict__ node_wr, int *__restrict__ split_dim,
-                                   int *__restrict__ nleft, int *__restrict__ flag) {
-    const int lane = threadIdx.x & 31;
-    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (s >= na) return;
-    const int node = act[s];
-    const int4 ni = node_i[node];
-    const int c0 = choff[s], c1 = c0 + nch[s];
-    double rad = 0.0;
-    int run = 0;  // running left count (exclusive offsets)
-    for (int base = c0; base < c1; base += 32) {
-        int c = base + lane;
-        int v = c < c1 ? lcnt[c] : 0;
-        if (c < c1) rad = fmax(rad, part2[c]);
-        // inclusive warp scan
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (c < c1) loff[c] = run + incl - v;
-        run += __shfl_sync(kFull, incl, 31);
-    }
-    rad = warp_max(rad);
-    if (lane == 0) {
-        double2 wr = node_wr[node];
-        wr.y = rad;
-        node_wr[node] = wr;
-        int sd = split_dim[s];
-        bool split = sd >= 0 && run > 0 && run < ni.y;
-        if (!split) split_dim[s] = -1;
-        nleft[s] = run;
-        flag[s] = split ? 1 : 0;
-    }
-}
-
-// per chunk: leaves copy to the final arrays; split nodes partition stably
-template <int D>
-__global__ void __launch_bounds__(kBuildThreads)
-scatter_kernel(int64_t n, const double *__restrict__ x, const double *__restrict__ w,
-               const int *__restrict__ idx, double *__restrict__ xn, double *__restrict__ wn,
-               int *__restrict__ idxn, double *__restrict__ xf, double *__restrict__ wf,
-               int *__restrict__ idxf, const int *__restrict__ act,
-               const int4 *__restrict__ node_i, const int *__restrict__ chunk_slot,
-               const int *__restrict__ chunk_begin, const int *__restrict__ split_dim,
-               const double *__restrict__ split_mid, const int *__restrict__ nleft,
-               const int *__restrict__ loff) {
-    typedef cub::BlockScan<int, kBuildThreads> Scan;
-    __shared__ typename Scan::TempStorage tmp;
-    const int c = blockIdx.x;
-    const int s = chunk_slot[c];
-    const int4 ni = node_i[act[s]];
-    const int cb = chunk_begin[c];
-    const int ce = min(cb + kChunk, ni.x + ni.y);
-    const int sd = split_dim[s];
-    if (sd < 0) {
-        for (int i = cb + threadIdx.x; i < ce; i += kBuildThreads) {
-#pragma unroll
-            for (int d = 0; d < D; d++) xf[(int64_t)d * n + i] = x[(int64_t)d * n + i];
-            wf[i] = w[i];
-            idxf[i] = idx[i];
-        }
-        return;
-    }
-    const double mid = split_mid[s];
-    const int i0 = cb + threadIdx.x * kPerThread;
-    unsigned mask = 0;
-    int cnt = 0;
-#pragma unroll
-    for (int k = 0; k < kPerThread; k++) {
-        int i = i0 + k;
-        if (i < ce && x[(int64_t)sd * n + i] < mid) {
-            mask |= 1u << k;
-            cnt++;
-        }
-    }
-    int excl;
-    Scan(tmp).ExclusiveSum(cnt, excl);
-    const int left_base = ni.x + loff[c];
-    // elements of this chunk before thread: threadIdx.x*kPerThread (if in range)
-    const int before = threadIdx.x * kPerThread;
-    const int right_base = ni.x + nleft[s] + (cb - ni.x - loff[c]);
-    int lrank = excl, rrank = before - excl;
-#pragma unroll
-    for (int k = 0; k < kPerThread; k++) {
-        int i = i0 + k;
-        if (i >= ce) break;
-        int dst;
-        if (mask & (1u << k)) dst = left_base + lrank++;
-        else dst = right_base + rrank++;
-#pragma unroll
-        for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = x[(int64_t)d * n + i];
-        wn[dst] = w[i];
-        idxn[dst] = idx[i];
-    }
-}
-
-__global__ void make_children_kernel(int na, int next_base, const int *__restrict__ act,
-                                     int4 *__restrict__ node_i, const int *__restrict__ flag,
-                                     const int *__restrict__ rank, const int *__restrict__ nleft,
-                                     int *__restrict__ act_next, int *__restrict__ nch_next) {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= na) return;
-    if (!flag[s]) return;
-    const int node = act[s];
-    int4 ni = node_i[node];
-    const int r = rank[s];
-    const int L = next_base + 2 * r, R = L + 1;
-    const int nl = nleft[s];
-    node_i[L] = make_int4(ni.x, nl, -1, -1);
-    node_i[R] = make_int4(ni.x + nl, ni.y - nl, -1, -1);
-    ni.z = L;
-    ni.w = R;
-    node_i[node] = ni;
-    act_next[2 * r] = L;
-    act_next[2 * r + 1] = R;
-    nch_next[2 * r] = (nl + kChunk - 1) / kChunk;
-    nch_next[2 * r + 1] = (ni.y - nl + kChunk - 1) / kChunk;
-}
-
-__global__ void totals_kernel(int na, const int *__restrict__ flag, const int *__restrict__ rank,
-                              const int *__restrict__ nch_next, const int *__restrict__ choff_next,
-                              int *__restrict__ totals) {
-    int nsplit = na > 0 ? rank[na - 1] + flag[na - 1] : 0;
-    int nn = 2 * nsplit;
-    totals[0] = nsplit;
-    totals[1] = nn > 0 ? choff_next[nn - 1] + nch_next[nn - 1] : 0;
-}
+#include "fg_tree_coop.cuh"
 
 template <int D>
 __global__ void pack_tree_kernel(int64_t n, const double *__restrict__ xf,
@@ -422,104 +159,89 @@ __global__ void pack_tree_kernel(int64_t n, const double *__restrict__ xf,
 }
 
 // ------------------------------------------------------------- host side
-static int scan_ints(const int *in, int *out, int count, BuildBufs &B) {
-    size_t bytes = 0;
-    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, count, stream()));
-    FG_TRY(B.scan_tmp.reserve(bytes + 16));
-    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(B.scan_tmp.p, bytes, in, out, count, stream()));
-    return FG_OK;
-}
-
 template <int D>
 static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
-    const int nmax = (int)std::max<int64_t>(2 * n, 2);
-    // node 0 = root
-    int4 root = make_int4(0, (int)n, -1, -1);
-    FG_CUDA_TRY(cudaMemcpyAsync(t.node_i.p, &root, sizeof(int4), cudaMemcpyHostToDevice, stream()));
-    int zero = 0;
-    int root_nch = (int)((n + kChunk - 1) / kChunk);
+    const int64_t nmax = std::max<int64_t>(2 * n, 2);
+    BuildArgs A;
+    A.n = n;
+    A.nmax = nmax;
+    A.leaf = leaf;
+    for (int k = 0; k < 2; k++) {
+        A.x[k] = B.x[k].as<double>();
+        A.w[k] = B.w[k].as<double>();
+        A.idx[k] = B.idx[k].as<int>();
+        A.act[k] = B.act[k].as<int>();
+    }
+    A.xf = B.xf.as<double>();
+    A.wf = B.wf.as<double>();
+    A.idxf = B.idxf.as<int>();
+    A.nch = B.nch.as<int>();
+    A.choff = B.choff.as<int>();
+    A.chunk_slot = B.chunk_slot.as<int>();
+    A.chunk_begin = B.chunk_begin.as<int>();
+    A.part = B.part.as<double>();
+    A.part2 = B.part2.as<double>();
+    A.lcnt = B.lcnt.as<int>();
+    A.loff = B.loff.as<int>();
+    A.split_dim = B.split_dim.as<int>();
+    A.split_mid = B.split_mid.as<double>();
+    A.nleft = B.nleft.as<int>();
+    A.flag = B.flag.as<int>();
+    A.rank = B.rank.as<int>();
+    A.sval = B.sval.as<unsigned long long>();
+    A.ctl = B.ctl.as<int>();
+    A.level_begin = B.level_begin.as<int>();
+    A.node_i = t.node_i.as<int4>();
+    A.node_box = t.node_box.as<double>();
+    A.node_c = t.node_c.as<double>();
+    A.node_wr = t.node_wr.as<double2>();
+
+    // level 0: the root owns every point
+    const int root_nch = (int)((n + kChunk - 1) / kChunk);
+    struct Init {
+        int4 root;
+        int ctl[kCtl];
+    } init;
+    init.root = make_int4(0, (int)n, -1, -1);
+    for (int k = 0; k < kCtl; k++) init.ctl[k] = 0;
+    init.ctl[kNa] = 1;
+    init.ctl[kNchunks] = root_nch;
+    init.ctl[kNextBase] = 1;
+    const int zero = 0;
+    FG_CUDA_TRY(cudaMemcpyAsync(t.node_i.p, &init.root, sizeof(int4), cudaMemcpyHostToDevice, stream()));
+    FG_CUDA_TRY(cudaMemcpyAsync(B.ctl.p, init.ctl, sizeof(init.ctl), cudaMemcpyHostToDevice, stream()));
     FG_CUDA_TRY(cudaMemcpyAsync(B.act[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, stream()));
     FG_CUDA_TRY(cudaMemcpyAsync(B.nch.p, &root_nch, sizeof(int), cudaMemcpyHostToDevice, stream()));
     FG_CUDA_TRY(cudaMemcpyAsync(B.choff.p, &zero, sizeof(int), cudaMemcpyHostToDevice, stream()));
-    int na = 1, nchunks = root_nch, cur = 0, next_base = 1, level = 0;
-    t.level_begin.assign(1, 0);
-    int *h_tot = nullptr;
-    FG_CUDA_TRY(cudaMallocHost(&h_tot, 2 * sizeof(int)));
-    int status = FG_OK;
-    while (na > 0) {
-        int *act = B.act[cur & 1].as<int>();
-        int *act_next = B.act[(cur + 1) & 1].as<int>();
-        int *nch = B.nch.as<int>() + (cur & 1) * nmax;
-        int *choff = B.choff.as<int>() + (cur & 1) * nmax;
-        int *nch_next = B.nch.as<int>() + ((cur + 1) & 1) * nmax;
-        int *choff_next = B.choff.as<int>() + ((cur + 1) & 1) * nmax;
-        const double *x = B.x[cur & 1].as<double>();
-        const double *w = B.w[cur & 1].as<double>();
-        const int *idx = B.idx[cur & 1].as<int>();
-        count_launch();
-        fill_chunks_kernel<<<(na + 127) / 128, 128, 0, stream()>>>(
-            na, act, t.node_i.as<int4>(), nch, choff, B.chunk_slot.as<int>(),
-            B.chunk_begin.as<int>());
-        count_launch();
-        stats_partial_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
-            n, x, w, act, t.node_i.as<int4>(), B.chunk_slot.as<int>(), B.chunk_begin.as<int>(),
-            B.part.as<double>());
-        const int wblocks = (na * 32 + 255) / 256;
-        count_launch();
-        node_stats_kernel<D><<<wblocks, 256, 0, stream()>>>(
-            na, leaf, act, t.node_i.as<int4>(), nch, choff, B.part.as<double>(),
-            t.node_box.as<double>(), t.node_c.as<double>(), t.node_wr.as<double2>(),
-            B.split_dim.as<int>(), B.split_mid.as<double>());
-        count_launch();
-        radius_count_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
-            n, x, act, t.node_i.as<int4>(), B.chunk_slot.as<int>(), B.chunk_begin.as<int>(),
-            t.node_c.as<double>(), B.split_dim.as<int>(), B.split_mid.as<double>(),
-            B.part2.as<double>(), B.lcnt.as<int>());
-        count_launch();
-        node_decide_kernel<<<wblocks, 256, 0, stream()>>>(
-            na, act, t.node_i.as<int4>(), nch, choff, B.part2.as<double>(), B.lcnt.as<int>(),
-            B.loff.as<int>(), t.node_wr.as<double2>(), B.split_dim.as<int>(),
-            B.nleft.as<int>(), B.flag.as<int>());
-        FG_CUDA_TRY(cudaGetLastError());
-        FG_TRY(scan_ints(B.flag.as<int>(), B.rank.as<int>(), na, B));
-        count_launch();
-        scatter_kernel<D><<<nchunks, kBuildThreads, 0, stream()>>>(
-            n, x, w, idx, B.x[(cur + 1) & 1].as<double>(), B.w[(cur + 1) & 1].as<double>(),
-            B.idx[(cur + 1) & 1].as<int>(), B.xf.as<double>(), B.wf.as<double>(),
-            B.idxf.as<int>(), act, t.node_i.as<int4>(), B.chunk_slot.as<int>(),
-            B.chunk_begin.as<int>(), B.split_dim.as<int>(), B.split_mid.as<double>(),
-            B.nleft.as<int>(), B.loff.as<int>());
-        FG_CUDA_TRY(cudaMemsetAsync(nch_next, 0, sizeof(int) * 2 * na, stream()));
-        count_launch();
-        make_children_kernel<<<(na + 127) / 128, 128, 0, stream()>>>(
-            na, next_base, act, t.node_i.as<int4>(), B.flag.as<int>(), B.rank.as<int>(),
-            B.nleft.as<int>(), act_next, nch_next);
-        FG_CUDA_TRY(cudaGetLastError());
-        FG_TRY(scan_ints(nch_next, choff_next, 2 * na, B));
-        count_launch();
-        totals_kernel<<<1, 1, 0, stream()>>>(na, B.flag.as<int>(), B.rank.as<int>(), nch_next,
-                                             choff_next, B.totals.as<int>());
-        FG_CUDA_TRY(cudaMemcpyAsync(h_tot, B.totals.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
-                                    stream()));
-        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
-        const int nsplit = h_tot[0];
-        nchunks = h_tot[1];
-        level++;
-        if (nsplit > 0) t.level_begin.push_back(next_base);
-        next_base += 2 * nsplit;
-        na = 2 * nsplit;
-        cur++;
-        if (next_base > nmax) {
-            set_error("tree build: node capacity exceeded");
-            status = FG_ECUDA;
-            break;
-        }
+    const int lb01[2] = {0, 1};  // level 0 = {root}, level 1 starts at id 1
+    FG_CUDA_TRY(cudaMemcpyAsync(B.level_begin.p, lb01, sizeof(lb01), cudaMemcpyHostToDevice, stream()));
+
+    // resident grid for the cooperative launch (cached per dimension)
+    static int grid_cache[kMaxDim + 1] = {0};
+    int dev = 0;
+    FG_CUDA_TRY(cudaGetDevice(&dev));
+    if (!grid_cache[D]) {
+        int sms = 0, occ = 0;
+        FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, build_coop_kernel<D>,
+                                                                  kBuildThreads, 0));
+        grid_cache[D] = sms * std::max(1, std::min(occ, 2));
     }
-    cudaFreeHost(h_tot);
-    FG_TRY(status);
-    t.levels = level;
-    t.nnodes = next_base;
-    t.level_begin.push_back(next_base);
+    const int grid = grid_cache[D];
+    FG_TRY(B.blk.reserve(sizeof(unsigned long long) * (grid + 1)));
+    A.blk = B.blk.as<unsigned long long>();
+    void *args[] = {(void *)&A};
+    count_launch();
+    FG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_coop_kernel<D>, grid,
+                                            kBuildThreads, args, 0, stream()));
+    int ctl[kCtl];
+    FG_CUDA_TRY(cudaMemcpyAsync(ctl, B.ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    FG_REQUIRE(!ctl[kOverflow] && ctl[kNa] == 0, FG_ECUDA, "tree build: node capacity exceeded");
+    const int levels = ctl[kLevels];
+    std::vector<int> lb(levels + 1);
+    FG_CUDA_TRY(cudaMemcpyAsync(lb.data(), B.level_begin.p, sizeof(int) * (levels + 1),
+                                cudaMemcpyDeviceToHost, stream()));
     // final packing
     FG_TRY(t.pw.reserve(sizeof(double) * n * packed_stride(D)));
     FG_TRY(t.perm.reserve(sizeof(int64_t) * n));
@@ -532,6 +254,9 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     FG_CUDA_TRY(cudaMemcpyAsync(&rootwr, t.node_wr.p, sizeof(double2), cudaMemcpyDeviceToHost,
                                 stream()));
     FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    t.levels = levels;
+    t.nnodes = ctl[kNextBase];
+    t.level_begin.assign(lb.begin(), lb.end());
     t.total_w = rootwr.x;
     return FG_OK;
 }
@@ -568,7 +293,9 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_TRY(B.nleft.reserve(sizeof(int) * nmax));
     FG_TRY(B.flag.reserve(sizeof(int) * nmax));
     FG_TRY(B.rank.reserve(sizeof(int) * nmax));
-    FG_TRY(B.totals.reserve(sizeof(int) * 2));
+    FG_TRY(B.sval.reserve(sizeof(unsigned long long) * nmax));
+    FG_TRY(B.ctl.reserve(sizeof(int) * kCtl));
+    FG_TRY(B.level_begin.reserve(sizeof(int) * (kMaxLevels + 2)));
     FG_TRY(B.bad.reserve(sizeof(int)));
     FG_TRY(t.node_i.reserve(sizeof(int4) * nmax));
     FG_TRY(t.node_box.reserve(sizeof(double) * nmax * 2 * dim));

@@ -1,0 +1,340 @@
+// fg_tree_coop.cuh -- the single-launch cooperative kd-tree build kernel
+// (included by fg_tree.cu).  Seven grid-wide barriers per level:
+//   P2 chunk statistics | P3 node combine + split choice | P4 radius + left
+//   counts | P5 split decision | P6 stable scatter + scan phase 1 |
+//   scan phase 2 | scan phase 3 + child allocation.
+// A chunk finds its slot by binary search over the slots' chunk offsets, and
+// one 64-bit scan over the slots yields both the children's BFS ranks and
+// their chunk offsets.
+#pragma once
+// (included inside namespace fg)
+
+typedef cub::BlockScan<int, kBuildThreads> BlockScanInt;
+typedef cub::BlockScan<unsigned long long, kBuildThreads> BlockScanU64;
+
+// slot owning chunk c: the last s with choff[s] <= c (offsets strictly increase)
+__device__ __forceinline__ int chunk_slot_of(const int *choff, int na, int c) {
+    int lo = 0, hi = na - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (choff[mid] <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBuildThreads)
+build_coop_kernel(const BuildArgs B) {
+    cg::grid_group g = cg::this_grid();
+    __shared__ double sh[(kBuildThreads / 32) * (3 * D + 1)];
+    __shared__ union {
+        typename BlockScanInt::TempStorage i32;
+        typename BlockScanU64::TempStorage u64;
+    } scan_tmp;
+    __shared__ double shr[kBuildThreads / 32];
+    __shared__ int shc[kBuildThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t n = B.n;
+    const int gtid = blockIdx.x * kBuildThreads + threadIdx.x;
+    const int gwarps = gridDim.x * kBuildThreads / 32;
+    const int gwarp = gtid >> 5;
+    const int nmax = (int)B.nmax;
+    unsigned long long *val = reinterpret_cast<unsigned long long *>(B.part2) + 0;  // unused
+    (void)val;
+
+    for (int level = 0; level < kMaxLevels; level++) {
+        const int cur = level & 1;
+        const int na = B.ctl[kNa];
+        if (na == 0) break;
+        const int nchunks = B.ctl[kNchunks];
+        const int next_base = B.ctl[kNextBase];
+        const int *act = B.act[cur];
+        int *act_next = B.act[cur ^ 1];
+        const int *choff = B.choff + cur * nmax;
+        int *choff_next = B.choff + (cur ^ 1) * nmax;
+        const double *x = B.x[cur];
+        const double *w = B.w[cur];
+        const int *idx = B.idx[cur];
+        auto chunk_end = [&](int s) { return s + 1 < na ? choff[s + 1] : nchunks; };
+
+        // ---- P2: per-chunk min / max / sum / weight
+        for (int c = gwarp; c < nchunks; c += gwarps) {
+            const int s = chunk_slot_of(choff, na, c);
+            const int4 ni = B.node_i[act[s]];
+            const int cb = ni.x + (c - choff[s]) * kChunk;
+            const int ce = min(cb + kChunk, ni.x + ni.y);
+            double lo[D], hi[D], sm[D], ws = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = CUDART_INF;
+                hi[d] = -CUDART_INF;
+                sm[d] = 0.0;
+            }
+            for (int i = cb + lane; i < ce; i += 32) {
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const double v = x[(int64_t)d * n + i];
+                    lo[d] = fmin(lo[d], v);
+                    hi[d] = fmax(hi[d], v);
+                    sm[d] += v;
+                }
+                ws += w[i];
+            }
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = warp_min(lo[d]);
+                hi[d] = warp_max(hi[d]);
+                sm[d] = warp_sum(sm[d]);
+            }
+            ws = warp_sum(ws);
+            if (lane == 0) {
+                double *p = B.part + (int64_t)c * (3 * D + 1);
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    p[d] = lo[d];
+                    p[D + d] = hi[d];
+                    p[2 * D + d] = sm[d];
+                }
+                p[3 * D] = ws;
+            }
+        }
+        g.sync();
+
+        // ---- P3: combine chunk partials per node, choose the split (warp per slot)
+        for (int s = gwarp; s < na; s += gwarps) {
+            const int node = act[s];
+            const int4 ni = B.node_i[node];
+            double lo[D], hi[D], sm[D], ws = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = CUDART_INF;
+                hi[d] = -CUDART_INF;
+                sm[d] = 0.0;
+            }
+            const int c0 = choff[s], c1 = chunk_end(s);
+            for (int c = c0 + lane; c < c1; c += 32) {
+                const double *p = B.part + (int64_t)c * (3 * D + 1);
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    lo[d] = fmin(lo[d], p[d]);
+                    hi[d] = fmax(hi[d], p[D + d]);
+                    sm[d] += p[2 * D + d];
+                }
+                ws += p[3 * D];
+            }
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = warp_min(lo[d]);
+                hi[d] = warp_max(hi[d]);
+                sm[d] = warp_sum(sm[d]);
+            }
+            ws = warp_sum(ws);
+            if (lane == 0) {
+                const double cnt = (double)ni.y;
+                int sd = 0;
+                double best = hi[0] - lo[0];
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    B.node_box[(int64_t)node * 2 * D + d] = lo[d];
+                    B.node_box[(int64_t)node * 2 * D + D + d] = hi[d];
+                    B.node_c[(int64_t)node * D + d] = sm[d] / cnt;
+                    const double wd = hi[d] - lo[d];
+                    if (d > 0 && wd > best) {
+                        best = wd;
+                        sd = d;
+                    }
+                }
+                B.node_wr[node] = make_double2(ws, 0.0);
+                const bool leafy = ni.y <= B.leaf || best == 0.0;
+                B.split_dim[s] = leafy ? -1 : sd;
+                B.split_mid[s] = 0.5 * (lo[sd] + hi[sd]);
+            }
+        }
+        g.sync();
+
+        // ---- P4: per chunk inf-norm radius partial and left count
+        for (int c = gwarp; c < nchunks; c += gwarps) {
+            const int s = chunk_slot_of(choff, na, c);
+            const int node = act[s];
+            const int4 ni = B.node_i[node];
+            const int cb = ni.x + (c - choff[s]) * kChunk;
+            const int ce = min(cb + kChunk, ni.x + ni.y);
+            const int sd = B.split_dim[s];
+            const double mid = B.split_mid[s];
+            double ctr[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) ctr[d] = B.node_c[(int64_t)node * D + d];
+            double rad = 0.0;
+            int cnt = 0;
+            for (int i = cb + lane; i < ce; i += 32) {
+#pragma unroll
+                for (int d = 0; d < D; d++) rad = fmax(rad, fabs(x[(int64_t)d * n + i] - ctr[d]));
+                if (sd >= 0) cnt += x[(int64_t)sd * n + i] < mid ? 1 : 0;
+            }
+            rad = warp_max(rad);
+            cnt = warp_sum(cnt);
+            if (lane == 0) {
+                B.part2[c] = rad;
+                B.lcnt[c] = cnt;
+            }
+        }
+        g.sync();
+
+        // ---- P5: radius, left count, per-chunk left offsets, final leaf test;
+        // the slot's scan value packs (is_split, chunks of its two children)
+        for (int s = gwarp; s < na; s += gwarps) {
+            const int node = act[s];
+            const int4 ni = B.node_i[node];
+            const int c0 = choff[s], c1 = chunk_end(s);
+            double rad = 0.0;
+            int run = 0;
+            for (int base = c0; base < c1; base += 32) {
+                const int c = base + lane;
+                const int v = c < c1 ? B.lcnt[c] : 0;
+                if (c < c1) rad = fmax(rad, B.part2[c]);
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                if (c < c1) B.loff[c] = run + incl - v;
+                run += __shfl_sync(kFull, incl, 31);
+            }
+            rad = warp_max(rad);
+            if (lane == 0) {
+                double2 wr = B.node_wr[node];
+                wr.y = rad;
+                B.node_wr[node] = wr;
+                const int sd = B.split_dim[s];
+                const bool split = sd >= 0 && run > 0 && run < ni.y;
+                if (!split) B.split_dim[s] = -1;
+                B.nleft[s] = run;
+                const unsigned long long ch =
+                    split ? (unsigned long long)((run + kChunk - 1) / kChunk +
+                                                 (ni.y - run + kChunk - 1) / kChunk)
+                          : 0ull;
+                B.sval[s] = (split ? 1ull : 0ull) | (ch << 32);
+            }
+        }
+        g.sync();
+
+        // ---- P6: stable scatter (leaves -> final arrays, splits -> next buffers)
+        for (int c = gwarp; c < nchunks; c += gwarps) {
+            const int s = chunk_slot_of(choff, na, c);
+            const int4 ni = B.node_i[act[s]];
+            const int cb = ni.x + (c - choff[s]) * kChunk;
+            const int ce = min(cb + kChunk, ni.x + ni.y);
+            const int sd = B.split_dim[s];
+            if (sd < 0) {
+                for (int i = cb + lane; i < ce; i += 32) {
+#pragma unroll
+                    for (int d = 0; d < D; d++) B.xf[(int64_t)d * n + i] = x[(int64_t)d * n + i];
+                    B.wf[i] = w[i];
+                    B.idxf[i] = idx[i];
+                }
+                continue;
+            }
+            // stable warp partition, 32 points per round, in order
+            const double mid = B.split_mid[s];
+            const int left_base = ni.x + B.loff[c];
+            const int right_base = ni.x + B.nleft[s] + (cb - ni.x - B.loff[c]);
+            double *xn = B.x[cur ^ 1];
+            double *wn = B.w[cur ^ 1];
+            int *idxn = B.idx[cur ^ 1];
+            const unsigned lt = (1u << lane) - 1u;
+            int nl = 0, nr = 0;
+            for (int base = cb; base < ce; base += 32) {
+                const int i = base + lane;
+                const bool in = i < ce;
+                const bool goes_left = in && x[(int64_t)sd * n + i] < mid;
+                const unsigned lm = __ballot_sync(kFull, goes_left);
+                const unsigned rm = __ballot_sync(kFull, in && !goes_left);
+                if (in) {
+                    const int dst = goes_left ? left_base + nl + __popc(lm & lt)
+                                              : right_base + nr + __popc(rm & lt);
+#pragma unroll
+                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = x[(int64_t)d * n + i];
+                    wn[dst] = w[i];
+                    idxn[dst] = idx[i];
+                }
+                nl += __popc(lm);
+                nr += __popc(rm);
+            }
+        }
+        // scan phase 1 over the slots: CTA b owns slots [b*per, (b+1)*per)
+        const int nb = gridDim.x;
+        const int per = (na + nb - 1) / nb;
+        const int s0 = blockIdx.x * per, s1 = min(na, s0 + per);
+        {
+            unsigned long long local = 0, tot;
+            for (int s = s0 + threadIdx.x; s < s1; s += kBuildThreads) local += B.sval[s];
+            __syncthreads();
+            BlockScanU64(scan_tmp.u64).ExclusiveSum(local, local, tot);
+            if (threadIdx.x == 0) B.blk[blockIdx.x] = tot;
+        }
+        g.sync();
+        // scan phase 2: CTA 0 scans the CTA totals
+        if (blockIdx.x == 0) {
+            unsigned long long carry = 0;
+            for (int base = 0; base < nb; base += kBuildThreads) {
+                const int i = base + threadIdx.x;
+                unsigned long long v = i < nb ? B.blk[i] : 0ull, ex, t;
+                __syncthreads();
+                BlockScanU64(scan_tmp.u64).ExclusiveSum(v, ex, t);
+                if (i < nb) B.blk[i] = carry + ex;
+                carry += t;
+            }
+            if (threadIdx.x == 0) B.blk[nb] = carry;
+        }
+        g.sync();
+        // scan phase 3 + child allocation: each split slot learns its rank r
+        // (children get BFS ids next_base + 2r, +1) and its children's chunk offsets
+        {
+            unsigned long long carry = B.blk[blockIdx.x];
+            const unsigned long long total = B.blk[nb];
+            const int nsplit = (int)(total & 0xffffffffull);
+            const int nchunks_next = (int)(total >> 32);
+            for (int base = s0; base < s1; base += kBuildThreads) {
+                const int s = base + threadIdx.x;
+                const unsigned long long v = s < s1 ? B.sval[s] : 0ull;
+                unsigned long long ex, t;
+                __syncthreads();
+                BlockScanU64(scan_tmp.u64).ExclusiveSum(v, ex, t);
+                ex += carry;
+                carry += t;
+                if (s < s1 && (v & 1ull)) {
+                    const int r = (int)(ex & 0xffffffffull);
+                    const int coff = (int)(ex >> 32);
+                    const int node = act[s];
+                    int4 ni = B.node_i[node];
+                    const int L = next_base + 2 * r, R = L + 1;
+                    const int nl = B.nleft[s];
+                    if (R < nmax) {
+                        B.node_i[L] = make_int4(ni.x, nl, -1, -1);
+                        B.node_i[R] = make_int4(ni.x + nl, ni.y - nl, -1, -1);
+                        ni.z = L;
+                        ni.w = R;
+                        B.node_i[node] = ni;
+                    }
+                    act_next[2 * r] = L;
+                    act_next[2 * r + 1] = R;
+                    choff_next[2 * r] = coff;
+                    choff_next[2 * r + 1] = coff + (nl + kChunk - 1) / kChunk;
+                }
+            }
+            if (gtid == 0) {
+                if (next_base + 2 * nsplit > nmax) B.ctl[kOverflow] = 1;
+                B.ctl[kNa] = B.ctl[kOverflow] ? 0 : 2 * nsplit;
+                B.ctl[kNchunks] = nchunks_next;
+                B.ctl[kNextBase] = next_base + 2 * nsplit;
+                B.ctl[kLevels] = level + 1;
+                // level l+1 spans [next_base, next_base + 2*nsplit): its end is the
+                // start of level l+2
+                B.level_begin[level + 2] = next_base + 2 * nsplit;
+            }
+        }
+        g.sync();
+    }
+}
