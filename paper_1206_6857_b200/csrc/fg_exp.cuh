@@ -31,6 +31,15 @@ static __constant__ double c_exp_tab[64] = {
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
 
+// 64-bit FP immediates with a non-zero low word cannot be encoded in DFMA; nvcc
+// then re-materialises them through two UMOVs at every use.  Reading them from
+// the constant bank lets DFMA take them as c[][] operands for free.
+static __constant__ double c_exp_coef[6] = {
+    0x1.71547652b82fep+6,     // 64 / ln 2
+    0x1.62e42fee00000p-7,     // ln 2 / 64, high part (32 significant bits)
+    0x1.a39ef35793c76p-39,    // ln 2 / 64, low part
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0};
+
 // copy the table to shared memory; call with all threads of the CTA, then sync
 __device__ __forceinline__ void exp_table_init(double *s_tab) {
     for (int i = threadIdx.x; i < 64; i += blockDim.x) s_tab[i] = c_exp_tab[i];
@@ -41,13 +50,13 @@ __device__ __forceinline__ void exp_table_init(double *s_tab) {
 // directly and skip the range test.
 __device__ __forceinline__ double fg_exp_normal(double x, const double *s_tab) {
     const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
-    double kd = fma(x, 0x1.71547652b82fep+6, magic);
+    double kd = fma(x, c_exp_coef[0], magic);
     const int k = __double2loint(kd);
     kd -= magic;
-    double r = fma(kd, -0x1.62e42fee00000p-7, x);
-    r = fma(kd, -0x1.a39ef35793c76p-39, r);
-    double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-    q = fma(q, r, 1.0 / 6.0);
+    double r = fma(kd, -c_exp_coef[1], x);
+    r = fma(kd, -c_exp_coef[2], r);
+    double q = fma(r, c_exp_coef[3], c_exp_coef[4]);
+    q = fma(q, r, c_exp_coef[5]);
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
     const double t = s_tab[k & 63];
@@ -55,21 +64,62 @@ __device__ __forceinline__ double fg_exp_normal(double x, const double *s_tab) {
     return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
 }
 
-__device__ __forceinline__ double fg_exp_fast(double x, const double *s_tab) {
-    if (x < -708.3) return x < -745.2 ? 0.0 : exp(x);
-    const double magic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
-    double kd = fma(x, 0x1.71547652b82fep+6, magic);
+// Register-resident constants for hot loops.  The values pass through an
+// opaque `mov` so the compiler cannot re-materialise them (LDC / UMOV pairs)
+// inside the loop, and the table is addressed with a 32-bit shared-window
+// address, avoiding a per-use generic-to-shared conversion.
+struct ExpK {
+    double l2e, ln2hi, ln2lo, c5, c4, c3;
+    unsigned tab;  // shared-memory address of the 2^(j/64) table
+};
+
+__device__ __forceinline__ double opaque(double v) {
+    double r;
+    asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+    return r;
+}
+
+__device__ __forceinline__ ExpK exp_consts(const double *s_tab) {
+    ExpK k;
+    k.l2e = opaque(c_exp_coef[0]);
+    k.ln2hi = opaque(-c_exp_coef[1]);
+    k.ln2lo = opaque(-c_exp_coef[2]);
+    k.c5 = opaque(c_exp_coef[3]);
+    k.c4 = opaque(c_exp_coef[4]);
+    k.c3 = opaque(c_exp_coef[5]);
+    unsigned a = (unsigned)__cvta_generic_to_shared(s_tab);
+    asm volatile("mov.b32 %0, %1;" : "=r"(k.tab) : "r"(a));
+    return k;
+}
+
+// fg_exp_normal with register constants (x >= -708.3)
+__device__ __forceinline__ double fg_exp_k(double x, const ExpK &K) {
+    const double magic = 6755399441055744.0;
+    double kd = fma(x, K.l2e, magic);
     const int k = __double2loint(kd);
     kd -= magic;
-    double r = fma(kd, -0x1.62e42fee00000p-7, x);
-    r = fma(kd, -0x1.a39ef35793c76p-39, r);
-    double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-    q = fma(q, r, 1.0 / 6.0);
+    double r = fma(kd, K.ln2hi, x);
+    r = fma(kd, K.ln2lo, r);
+    double q = fma(r, K.c5, K.c4);
+    q = fma(q, r, K.c3);
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
-    const double t = s_tab[k & 63];
+    double t;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(t) : "r"(K.tab + ((unsigned)(k & 63) << 3)));
     const double y = fma(t, r * q, t);
     return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+}
+
+// full range with register constants: zero below -745.2, libdevice in the
+// subnormal band (rare)
+__device__ __forceinline__ double fg_exp_kc(double x, const ExpK &K) {
+    if (x < -708.3) return x < -745.2 ? 0.0 : exp(x);
+    return fg_exp_k(x, K);
+}
+
+__device__ __forceinline__ double fg_exp_fast(double x, const double *s_tab) {
+    if (x < -708.3) return x < -745.2 ? 0.0 : exp(x);
+    return fg_exp_normal(x, s_tab);
 }
 
 __device__ __forceinline__ double fg_exp(double x) { return exp(x); }

@@ -38,6 +38,7 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
     __shared__ __align__(16) double tile[kNaiveTile * S];
     __shared__ double s_tab[64];
     exp_table_init(s_tab);
+    const ExpK K = exp_consts(s_tab);
     const int64_t q0 = (int64_t)blockIdx.x * kNaiveThreads * QPT;
     const int64_t r0 = (int64_t)blockIdx.y * rchunk;
     const int64_t r1 = min(n, r0 + rchunk);
@@ -83,7 +84,7 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
                     double df = x[i][d] - y[d];
                     d2 = fma(df, df, d2);
                 }
-                acc[i] = fma(fg_exp_fast(d2 * neg_inv, s_tab), w, acc[i]);
+                acc[i] = fma(fg_exp_kc(d2 * neg_inv, K), w, acc[i]);
             }
         }
     }

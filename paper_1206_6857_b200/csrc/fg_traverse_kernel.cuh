@@ -152,6 +152,7 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
                                             double neg_inv, const double *s_tab) {
     constexpr int S = packed_stride(D);
     constexpr int U = CHECKED ? 2 : 4;  // independent exp chains per step
+    const ExpK K = exp_consts(s_tab);   // register-resident for the loop
     double acc[U];
 #pragma unroll
     for (int u = 0; u < U; u++) acc[u] = 0.0;
@@ -174,8 +175,7 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             }
 #pragma unroll
         for (int u = 0; u < U; u++)
-            acc[u] = fma(CHECKED ? fg_exp_fast(d2[u] * neg_inv, s_tab)
-                                 : fg_exp_normal(d2[u] * neg_inv, s_tab),
+            acc[u] = fma(CHECKED ? fg_exp_kc(d2[u] * neg_inv, K) : fg_exp_k(d2[u] * neg_inv, K),
                          w[u], acc[u]);
     }
     double acc0 = acc[0], acc1 = acc[1];
@@ -193,9 +193,9 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             d0 = fma(f0, f0, d0);
             d1 = fma(f1, f1, d1);
         }
-        acc0 = fma(CHECKED ? fg_exp_fast(d0 * neg_inv, s_tab) : fg_exp_normal(d0 * neg_inv, s_tab),
+        acc0 = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K),
                    w0, acc0);
-        acc1 = fma(CHECKED ? fg_exp_fast(d1 * neg_inv, s_tab) : fg_exp_normal(d1 * neg_inv, s_tab),
+        acc1 = fma(CHECKED ? fg_exp_kc(d1 * neg_inv, K) : fg_exp_k(d1 * neg_inv, K),
                    w1, acc1);
     }
     if (j < rc) {
@@ -208,7 +208,7 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             const double f0 = x[d] - y0[d];
             d0 = fma(f0, f0, d0);
         }
-        acc0 = fma(CHECKED ? fg_exp_fast(d0 * neg_inv, s_tab) : fg_exp_normal(d0 * neg_inv, s_tab),
+        acc0 = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K),
                    w0, acc0);
     }
     return acc0 + acc1;

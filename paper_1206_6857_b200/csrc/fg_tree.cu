@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "fg_device.cuh"
@@ -225,7 +226,9 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
         FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, build_coop_kernel<D>,
                                                                   kBuildThreads, 0));
-        grid_cache[D] = sms * std::max(1, std::min(occ, 2));
+        const char *env = getenv("FG_BUILD_OCC");
+        const int cap = env ? atoi(env) : 2;  // more CTAs only make the grid barriers dearer
+        grid_cache[D] = sms * std::max(1, std::min(occ, cap));
     }
     const int grid = grid_cache[D];
     FG_TRY(B.blk.reserve(sizeof(unsigned long long) * (grid + 1)));
