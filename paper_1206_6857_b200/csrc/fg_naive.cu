@@ -30,6 +30,65 @@ __global__ void pack_points_kernel(const double *__restrict__ pts, const double 
     for (int d = dim + 1; d < stride; d++) o[d] = 0.0;
 }
 
+// CTA-wide min of lo[] and max of hi[]; every thread gets the result
+template <int D>
+__device__ __forceinline__ void block_minmax(double (&lo)[D], double (&hi)[D], double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int NW = kNaiveThreads / 32;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        lo[d] = warp_min(lo[d]);
+        hi[d] = warp_max(hi[d]);
+    }
+    __syncthreads();  // previous users of sh are done
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            sh[wid * 2 * D + d] = lo[d];
+            sh[wid * 2 * D + D + d] = hi[d];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        lo[d] = sh[d];
+        hi[d] = sh[D + d];
+        for (int k = 1; k < NW; k++) {
+            lo[d] = fmin(lo[d], sh[k * 2 * D + d]);
+            hi[d] = fmax(hi[d], sh[k * 2 * D + D + d]);
+        }
+    }
+}
+
+// one reference record against this thread's QPT queries
+template <int D, int QPT, bool CHECKED>
+__device__ __forceinline__ void naive_pair_step(const double (&x)[QPT][D], const double *rec,
+                                                double neg_inv, const ExpK &K, double (&acc)[QPT]) {
+    constexpr int S = packed_stride(D);
+    double y[D], w;
+    const double2 *t2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+    for (int k = 0; k < S / 2; k++) {
+        const double2 v = t2[k];
+        if (2 * k < D) y[2 * k] = v.x;
+        else if (2 * k == D) w = v.x;
+        if (2 * k + 1 < D) y[2 * k + 1] = v.y;
+        else if (2 * k + 1 == D) w = v.y;
+    }
+#pragma unroll
+    for (int i = 0; i < QPT; i++) {
+        const double diff = x[i][0] - y[0];
+        double d2 = diff * diff;
+#pragma unroll
+        for (int d = 1; d < D; d++) {
+            const double df = x[i][d] - y[d];
+            d2 = fma(df, df, d2);
+        }
+        const double e = CHECKED ? fg_exp_kc(d2 * neg_inv, K) : fg_exp_k(d2 * neg_inv, K);
+        acc[i] = fma(e, w, acc[i]);
+    }
+}
+
 template <int D, int QPT>
 __global__ void __launch_bounds__(kNaiveThreads)
 naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__ r, int64_t n,
@@ -37,6 +96,7 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
     constexpr int S = packed_stride(D);
     __shared__ __align__(16) double tile[kNaiveTile * S];
     __shared__ double s_tab[64];
+    __shared__ double s_red[2 * D * (kNaiveThreads / 32)];
     exp_table_init(s_tab);
     const ExpK K = exp_consts(s_tab);
     const int64_t q0 = (int64_t)blockIdx.x * kNaiveThreads * QPT;
@@ -54,6 +114,21 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
             for (int d = 0; d < D; d++) x[i][d] = 0.0;
         }
     }
+    // bounding box of this CTA's queries (uniform across the CTA)
+    double qlo[D], qhi[D];
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        qlo[d] = CUDART_INF;
+        qhi[d] = -CUDART_INF;
+#pragma unroll
+        for (int i = 0; i < QPT; i++) {
+            if (q0 + threadIdx.x + (int64_t)i * kNaiveThreads < m) {
+                qlo[d] = fmin(qlo[d], x[i][d]);
+                qhi[d] = fmax(qhi[d], x[i][d]);
+            }
+        }
+    }
+    block_minmax<D>(qlo, qhi, s_red);
     for (int64_t t0 = r0; t0 < r1; t0 += kNaiveTile) {
         const int cnt = (int)min((int64_t)kNaiveTile, r1 - t0);
         __syncthreads();
@@ -62,30 +137,33 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
             double2 *dst = reinterpret_cast<double2 *>(tile);
             for (int k = threadIdx.x; k < cnt * S / 2; k += kNaiveThreads) dst[k] = __ldg(src + k);
         }
-        __syncthreads();
+        // tile box -> skip the tile (every exp underflows to exactly 0), run the
+        // range-test-free exp (every argument >= -708), or the checked exp
+        double tlo[D], thi[D];
+        {
+            const bool v = threadIdx.x < cnt;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                tlo[d] = v ? tile[threadIdx.x * S + d] : CUDART_INF;
+                thi[d] = v ? tile[threadIdx.x * S + d] : -CUDART_INF;
+            }
+            block_minmax<D>(tlo, thi, s_red);
+        }
+        double min_sq = 0.0, max_sq = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const double g = fmax(fmax(qlo[d] - thi[d], tlo[d] - qhi[d]), 0.0);
+            min_sq += g * g;
+            const double s = fmax(qhi[d] - tlo[d], thi[d] - qlo[d]);
+            max_sq += s * s;
+        }
+        if (min_sq * neg_inv < -746.0) continue;
+        if (max_sq * neg_inv > -708.0) {
 #pragma unroll 2
-        for (int j = 0; j < cnt; j++) {
-            double y[D], w;
-            const double2 *t2 = reinterpret_cast<const double2 *>(tile + j * S);
-#pragma unroll
-            for (int k = 0; k < S / 2; k++) {
-                double2 v = t2[k];
-                if (2 * k < D) y[2 * k] = v.x;
-                else if (2 * k == D) w = v.x;
-                if (2 * k + 1 < D) y[2 * k + 1] = v.y;
-                else if (2 * k + 1 == D) w = v.y;
-            }
-#pragma unroll
-            for (int i = 0; i < QPT; i++) {
-                double diff = x[i][0] - y[0];
-                double d2 = diff * diff;
-#pragma unroll
-                for (int d = 1; d < D; d++) {
-                    double df = x[i][d] - y[d];
-                    d2 = fma(df, df, d2);
-                }
-                acc[i] = fma(fg_exp_kc(d2 * neg_inv, K), w, acc[i]);
-            }
+            for (int j = 0; j < cnt; j++) naive_pair_step<D, QPT, false>(x, tile + j * S, neg_inv, K, acc);
+        } else {
+#pragma unroll 2
+            for (int j = 0; j < cnt; j++) naive_pair_step<D, QPT, true>(x, tile + j * S, neg_inv, K, acc);
         }
     }
 #pragma unroll
