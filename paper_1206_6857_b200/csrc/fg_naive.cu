@@ -95,7 +95,7 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
              int64_t rchunk, double neg_inv, double *__restrict__ part) {
     constexpr int S = packed_stride(D);
     __shared__ __align__(16) double tile[kNaiveTile * S];
-    __shared__ double s_tab[64];
+    __shared__ double s_tab[kExpTab];
     __shared__ double s_red[2 * D * (kNaiveThreads / 32)];
     exp_table_init(s_tab);
     const ExpK K = exp_consts(s_tab);

@@ -155,15 +155,9 @@ static TravScratch g_scr;
 
 template <int D>
 static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
+    // 4 resident CTAs of 128 threads per SM (<= 128 registers): measured best;
+    // capping registers lower spills and runs slower
     auto kern = traverse_kernel<D, 4>;
-    if (D == 3) {
-        const char *env = getenv("FG_TRAV_MINB");
-        const int mb = env ? atoi(env) : 4;
-        if (mb == 5) kern = traverse_kernel<D, 5>;
-        if (mb == 6) kern = traverse_kernel<D, 6>;
-        if (mb == 8) kern = traverse_kernel<D, 8>;
-        if (mb == 1) kern = traverse_kernel<D, 1>;
-    }
     // resident-grid size, cached per (kernel, shared memory size)
     static thread_local const void *c_kern = nullptr;
     static thread_local size_t c_smem = 0;

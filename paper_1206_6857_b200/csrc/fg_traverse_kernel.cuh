@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kTravThreads, MINB)
 traverse_kernel(const TravArgs A) {
     constexpr int S = packed_stride(D);
     extern __shared__ double smem[];
-    __shared__ double s_tab[64];
+    __shared__ double s_tab[kExpTab];
     exp_table_init(s_tab);
     __syncthreads();
     const int lane = threadIdx.x & 31;
