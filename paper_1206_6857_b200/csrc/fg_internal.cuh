@@ -150,6 +150,11 @@ struct TreeDev {
     DBuf qb_box;    // double nqb x 2*dim
     DBuf qb_c;      // double nqb x dim
     DBuf qb_rad;    // double nqb
+    // heaviest-first visiting order from the previous full run's block costs
+    bool qb_order_valid = false;
+    DBuf qb_cost;   // uint64 nqb: cycles per block in the last full run
+    DBuf qb_order;  // int nqb
+    DBuf qb_keys, qb_sort_tmp, qb_iota;
 };
 
 }  // namespace fg

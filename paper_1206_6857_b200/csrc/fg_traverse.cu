@@ -29,6 +29,8 @@
 //    local coefficients in shared memory); the post pass is one EVALL per lane.
 #include <cuda_runtime.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -143,10 +145,16 @@ int query_blocks(TreeDev &t) {
     FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     t.nqb = nqb;
     t.qb_valid = true;
+    t.qb_order_valid = false;
     return FG_OK;
 }
 
 // ---------------------------------------------------------------- launch
+__global__ void iota_kernel(int *out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
 struct TravScratch {
     DBuf st_node, st_f, ser, work, counters, dbg, prime;
     int grid = 0, cap = 0;
@@ -328,8 +336,41 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
             A.prime_in = g_scr.prime.as<double>();
         }
     }
+    const bool full = b0 == 0 && b1 == q.nqb && A.stride == 1;
+    if (st == FG_OK && full && nb > 1) {
+        st = q.qb_cost.reserve(sizeof(unsigned long long) * q.nqb);
+        if (st == FG_OK) A.cost = q.qb_cost.as<unsigned long long>();
+        if (q.qb_order_valid) A.order = q.qb_order.as<int>();
+    }
     if (st == FG_OK && nb > 0) st = launch_dispatch(D, A, smem, nb);
     cudaEventRecord(e1, stream());
+    if (st == FG_OK && A.cost) {
+        // next run on this tree visits blocks heaviest-first (LPT order)
+        const int nq = (int)q.nqb;
+        size_t tmp_bytes = 0;
+        st = q.qb_iota.reserve(sizeof(int) * nq);
+        const int *iota = q.qb_iota.as<int>();
+        if (st == FG_OK) {
+            count_launch();
+            iota_kernel<<<(nq + 255) / 256, 256, 0, stream()>>>(q.qb_iota.as<int>(), nq);
+        }
+        cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
+            nullptr, tmp_bytes, A.cost, (unsigned long long *)nullptr, iota, (int *)nullptr, nq,
+            0, 64, stream());
+        if (e == cudaSuccess) st = q.qb_sort_tmp.reserve(tmp_bytes + 16);
+        if (e == cudaSuccess && st == FG_OK) st = q.qb_keys.reserve(sizeof(unsigned long long) * nq);
+        if (e == cudaSuccess && st == FG_OK) st = q.qb_order.reserve(sizeof(int) * nq);
+        if (e == cudaSuccess && st == FG_OK)
+            e = cub::DeviceRadixSort::SortPairsDescending(
+                q.qb_sort_tmp.p, tmp_bytes, A.cost, q.qb_keys.as<unsigned long long>(), iota,
+                q.qb_order.as<int>(), nq, 0, 64, stream());
+        if (e != cudaSuccess) {
+            set_error(std::string("block order sort: ") + cudaGetErrorString(e));
+            st = FG_ECUDA;
+        } else if (st == FG_OK) {
+            q.qb_order_valid = true;
+        }
+    }
     const char *dbg_path = getenv("FG_DEBUG_BLOCKS");
     for (int k = 0; k < 8; k++) cnt[k] = 0;
     if (st == FG_OK) {

@@ -57,6 +57,8 @@ struct TravArgs {
     const double *prime_in;        // per-block primed lower bound on G (or null)
     double *prime_out;             // coarse pass: write per-block bound instead of values
     double prime_scale;            // safety / (1 + eps1)
+    const int *order;              // block visiting order (full runs) or null
+    unsigned long long *cost;      // per-block cycles of this run (or null)
 };
 
 // Admit candidates in lane order under the token rule.  Unconditional
@@ -241,7 +243,13 @@ traverse_kernel(const TravArgs A) {
 
     for (;;) {
         long long b = 0;
-        if (lane == 0) b = (long long)atomicAdd(A.work, 1ULL) * A.stride + A.b0;
+        if (lane == 0) {
+            const long long i = (long long)atomicAdd(A.work, 1ULL);
+            b = i * A.stride + A.b0;
+            // full runs visit blocks in the given order (heaviest first, from
+            // the previous run's measured costs): shortens the tail
+            if (A.order && b < A.b1) b = A.order[b];
+        }
         b = __shfl_sync(kFull, b, 0);
         if (b >= A.b1) break;
 
@@ -506,6 +514,7 @@ traverse_kernel(const TravArgs A) {
         } else if (valid) {
             A.out[A.q_perm[qs + lane]] = val;
         }
+        if (lane == 0 && A.cost) A.cost[b] = (unsigned long long)(clock64() - t_start);
         if (lane == 0 && A.dbg) {
             A.dbg[4 * b + 0] = (unsigned long long)(clock64() - t_start);
             A.dbg[4 * b + 1] = steps;
