@@ -48,7 +48,9 @@ typedef struct {
     int64_t hermite_prunes;
     int64_t local_prunes;
     int64_t h2l_prunes;
-    int64_t exact_pairs; /* query x reference pairs evaluated exactly */
+    int64_t exact_pairs; /* query x reference pairs evaluated exactly in FP64 */
+    int64_t fp32_pairs;  /* pairs evaluated in FP32 with their error bound charged
+                            through the token rule (see fg_set_engine_params) */
 } fg_counters;
 
 typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_index.py:144) */
@@ -114,8 +116,12 @@ int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
                  int32_t plimit, int64_t block_begin, int64_t block_end, int64_t block_stride,
                  double *values, fg_counters *counters, double *seconds);
 /* engine knobs (0 keeps the current value): reference-side leaf size used by
- * the traversal, per-warp stack capacity.  Not part of the reference API. */
-int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap);
+ * the traversal, per-warp stack capacity; fp32_base (-1 keeps, 0 off, 1 on,
+ * default on) lets the traversal evaluate a leaf pair in FP32 when the
+ * rigorous error bound of that evaluation fits within the pair's own share of
+ * the eps budget (it is charged through the token rule, so the eps guarantee
+ * holds; eps = 0 always uses FP64).  Not part of the reference API. */
+int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap, int32_t fp32_base);
 
 /* ---- series algebra (series_expansion.py), batched over `batch` items ---
  * All arrays host or device, row-major per item.  Used by the Python mirror

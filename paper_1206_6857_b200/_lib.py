@@ -30,7 +30,7 @@ _F64 = ctypes.c_double
 class fg_counters(ctypes.Structure):
     _fields_ = [("pair_visits", _I64), ("base_cases", _I64), ("fd_prunes", _I64),
                 ("hermite_prunes", _I64), ("local_prunes", _I64), ("h2l_prunes", _I64),
-                ("exact_pairs", _I64)]
+                ("exact_pairs", _I64), ("fp32_pairs", _I64)]
 
 
 # name -> argtypes (all functions return int status except fg_last_error)
@@ -53,7 +53,7 @@ SIGNATURES = {
     "fg_run_range": [_P, _P, _F64, _F64, _I32, _I32, _I64, _I64, _I64, _P, _P, _P],
     "fg_launch_count": [_P],
     "fg_fp64_peak": [_P],
-    "fg_set_engine_params": [_I32, _I32],
+    "fg_set_engine_params": [_I32, _I32, _I32],
     "fg_series_accumulate": [_I32, _P, _P, _P, _I32, _I32, _P, _I32, _F64, _P],
     "fg_series_eval": [_I32, _P, _I32, _P, _I32, _I32, _I32, _F64, _P, _P, _P],
     "fg_series_translate": [_I32, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _F64, _P],

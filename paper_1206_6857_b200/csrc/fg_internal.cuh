@@ -145,6 +145,11 @@ struct TreeDev {
     bool mom_valid = false, mom0_valid = false;
     // query blocks (bandwidth-independent): ranges of <= 32 tree-order points
     bool qb_valid = false;
+    bool fp32_ok = true;  // coordinates and weights fit the FP32 base case's range
+    // FP32 records for the traversal's FP32 base case (fp32_pack, fg_traverse.cu)
+    bool pf_valid = false;
+    DBuf pf;      // float n x fstride: coords about the anchor centre, then weight
+    DBuf anchor;  // int n: the point's maximal node with <= 32 points (BFS id)
     int64_t nqb = 0;
     DBuf qb_range;  // int2 (start, count)
     DBuf qb_box;    // double nqb x 2*dim
@@ -182,4 +187,5 @@ int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w
 extern int g_ref_leaf;
 extern int g_qblock_mode;
 extern int g_stack_cap;
+extern int g_fp32_base;
 }  // namespace fg

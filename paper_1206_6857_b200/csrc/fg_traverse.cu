@@ -48,6 +48,8 @@ namespace fg {
 
 int g_ref_leaf = 32;
 int g_stack_cap = 4096;
+int g_fp32_base = 1;
+static constexpr double kFp32Share = 0.05;
 
 // ---------------------------------------------------------- query blocks
 // A query block is a run of <= 32 consecutive tree-order points owned by one
@@ -146,6 +148,81 @@ int query_blocks(TreeDev &t) {
     t.nqb = nqb;
     t.qb_valid = true;
     t.qb_order_valid = false;
+    return FG_OK;
+}
+
+// ------------------------------------------------------------ FP32 records
+// Anchor of a point = its maximal tree node with <= 32 points (every base item
+// of <= 32 points lies inside one).  One thread per node: an internal node with
+// > 32 points labels the points of each child that has <= 32.
+__global__ void anchor_kernel(int64_t nnodes, const int4 *__restrict__ ni, int *__restrict__ anchor) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= nnodes) return;
+    const int4 e = ni[v];
+    if (v == 0 && e.y <= 32) {
+        for (int i = 0; i < e.y; i++) anchor[e.x + i] = 0;
+        return;
+    }
+    if (e.y <= 32 || e.z < 0) return;
+    for (int c = 0; c < 2; c++) {
+        const int ch = c == 0 ? e.z : e.w;
+        const int4 ce = ni[ch];
+        if (ce.y <= 32)
+            for (int i = 0; i < ce.y; i++) anchor[ce.x + i] = ch;
+    }
+}
+
+// FP32 record of each point: coordinates about its anchor's centre (rounded
+// from the FP64 difference) and the weight.  Points of leaves with > 32
+// points have no anchor and are never evaluated in FP32 (zero records).
+template <int D>
+__global__ void fp32_pack_kernel(int64_t n, const double *__restrict__ pw,
+                                 const double *__restrict__ ctr, const int *__restrict__ anchor,
+                                 float *__restrict__ pf) {
+    constexpr int S = packed_stride(D);
+    constexpr int F = fstride<D>();
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int a = anchor[i];
+    float rec[F];
+#pragma unroll
+    for (int k = 0; k < F; k++) rec[k] = 0.f;
+    if (a >= 0) {
+#pragma unroll
+        for (int d = 0; d < D; d++) rec[d] = (float)(pw[i * S + d] - ctr[(int64_t)a * D + d]);
+        rec[D] = (float)pw[i * S + D];
+    }
+#pragma unroll
+    for (int k = 0; k < F; k += 4)
+        *reinterpret_cast<float4 *>(pf + i * F + k) = make_float4(rec[k], rec[k + 1], rec[k + 2], rec[k + 3]);
+}
+
+static int fp32_pack(TreeDev &t) {
+    if (t.pf_valid) return FG_OK;
+    const int D = t.dim;
+    const int F = (D + 1 + 3) & ~3;
+    FG_TRY(t.anchor.reserve(sizeof(int) * t.n));
+    FG_TRY(t.pf.reserve(sizeof(float) * t.n * F));
+    FG_CUDA_TRY(cudaMemsetAsync(t.anchor.p, 0xff, sizeof(int) * t.n, stream()));
+    count_launch();
+    anchor_kernel<<<(unsigned)((t.nnodes + 255) / 256), 256, 0, stream()>>>(
+        t.nnodes, t.node_i.as<int4>(), t.anchor.as<int>());
+    FG_CUDA_TRY(cudaGetLastError());
+    const unsigned blocks = (unsigned)((t.n + 255) / 256);
+#define FG_PF(DD)                                                                            \
+    case DD:                                                                                 \
+        count_launch();                                                                      \
+        fp32_pack_kernel<DD><<<blocks, 256, 0, stream()>>>(t.n, t.pw.as<double>(),           \
+                                                            t.node_c.as<double>(),           \
+                                                            t.anchor.as<int>(), t.pf.as<float>()); \
+        break;
+    switch (D) {
+        FG_PF(1) FG_PF(2) FG_PF(3) FG_PF(4) FG_PF(5) FG_PF(6) FG_PF(7) FG_PF(8)
+        default: return FG_EUNSUPPORTED;
+    }
+#undef FG_PF
+    FG_CUDA_TRY(cudaGetLastError());
+    t.pf_valid = true;
     return FG_OK;
 }
 
@@ -306,6 +383,19 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     FG_CUDA_TRY(cudaMemsetAsync(g_scr.counters.p, 0, sizeof(unsigned long long) * 8, stream()));
     A.work = g_scr.work.as<unsigned long long>();
     A.no_eager = getenv("FG_NO_EAGER") ? 1 : 0;
+    // FP32 base cases: a share kFp32Share of eps
+    // is reserved for their rounding error, the rest drives the traversal
+    int fp32 = g_fp32_base;
+    if (const char *env = getenv("FG_FP32_BASE")) fp32 = atoi(env);
+    A.ex2_scale = (float)(-1.4426950408889634 / (2.0 * h * h));
+    if (!q.fp32_ok || !r.fp32_ok || !(fabsf(A.ex2_scale) < 1e30f) || !(eps > 0.0)) fp32 = 0;
+    if (fp32) {
+        FG_TRY(fp32_pack(r));
+        A.r_pf = r.pf.as<float>();
+        A.r_anchor = r.anchor.as<int>();
+    }
+    A.fp32_rho = fp32 ? kFp32Share * eps : 0.0;
+    A.eps = fp32 ? (1.0 - kFp32Share) * eps : eps;
     if (getenv("FG_DEBUG_BLOCKS")) {
         FG_TRY(g_scr.dbg.reserve(sizeof(unsigned long long) * 4 * q.nqb));
         FG_CUDA_TRY(cudaMemsetAsync(g_scr.dbg.p, 0, sizeof(unsigned long long) * 4 * q.nqb, stream()));
@@ -405,6 +495,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         counters->local_prunes = (int64_t)cnt[4];
         counters->h2l_prunes = (int64_t)cnt[5];
         counters->exact_pairs = (int64_t)cnt[6];
+        counters->fp32_pairs = (int64_t)cnt[7];
     }
     return FG_OK;
 }

@@ -59,6 +59,10 @@ struct TravArgs {
     double prime_scale;            // safety / (1 + eps1)
     const int *order;              // block visiting order (full runs) or null
     unsigned long long *cost;      // per-block cycles of this run (or null)
+    double fp32_rho;               // relative error allowed per FP32 leaf item (0: FP64 only)
+    const float *r_pf;             // FP32 records about each point's anchor (fp32_pack)
+    const int *r_anchor;           // per point: its anchor node
+    float ex2_scale;               // -log2(e) / (2 h^2)
 };
 
 // Admit candidates in lane order under the token rule.  Unconditional
@@ -216,6 +220,106 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
     return acc0 + acc1;
 }
 
+// ---- FP32 base case --------------------------------------------------------
+// The reference tree keeps an FP32 copy of its points (fp32_pack,
+// fg_traverse.cu): coordinates relative to the centre of the point's anchor
+// (its maximal tree node with <= 32 points) and the weight.  A base item of
+// <= 32 points lies inside one anchor; the query coordinates are shifted to
+// the same centre in FP64 and rounded, the kernel is exp2 on the SFU
+// (ex2.approx) and the item sum accumulates in FP32.
+// Every term's relative error is bounded by fp32_item_rho (DESIGN.md "FP32
+// base case"); an item is evaluated this way only when that bound is at most
+// A.fp32_rho = phi * eps, so all FP32 items together err by at most
+// phi * eps * G(x_q).  The host runs the traversal's approximation rules
+// (summation_engine.py:157-188) with (1 - phi) * eps, so the total error stays
+// within eps * G (Theorem 2).
+template <int D>
+constexpr int fstride() { return (D + 1 + 3) & ~3; }
+
+__device__ __forceinline__ float ex2_approx(float v) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+// Upper bound rho on |S_fp32 - S| / S for the item (query block box `sq`,
+// reference points inside anchor `anc`), for every query of the block: each
+// term's relative error is at most
+//   da + 2^-18,  da = 2^-22 sqrt(D) M sqrt(a_max) / (sqrt2 h) + (4+D) 2^-24 a_max
+// (coordinate rounding with |coords| <= M about the anchor centre, the FP32
+// squared distance and scaling, ex2.approx (measured <= 2^-22.7,
+// tools/ex2_accuracy.cu), weight rounding and a 16-term FP32 sum per
+// accumulator), doubled for safety.  a_max = -log K_lo is the largest pair
+// exponent of the item.  Returns +inf when FP32 must not be used.
+template <int D>
+__device__ __forceinline__ double fp32_item_rho(const TravArgs &A, const double *sq, int anc,
+                                                double klo) {
+    const double a_max = -log(klo);
+    if (!(a_max < 80.0)) return CUDART_INF;  // keep every ex2 argument far from FTZ
+    const double *abox = A.r_box + (int64_t)anc * 2 * D;
+    const double *ac = A.r_c + (int64_t)anc * D;
+    double M = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double c = __ldg(ac + d);
+        M = fmax(M, fmax(fmax(fabs(__ldg(abox + d) - c), fabs(__ldg(abox + D + d) - c)),
+                         fmax(fabs(sq[d] - c), fabs(sq[D + d] - c))));
+    }
+    const double da = 0x1.0p-22 * sqrt((double)D) * M * sqrt(a_max) * A.inv_h * 0.7071067811865476 +
+                      (4.0 + D) * 0x1.0p-24 * a_max;
+    return 2.0 * (da + 0x1.0p-18);
+}
+
+// cp.async the FP32 records of base item `i` (fstride floats per point).
+template <int D>
+__device__ __forceinline__ void stage_points_f32(const float *__restrict__ pf, int ni_x,
+                                                 int ni_y, int i, float *buf) {
+    constexpr int F = fstride<D>();
+    const int lane = threadIdx.x & 31;
+    const int rs = __shfl_sync(kFull, ni_x, i);
+    const int rc = __shfl_sync(kFull, ni_y, i);
+    if (lane < rc) {
+        const float *src = pf + (int64_t)(rs + lane) * F;
+        float *dst = buf + lane * F;
+#pragma unroll
+        for (int q = 0; q < F / 4; q++) __pipeline_memcpy_async(dst + 4 * q, src + 4 * q, 16);
+    }
+    __pipeline_commit();
+}
+
+// FP32 evaluation of one staged item (rc <= 32 records); xq = this lane's
+// query relative to the item's anchor centre.
+template <int D>
+__device__ __forceinline__ double base_case_f32(const float (&xq)[D], const float *fb, int rc,
+                                                float ex2s) {
+    constexpr int F = fstride<D>();
+    float acc0 = 0.f, acc1 = 0.f;
+    int j = 0;
+    for (; j + 1 < rc; j += 2) {
+        const float *r0 = fb + j * F, *r1 = r0 + F;
+        float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float f0 = xq[d] - r0[d], f1 = xq[d] - r1[d];
+            d0 = fmaf(f0, f0, d0);
+            d1 = fmaf(f1, f1, d1);
+        }
+        acc0 = fmaf(ex2_approx(d0 * ex2s), r0[D], acc0);
+        acc1 = fmaf(ex2_approx(d1 * ex2s), r1[D], acc1);
+    }
+    if (j < rc) {
+        const float *r0 = fb + j * F;
+        float d0 = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float f0 = xq[d] - r0[d];
+            d0 = fmaf(f0, f0, d0);
+        }
+        acc0 = fmaf(ex2_approx(d0 * ex2s), r0[D], acc0);
+    }
+    return (double)acc0 + (double)acc1;
+}
+
 template <int D, int MINB>
 __global__ void __launch_bounds__(kTravThreads, MINB)
 traverse_kernel(const TravArgs A) {
@@ -229,6 +333,7 @@ traverse_kernel(const TravArgs A) {
     const int64_t gw = (int64_t)blockIdx.x * kTravWarps + wib;
     // per-warp shared memory: query box (lo, hi), centroid, local coefficients
     // and a double buffer of 2 x 32 staged reference points
+    // (FP32 items stage their fstride-float records into the same buffers)
     const int head = (3 * D + A.K + 1) & ~1;
     double *sq = smem + wib * (head + 64 * S);
     double *sqc = sq + 2 * D;
@@ -274,7 +379,7 @@ traverse_kernel(const TravArgs A) {
         const double gprime = A.prime_in ? A.prime_in[b] : 0.0;
         double pt_est = 0.0, pt_mass = 0.0;                    // per point
         double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
-        unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0;
+        unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
         int nser = 0;
 
         // root entry
@@ -420,12 +525,28 @@ traverse_kernel(const TravArgs A) {
 
             // ---- exhaustive base cases, eager (dito_base, :221-250).  Reference
             // leaves of <= 32 points are staged into shared memory with cp.async,
-            // double-buffered so the next item's points load while this one computes.
+            // double-buffered so the next item's points load while this one
+            // computes.  Items whose FP32 error bound fits the FP32 share of eps
+            // (decided lane-parallel, one item per lane) stage FP32 records.
             const unsigned small_mask = __ballot_sync(kFull, ni.y <= 32) & base_mask;
-            int bi = 0;
-            if (small_mask) {
-                stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(small_mask) - 1, sbuf);
+            unsigned f32_mask = 0;
+            int anc = 0;
+            if (A.fp32_rho > 0.0 && small_mask) {
+                bool use = false;
+                if (((small_mask >> lane) & 1u) && klo > 0.0) {
+                    anc = __ldg(A.r_anchor + ni.x);
+                    use = fp32_item_rho<D>(A, sq, anc, klo) <= A.fp32_rho;
+                }
+                f32_mask = __ballot_sync(kFull, use);
             }
+            auto stage = [&](int i, double *buf) {
+                if ((f32_mask >> i) & 1u)
+                    stage_points_f32<D>(A.r_pf, ni.x, ni.y, i, reinterpret_cast<float *>(buf));
+                else
+                    stage_points<D>(A.r_pw, ni.x, ni.y, i, buf);
+            };
+            int bi = 0;
+            if (small_mask) stage(__ffs(small_mask) - 1, sbuf);
             for (unsigned m = base_mask; m; m &= m - 1) {
                 const int i = __ffs(m) - 1;
                 const int rs = __shfl_sync(kFull, ni.x, i);
@@ -434,17 +555,36 @@ traverse_kernel(const TravArgs A) {
                 // every pair of this item has K >= K_lo: skip the exp range test
                 // when K_lo is a normal number
                 const double kli = __shfl_sync(kFull, klo, i);
+                const int ai = __shfl_sync(kFull, anc, i);
                 double contrib;
                 if ((small_mask >> i) & 1u) {
                     const unsigned rest = small_mask & ~((2u << i) - 1u);
                     if (rest) {
-                        stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1, sbuf + (bi ^ 1) * 32 * S);
+                        stage(__ffs(rest) - 1, sbuf + (bi ^ 1) * 32 * S);
                         __pipeline_wait_prior(1);
                     } else {
                         __pipeline_wait_prior(0);
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * 32 * S;
+                    if ((f32_mask >> i) & 1u) {
+                        float xq[D];
+#pragma unroll
+                        for (int d = 0; d < D; d++)
+                            xq[d] = (float)(x[d] - __ldg(A.r_c + (int64_t)ai * D + d));
+                        contrib = base_case_f32<D>(xq, reinterpret_cast<const float *>(bp), rc,
+                                                   A.ex2_scale);
+                        __syncwarp();
+                        bi ^= 1;
+                        pt_est += contrib;
+                        // |contrib - S| <= rho S with rho <= fp32_rho, so
+                        // contrib (1 - fp32_rho) <= S; the item's tokens stay unspent
+                        pt_mass += contrib * (1.0 - A.fp32_rho);
+                        if (A.use_tokens) tokens += wri;
+                        c_f32 += (unsigned)(qn * rc);
+                        c_base++;
+                        continue;
+                    }
                     contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, A.neg_inv, s_tab)
                                               : base_case<D, true>(x, bp, rc, A.neg_inv, s_tab);
                     __syncwarp();
@@ -529,6 +669,7 @@ traverse_kernel(const TravArgs A) {
             atomicAdd(A.counters + 4, (unsigned long long)c_dl);
             atomicAdd(A.counters + 5, (unsigned long long)c_h2l);
             atomicAdd(A.counters + 6, (unsigned long long)c_pairs);
+            atomicAdd(A.counters + 7, (unsigned long long)c_f32);
         }
         __syncwarp();
     }

@@ -91,9 +91,12 @@ __global__ void init_soa_kernel(const double *__restrict__ pts, const double *__
         double v = pts[i * dim + d];
         x[(int64_t)d * n + i] = v;
         if (!(v == v) || v == CUDART_INF || v == -CUDART_INF) atomicOr(bad, 2);
+        else if (fabs(v) > 0x1.0p60) atomicOr(bad, 4);
     }
     double wi = w ? w[i] : 1.0;
     if (!(wi > 0.0)) atomicOr(bad, 1);
+    // FP32 base cases need weights well inside the FP32 normal range
+    else if (wi < 0x1.0p-60 || wi > 0x1.0p60) atomicOr(bad, 4);
     wo[i] = wi;
     idx[i] = (int)i;
 }
@@ -321,6 +324,8 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     t.stride = packed_stride(dim);
     t.mom_valid = t.mom0_valid = false;
     t.qb_valid = false;
+    t.fp32_ok = !(bad & 4);
+    t.pf_valid = false;
     switch (dim) {
         case 1: return build_levels<1>(n, leaf, B, t);
         case 2: return build_levels<2>(n, leaf, B, t);

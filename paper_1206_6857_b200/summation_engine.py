@@ -43,7 +43,8 @@ class RunConfig:
 
 @dataclass
 class TraversalCounters:
-    """summation_engine.py:81-104, plus the number of exactly evaluated pairs."""
+    """summation_engine.py:81-104, plus the pairs evaluated exactly in FP64 and
+    the pairs evaluated in FP32 with a charged error bound."""
 
     pair_visits: int = 0
     base_cases: int = 0
@@ -52,6 +53,7 @@ class TraversalCounters:
     local_prunes: int = 0
     h2l_prunes: int = 0
     exact_pairs: int = 0
+    fp32_pairs: int = 0
 
     @property
     def prunes(self) -> int:
@@ -70,7 +72,7 @@ class TraversalCounters:
     @classmethod
     def _from_c(cls, c: _lib.fg_counters) -> "TraversalCounters":
         return cls(c.pair_visits, c.base_cases, c.fd_prunes, c.hermite_prunes, c.local_prunes,
-                   c.h2l_prunes, c.exact_pairs)
+                   c.h2l_prunes, c.exact_pairs, c.fp32_pairs)
 
 
 @dataclass

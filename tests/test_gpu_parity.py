@@ -321,3 +321,56 @@ def test_lscv_score_and_selection(fg, D):
             assert abs(s - (t1 - t2)) <= eps * (abs(t1) + abs(t2)) + 1e-12 * (t1 + t2)
     h_sel = select_bandwidth(pts, seed=0)
     assert abs(np.log(h_sel / float(g[f"D{D}_h_select"]))) <= 0.05
+
+
+# ------------------------------------------------------- FP32 base cases
+def _fp32_base(on):
+    from paper_1206_6857_b200 import _lib
+
+    _lib.call("fg_set_engine_params", 0, 0, 1 if on else 0)
+
+
+@pytest.mark.parametrize("D,offset,wspan", [(1, 0.0, 1.0), (2, 0.0, 1e3), (3, 1e3, 1.0),
+                                            (3, 0.0, 1e6), (5, 0.0, 1.0), (8, -50.0, 10.0)])
+def test_fp32_base_cases_within_eps(fg, oracle, D, offset, wspan):
+    """FP32 leaf evaluation keeps the eps contract,
+    including far from the origin (anchor-relative coordinates) and with
+    weights spanning many decades; disabling it gives FP64-only base cases."""
+    rng = np.random.default_rng(40 + D)
+    n = 6000
+    pts = rng.random((n, D)) * 0.5 + offset
+    w = np.exp(rng.uniform(0.0, np.log(wspan), n)) if wspan > 1 else np.ones(n)
+    h = {1: 0.002, 2: 0.01, 3: 0.03, 5: 0.08, 8: 0.15}[D]
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    t.refresh_moments(h, fg.default_plimit(D))
+    exact = oracle.naive_sum(pts, pts, w, h, threads=0)
+    try:
+        for on in (True, False):
+            _fp32_base(on)
+            for eps in (0.01, 1e-4):
+                for run in (fg.dfd_run, fg.dfdo_run, fg.dito_run):
+                    res = run(fg.RunConfig(bandwidth=h, epsilon=eps), t, t)
+                    assert oracle.max_rel_error(res.values, exact) <= eps, (on, eps, run)
+                    if not on:
+                        assert res.counters.fp32_pairs == 0
+                    elif eps == 0.01:
+                        assert res.counters.fp32_pairs > 0, run
+            _fp32_base(True)
+            res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=0.0), t, t)
+            assert res.counters.fp32_pairs == 0  # eps = 0 is FP64 only
+            assert oracle.max_rel_error(res.values, exact) <= 1e-12
+    finally:
+        _fp32_base(True)
+
+
+def test_fp32_base_cases_off_outside_fp32_range(fg, oracle):
+    """Weights outside the FP32 base case's safe range fall back to FP64."""
+    rng = np.random.default_rng(5)
+    pts = rng.random((3000, 3))
+    w = np.full(3000, 1e-30)
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    t.refresh_moments(0.03, fg.default_plimit(3))
+    res = fg.dito_run(fg.RunConfig(bandwidth=0.03, epsilon=0.01), t, t)
+    assert res.counters.fp32_pairs == 0 and res.counters.exact_pairs > 0
+    exact = oracle.naive_sum(pts, pts, w, 0.03, threads=0)
+    assert oracle.max_rel_error(res.values, exact) <= 0.01

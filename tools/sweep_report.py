@@ -29,7 +29,7 @@ def main():
     import oracle
 
     if args.ref_leaf:
-        _lib.call("fg_set_engine_params", args.ref_leaf, 0)
+        _lib.call("fg_set_engine_params", args.ref_leaf, 0, -1)
     wl = config(args.config, scale=args.scale)
     qp = wl.query_points()
     t0 = time.perf_counter()
@@ -58,6 +58,7 @@ def main():
         line = dict(h=round(h, 6), kern_ms=round(res.seconds * 1e3, 3),
                     wall_ms=round(t_run * 1e3, 2), refresh_ms=round(t_ref * 1e3, 2),
                     err=float(f"{err:.3e}"), exact_share=float(f"{share:.4f}"),
+                    fp32_share=float(f"{c.fp32_pairs / (wl.m * wl.n):.4f}"),
                     visits=c.pair_visits, base=c.base_cases, fd=c.fd_prunes,
                     dh=c.hermite_prunes, dl=c.local_prunes, h2l=c.h2l_prunes,
                     pair_rate=float(f"{c.exact_pairs / max(res.seconds, 1e-9):.3e}"))

@@ -4,6 +4,6 @@ import sys,json
 for l in sys.stdin:
     l=l.strip()
     if l.startswith('{'):
-        d=json.loads(l); print(d['h'], d['kern_ms'], d['err'], d['exact_share'], d['visits'], d['dh'], d.get('naive_ms',''))
+        d=json.loads(l); print(d['h'], d['kern_ms'], d['err'], d['exact_share'], d['fp32_share'], d['visits'], d['dh'], d.get('naive_ms',''))
     else: print(l)
 "
