@@ -253,7 +253,7 @@ def run_ours(args):
     flush = torch.empty(int(512 * 2**20) // 4, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
-    stats = {"kernel_s": 0.0, "pairs": 0, "visits": 0}
+    stats = {"kernel_s": 0.0, "pairs": 0, "pairs32": 0, "visits": 0}
 
     def step(record=True):
         vals_d.zero_()
@@ -270,6 +270,7 @@ def run_ours(args):
             if record:
                 stats["kernel_s"] += res.seconds
                 stats["pairs"] += res.counters.exact_pairs
+                stats["pairs32"] += res.counters.fp32_pairs
                 stats["visits"] += res.counters.pair_visits
         del tree
 
@@ -303,19 +304,37 @@ def run_ours(args):
     pairs_eff = wl.m * wl.n * len(wl.bandwidths)
     value = pairs_eff * args.steps / total
 
-    # roofline of the dominant kernel (fused traversal + base-case kernel)
+    # roofline of the dominant kernel (fused traversal + base-case kernel).
+    # Its pair work has two legs: FP64 pairs bound by
+    # the DFMA pipe at F(D) flops per pair, FP32 pairs bound by the SFU at one
+    # ex2 per pair.  peak = the pair rate of the ideal kernel for this step's
+    # FP64/FP32 mix; achieved = pairs evaluated / kernel time.
     peak = np.zeros(1)
     _lib.call("fg_fp64_peak", _lib.ptr(peak))
     peak_tf = float(peak[0])
-    achieved_tf = stats["pairs"] * F_OF_D[D] / stats["kernel_s"] / 1e12 if stats["kernel_s"] else 0.0
-    roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak_tf if peak_tf else None,
+    ex2 = np.zeros(1)
+    _lib.call("fg_ex2_peak", _lib.ptr(ex2))
+    ex2_gops = float(ex2[0])
+    n64, n32, ks = stats["pairs"], stats["pairs32"], stats["kernel_s"]
+    ideal_s = n64 * F_OF_D[D] / (peak_tf * 1e12) + n32 / (ex2_gops * 1e9)
+    achieved = (n64 + n32) / ks / 1e9 if ks else 0.0
+    peak_mix = (n64 + n32) / ideal_s / 1e9 if ideal_s else None
+    roofline = {"bound": "fp64+sfu", "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
+                "frac": achieved / peak_mix if peak_mix else None,
                 "traffic": profiled_traffic(),
-                "kernel": "traverse_kernel<3> (fused traversal + exact base cases)",
-                "flops_per_pair": F_OF_D[D],
-                "kernel_share_of_step": stats["kernel_s"] / total if total else None,
-                "peak_source": "measured: DFMA microbenchmark fg_fp64_peak (burst)",
-                "exact_pair_share": stats["pairs"] / (pairs_eff * args.steps)}
+                "kernel": f"traverse_kernel<{D}> (fused traversal + leaf base cases)",
+                "legs": {"fp64": {"pairs_per_step": n64 / args.steps,
+                                  "flops_per_pair": F_OF_D[D], "peak_tflops": peak_tf,
+                                  "achieved_tflops_over_kernel_time":
+                                      n64 * F_OF_D[D] / ks / 1e12 if ks else 0.0},
+                         "fp32": {"pairs_per_step": n32 / args.steps, "ex2_per_pair": 1,
+                                  "peak_ex2_gops": ex2_gops}},
+                "kernel_share_of_step": ks / total if total else None,
+                "visits_per_s_in_kernel": stats["visits"] / ks if ks else None,
+                "peak_source": "measured: DFMA microbenchmark fg_fp64_peak and ex2.approx "
+                               "microbenchmark fg_ex2_peak (burst)",
+                "pair_share": {"fp64": n64 / (pairs_eff * args.steps),
+                               "fp32": n32 / (pairs_eff * args.steps)}}
 
     # end to end through the public API with host buffers
     e2e = None
@@ -360,7 +379,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64+f32",
+            "dtype_note": "FP64 traversal, bounds, series and results; leaf pairs in FP32 where "
+                          "their rigorous error bound fits a reserved 5% of eps (DESIGN.md)",
             "data": "synthetic (seeded; SURVEY Appendix C)",
             "config": {"workload": describe(wl), "epsilon": wl.epsilon,
                        "bandwidths": len(wl.bandwidths), "parallelism": f"query-blocks x{world}",
@@ -371,7 +393,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "detail": {"kernel_ms_per_step": 1e3 * stats["kernel_s"] / args.steps,
                        "visits_per_step": stats["visits"] / args.steps,
-                       "exact_pairs_per_step": stats["pairs"] / args.steps},
+                       "exact_pairs_per_step": stats["pairs"] / args.steps,
+                       "fp32_pairs_per_step": stats["pairs32"] / args.steps},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

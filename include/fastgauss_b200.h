@@ -57,10 +57,13 @@ typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_inde
 
 int fg_version(void);
 const char *fg_last_error(void);
-/* diagnostics: number of kernels this library has launched so far, and a
+/* diagnostics: number of kernels this library has launched so far, and
  * measured FP64 FMA throughput (TFLOP/s) on the current device */
 int fg_launch_count(int64_t *count);
 int fg_fp64_peak(double *tflops);
+/* measured ex2.approx.f32 (SFU) throughput, Gop/s: the FP32 base case's
+ * per-pair limit (one ex2 per pair) */
+int fg_ex2_peak(double *gops);
 /* stream: a cudaStream_t (NULL = legacy default stream) */
 int fg_set_stream(void *stream);
 int fg_set_device(int device);

@@ -52,6 +52,20 @@ __global__ void dfma_peak_kernel(double *out, int iters, double a, double b) {
     const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
     if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
+// SFU throughput probe: independent ex2.approx chains (the FP32 base case's
+// per-pair limiter), results folded so the chains stay live.
+__global__ void ex2_peak_kernel(float *out, int iters) {
+    float x0 = -1e-3f * threadIdx.x, x1 = x0 - 0.1f, x2 = x0 - 0.2f, x3 = x0 - 0.3f;
+    float x4 = x0 - 0.4f, x5 = x0 - 0.5f, x6 = x0 - 0.6f, x7 = x0 - 0.7f;
+#define FG_EX2(v) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(v))
+    for (int i = 0; i < iters; i++) {
+        FG_EX2(x0); FG_EX2(x1); FG_EX2(x2); FG_EX2(x3);
+        FG_EX2(x4); FG_EX2(x5); FG_EX2(x6); FG_EX2(x7);
+    }
+#undef FG_EX2
+    const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 12345.678f) out[0] = s;
+}
 cudaStream_t stream() { return g_stream; }
 
 bool is_device_ptr(const void *ptr) {
@@ -286,6 +300,34 @@ int fg_fp64_peak(double *tflops) {
     cudaEventDestroy(e1);
     const double flops = 2.0 * 8.0 * (double)iters * threads * blocks;
     *tflops = flops / (best * 1e-3) / 1e12;
+    return FG_OK;
+}
+
+int fg_ex2_peak(double *gops) {
+    FG_REQUIRE(gops, FG_EINVAL, "null pointer");
+    int dev = 0, sms = 0;
+    FG_CUDA_TRY(cudaGetDevice(&dev));
+    FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DBuf sink;
+    FG_TRY(sink.reserve(sizeof(float)));
+    const int threads = 256, blocks = sms * 8, iters = 1 << 12;
+    cudaEvent_t e0, e1;
+    FG_CUDA_TRY(cudaEventCreate(&e0));
+    FG_CUDA_TRY(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; rep++) {
+        cudaEventRecord(e0, stream());
+        count_launch();
+        ex2_peak_kernel<<<blocks, threads, 0, stream()>>>(sink.as<float>(), iters);
+        cudaEventRecord(e1, stream());
+        FG_CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *gops = 8.0 * (double)iters * threads * blocks / (best * 1e-3) / 1e9;
     return FG_OK;
 }
 

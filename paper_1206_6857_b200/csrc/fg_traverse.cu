@@ -377,7 +377,15 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         A.floor_c = floor_c;
     }
     // per warp: query box + centroid + local coefficients, then 2 x 32 staged points
-    smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 64 * packed_stride(D)) * kTravWarps;
+    {
+        static const int f32d[9] = {0,
+                                    f32_smem_doubles<1>(), f32_smem_doubles<2>(),
+                                    f32_smem_doubles<3>(), f32_smem_doubles<4>(),
+                                    f32_smem_doubles<5>(), f32_smem_doubles<6>(),
+                                    f32_smem_doubles<7>(), f32_smem_doubles<8>()};
+        smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 64 * packed_stride(D) + f32d[D]) *
+               kTravWarps;
+    }
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
     FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * 8));
     FG_CUDA_TRY(cudaMemsetAsync(g_scr.counters.p, 0, sizeof(unsigned long long) * 8, stream()));

@@ -222,19 +222,35 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
 
 // ---- FP32 base case --------------------------------------------------------
 // The reference tree keeps an FP32 copy of its points (fp32_pack,
-// fg_traverse.cu): coordinates relative to the centre of the point's anchor
-// (its maximal tree node with <= 32 points) and the weight.  A base item of
-// <= 32 points lies inside one anchor; the query coordinates are shifted to
-// the same centre in FP64 and rounded, the kernel is exp2 on the SFU
-// (ex2.approx) and the item sum accumulates in FP32.
-// Every term's relative error is bounded by fp32_item_rho (DESIGN.md "FP32
-// base case"); an item is evaluated this way only when that bound is at most
-// A.fp32_rho = phi * eps, so all FP32 items together err by at most
-// phi * eps * G(x_q).  The host runs the traversal's approximation rules
-// (summation_engine.py:157-188) with (1 - phi) * eps, so the total error stays
-// within eps * G (Theorem 2).
+// fg_traverse.cu): coordinates relative to the centre c_a of the point's
+// anchor (its maximal tree node with <= 32 points) and the weight.  A base
+// item of <= 32 points lies inside one anchor.  All FP32 items of a traversal
+// step are evaluated as ONE batch: their records are staged back to back
+// (each item padded to a multiple of 4 with zero records) in transposed
+// layout, every group of 4 points carries its item's offset
+// delta = fl(c_a - c_b) (c_b = the query block's centroid), and each lane
+// streams the whole batch with its query xf = fl(x - c_b) shifted to
+// xq = fl(xf - delta): packed FP32 pairs (FADD2/FFMA2/FMUL2), exp2 on the SFU
+// (ex2.approx), four FP32 accumulators.
+//
+// The batch error is bounded by rho S + abs (fp32_item_bound; DESIGN.md
+// "FP32 base case"), S the exact sum.  An item joins only when rho <=
+// A.fp32_rho = phi * eps -- all FP32 items together then err by at most
+// phi * eps * G(x_q) through their relative parts -- and when its own token
+// share covers abs, which is charged through the token rule
+// (summation_engine.py:157-188) like a prune's error.  The host runs the
+// traversal's approximation rules with (1 - phi) * eps, so the total error
+// stays within eps * G (Theorem 2).
 template <int D>
 constexpr int fstride() { return (D + 1 + 3) & ~3; }
+// points per staged batch and floats per group offset record
+template <int D>
+constexpr int f32_cap() { return D <= 4 ? 256 : 128; }
+template <int D>
+constexpr int f32_fd() { return (D + 3) & ~3; }
+// per-warp shared memory of the batch, in doubles
+template <int D>
+constexpr int f32_smem_doubles() { return (f32_cap<D>() * (D + 1) + f32_cap<D>() / 4 * f32_fd<D>()) / 2; }
 
 __device__ __forceinline__ float ex2_approx(float v) {
     float r;
@@ -242,82 +258,119 @@ __device__ __forceinline__ float ex2_approx(float v) {
     return r;
 }
 
-// Upper bound rho on |S_fp32 - S| / S for the item (query block box `sq`,
-// reference points inside anchor `anc`), for every query of the block: each
-// term's relative error is at most
-//   da + 2^-18,  da = 2^-22 sqrt(D) M sqrt(a_max) / (sqrt2 h) + (4+D) 2^-24 a_max
-// (coordinate rounding with |coords| <= M about the anchor centre, the FP32
-// squared distance and scaling, ex2.approx (measured <= 2^-22.7,
-// tools/ex2_accuracy.cu), weight rounding and a 16-term FP32 sum per
-// accumulator), doubled for safety.  a_max = -log K_lo is the largest pair
-// exponent of the item.  Returns +inf when FP32 must not be used.
+// Error bound |S_fp32 - S| <= rho S + abs for one item (query block box `sq`
+// with centroid `sqc`, reference points inside anchor `anc`, weight wr), for
+// every query of the block.  With M bounding |x - c_b|, |c_a - c_b|,
+// |x - c_a| and |y - c_a| per coordinate, each coordinate difference carries
+// at most 4 u M of rounding (u = 2^-24) before its own rounding, so a term
+// with exponent a <= a_c = min(a_max, 80) has relative error at most
+//   da + 2^-17,  da = 2^-21 sqrt(D) M sqrt(a_c) / (sqrt2 h) + (4+D) u a_c
+// (the FP32 difference, squared distance and scaling; ex2.approx, measured
+// <= 2^-22.7 by tools/ex2_accuracy.cu; weight rounding; <= 63 additions per
+// FP32 accumulator); rho doubles that for safety.  a_max = -log K_lo is the
+// item's largest pair exponent (+inf when K_lo underflows).  Terms beyond a_c
+// (ex2 may flush them to zero) are worth at most w e^-80 and so are their
+// computed values: abs = 2 wr e^-80 when a_max > 80, plus 2^-140 for
+// subnormal rounding in the FP32 accumulation.
 template <int D>
-__device__ __forceinline__ double fp32_item_rho(const TravArgs &A, const double *sq, int anc,
-                                                double klo) {
-    const double a_max = -log(klo);
-    if (!(a_max < 80.0)) return CUDART_INF;  // keep every ex2 argument far from FTZ
+__device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const double *sq, int anc,
+                                                  double klo, double wr, double &abs_err) {
+    const double a_max = klo > 0.0 ? -log(klo) : CUDART_INF;
+    const double a_c = fmin(a_max, 80.0);
+    abs_err = (a_max > 80.0 ? 2.0 * wr * 1.8048513878454153e-35 : 0.0) + 0x1.0p-140;
     const double *abox = A.r_box + (int64_t)anc * 2 * D;
     const double *ac = A.r_c + (int64_t)anc * D;
     double M = 0.0;
 #pragma unroll
     for (int d = 0; d < D; d++) {
-        const double c = __ldg(ac + d);
+        const double c = __ldg(ac + d), cb = sq[2 * D + d];
+        const double qlo = sq[d], qhi = sq[D + d];
         M = fmax(M, fmax(fmax(fabs(__ldg(abox + d) - c), fabs(__ldg(abox + D + d) - c)),
-                         fmax(fabs(sq[d] - c), fabs(sq[D + d] - c))));
+                         fmax(fabs(qlo - c), fabs(qhi - c))));
+        M = fmax(M, fmax(fabs(c - cb), fmax(fabs(qlo - cb), fabs(qhi - cb))));
     }
-    const double da = 0x1.0p-22 * sqrt((double)D) * M * sqrt(a_max) * A.inv_h * 0.7071067811865476 +
-                      (4.0 + D) * 0x1.0p-24 * a_max;
-    return 2.0 * (da + 0x1.0p-18);
+    const double da = 0x1.0p-21 * sqrt((double)D) * M * sqrt(a_c) * A.inv_h * 0.7071067811865476 +
+                      (4.0 + D) * 0x1.0p-24 * a_c;
+    return 2.0 * (da + 0x1.0p-17);
 }
 
-// cp.async the FP32 records of base item `i` (fstride floats per point).
+// packed FP32 pairs (sm_100 FADD2 / FFMA2 / FMUL2, round-to-nearest per lane)
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    return (unsigned long long)__float_as_uint(lo) |
+           ((unsigned long long)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float f2_hi(unsigned long long v) {
+    return __uint_as_float((unsigned)(v >> 32));
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b,
+                                                     unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long f2_ex2(unsigned long long v) {
+    return f2_pack(ex2_approx(f2_lo(v)), ex2_approx(f2_hi(v)));
+}
+
+// Stream one staged batch of `total` points (a multiple of 4): component c of
+// point j at fst[c * CAP + j], group g's offset record at gd[g * FD].
 template <int D>
-__device__ __forceinline__ void stage_points_f32(const float *__restrict__ pf, int ni_x,
-                                                 int ni_y, int i, float *buf) {
-    constexpr int F = fstride<D>();
+__device__ __forceinline__ double batch_f32(const float (&xf)[D], const float *fst,
+                                            const float *gd, int total, float ex2s) {
+    constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>();
+    const unsigned long long s2 = f2_pack(ex2s, ex2s);
+    unsigned long long acc_a = 0ull, acc_b = 0ull;
+    for (int j = 0; j < total; j += 4) {
+        float dl[FD];
+#pragma unroll
+        for (int k = 0; k < FD; k += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(gd + (j >> 2) * FD + k);
+            dl[k] = v.x; dl[k + 1] = v.y; dl[k + 2] = v.z; dl[k + 3] = v.w;
+        }
+        unsigned long long da, db;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float q = xf[d] - dl[d];
+            const unsigned long long q2 = f2_pack(q, q);
+            const float4 c = *reinterpret_cast<const float4 *>(fst + d * CAP + j);
+            const unsigned long long fa = f2_sub(q2, f2_pack(c.x, c.y));
+            const unsigned long long fb = f2_sub(q2, f2_pack(c.z, c.w));
+            if (d == 0) {
+                da = f2_mul(fa, fa);
+                db = f2_mul(fb, fb);
+            } else {
+                da = f2_fma(fa, fa, da);
+                db = f2_fma(fb, fb, db);
+            }
+        }
+        const float4 w = *reinterpret_cast<const float4 *>(fst + D * CAP + j);
+        acc_a = f2_fma(f2_ex2(f2_mul(da, s2)), f2_pack(w.x, w.y), acc_a);
+        acc_b = f2_fma(f2_ex2(f2_mul(db, s2)), f2_pack(w.z, w.w), acc_b);
+    }
+    return ((double)f2_lo(acc_a) + (double)f2_hi(acc_a)) +
+           ((double)f2_lo(acc_b) + (double)f2_hi(acc_b));
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v) {
     const int lane = threadIdx.x & 31;
-    const int rs = __shfl_sync(kFull, ni_x, i);
-    const int rc = __shfl_sync(kFull, ni_y, i);
-    if (lane < rc) {
-        const float *src = pf + (int64_t)(rs + lane) * F;
-        float *dst = buf + lane * F;
+    int s = v;
 #pragma unroll
-        for (int q = 0; q < F / 4; q++) __pipeline_memcpy_async(dst + 4 * q, src + 4 * q, 16);
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += t;
     }
-    __pipeline_commit();
-}
-
-// FP32 evaluation of one staged item (rc <= 32 records); xq = this lane's
-// query relative to the item's anchor centre.
-template <int D>
-__device__ __forceinline__ double base_case_f32(const float (&xq)[D], const float *fb, int rc,
-                                                float ex2s) {
-    constexpr int F = fstride<D>();
-    float acc0 = 0.f, acc1 = 0.f;
-    int j = 0;
-    for (; j + 1 < rc; j += 2) {
-        const float *r0 = fb + j * F, *r1 = r0 + F;
-        float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            const float f0 = xq[d] - r0[d], f1 = xq[d] - r1[d];
-            d0 = fmaf(f0, f0, d0);
-            d1 = fmaf(f1, f1, d1);
-        }
-        acc0 = fmaf(ex2_approx(d0 * ex2s), r0[D], acc0);
-        acc1 = fmaf(ex2_approx(d1 * ex2s), r1[D], acc1);
-    }
-    if (j < rc) {
-        const float *r0 = fb + j * F;
-        float d0 = 0.f;
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            const float f0 = xq[d] - r0[d];
-            d0 = fmaf(f0, f0, d0);
-        }
-        acc0 = fmaf(ex2_approx(d0 * ex2s), r0[D], acc0);
-    }
-    return (double)acc0 + (double)acc1;
+    return s - v;
 }
 
 template <int D, int MINB>
@@ -331,14 +384,16 @@ traverse_kernel(const TravArgs A) {
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kTravWarps + wib;
-    // per-warp shared memory: query box (lo, hi), centroid, local coefficients
-    // and a double buffer of 2 x 32 staged reference points
-    // (FP32 items stage their fstride-float records into the same buffers)
+    // per-warp shared memory: query box (lo, hi), centroid, local coefficients,
+    // a double buffer of 2 x 32 staged FP64 reference points, then the FP32
+    // batch (transposed records and per-group offsets)
     const int head = (3 * D + A.K + 1) & ~1;
-    double *sq = smem + wib * (head + 64 * S);
+    double *sq = smem + wib * (head + 64 * S + f32_smem_doubles<D>());
     double *sqc = sq + 2 * D;
     double *loc = sq + 3 * D;
     double *sbuf = sq + head;
+    float *fst = reinterpret_cast<float *>(sbuf + 64 * S);
+    float *gdl = fst + f32_cap<D>() * (D + 1);
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;
@@ -523,31 +578,89 @@ traverse_kernel(const TravArgs A) {
             fsum = fsum - batch_sum + warp_sum(child_sum);
             if (fsum < 0.0) fsum = 0.0;
 
-            // ---- exhaustive base cases, eager (dito_base, :221-250).  Reference
-            // leaves of <= 32 points are staged into shared memory with cp.async,
-            // double-buffered so the next item's points load while this one
-            // computes.  Items whose FP32 error bound fits the FP32 share of eps
-            // (decided lane-parallel, one item per lane) stage FP32 records.
+            // ---- exhaustive base cases, eager (dito_base, :221-250).  Items whose
+            // FP32 error bound fits (decided lane-parallel, one item per lane) run
+            // as one FP32 batch; the rest (FP64) are staged one by one into shared
+            // memory with cp.async, double-buffered so the next item's points load
+            // while this one computes (leaves of > 32 points read global memory).
             const unsigned small_mask = __ballot_sync(kFull, ni.y <= 32) & base_mask;
             unsigned f32_mask = 0;
             int anc = 0;
-            if (A.fp32_rho > 0.0 && small_mask) {
+            double abs32 = 0.0;
+            if (A.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
                 bool use = false;
-                if (((small_mask >> lane) & 1u) && klo > 0.0) {
+                if ((small_mask >> lane) & 1u) {
                     anc = __ldg(A.r_anchor + ni.x);
-                    use = fp32_item_rho<D>(A, sq, anc, klo) <= A.fp32_rho;
+                    const double rho = fp32_item_bound<D>(A, sq, anc, klo, WR, abs32);
+                    use = rho <= A.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
             }
-            auto stage = [&](int i, double *buf) {
-                if ((f32_mask >> i) & 1u)
-                    stage_points_f32<D>(A.r_pf, ni.x, ni.y, i, reinterpret_cast<float *>(buf));
-                else
-                    stage_points<D>(A.r_pw, ni.x, ni.y, i, buf);
-            };
+            if (f32_mask) {
+                constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>(), F = fstride<D>();
+                const bool mine = (f32_mask >> lane) & 1u;
+                const int rc4 = mine ? ((ni.y + 3) & ~3) : 0;
+                const int off = warp_excl_scan(rc4);
+                float dl[D];
+                if (mine) {
+#pragma unroll
+                    for (int d = 0; d < D; d++)
+                        dl[d] = (float)(__ldg(A.r_c + (int64_t)anc * D + d) - sqc[d]);
+                }
+                if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
+                const double abs_sum = warp_sum(mine ? abs32 : 0.0);
+                c_f32 += (unsigned)qn * (unsigned)warp_sum(mine ? ni.y : 0);
+                c_base += __popc(f32_mask);
+                float xf[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) xf[d] = (float)(x[d] - sqc[d]);
+                double sum32 = 0.0;
+                unsigned todo = f32_mask;
+                while (todo) {
+                    // the next run of whole items that fits the staging area
+                    const int base = __shfl_sync(kFull, off, __ffs(todo) - 1);
+                    const unsigned batch =
+                        __ballot_sync(kFull, ((todo >> lane) & 1u) && off - base + rc4 <= CAP);
+                    todo &= ~batch;
+                    if ((batch >> lane) & 1u) {
+                        for (int g = (off - base) >> 2; g < (off - base + rc4) >> 2; g++) {
+#pragma unroll
+                            for (int d = 0; d < D; d++) gdl[g * FD + d] = dl[d];
+                        }
+                    }
+                    int total = 0;
+                    for (unsigned m = batch; m; m &= m - 1) {
+                        const int i = __ffs(m) - 1;
+                        const int rs = __shfl_sync(kFull, ni.x, i);
+                        const int rc = __shfl_sync(kFull, ni.y, i);
+                        const int o = __shfl_sync(kFull, off, i) - base;
+                        if (lane < rc) {
+                            const float *src = A.r_pf + (int64_t)(rs + lane) * F;
+#pragma unroll
+                            for (int c = 0; c <= D; c++)
+                                __pipeline_memcpy_async(fst + c * CAP + o + lane, src + c, 4);
+                        } else if (lane < ((rc + 3) & ~3)) {
+#pragma unroll
+                            for (int c = 0; c <= D; c++) fst[c * CAP + o + lane] = 0.f;
+                        }
+                        total = o + ((rc + 3) & ~3);
+                    }
+                    __pipeline_commit();
+                    __pipeline_wait_prior(0);
+                    __syncwarp();
+                    sum32 += batch_f32<D>(xf, fst, gdl, total, A.ex2_scale);
+                    __syncwarp();
+                }
+                pt_est += sum32;
+                // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho, so
+                // sum32 (1 - fp32_rho) - sum(abs) <= S
+                pt_mass += fmax(sum32 * (1.0 - A.fp32_rho) - abs_sum, 0.0);
+            }
+            const unsigned base64 = base_mask & ~f32_mask;
+            const unsigned small64 = small_mask & ~f32_mask;
             int bi = 0;
-            if (small_mask) stage(__ffs(small_mask) - 1, sbuf);
-            for (unsigned m = base_mask; m; m &= m - 1) {
+            if (small64) stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(small64) - 1, sbuf);
+            for (unsigned m = base64; m; m &= m - 1) {
                 const int i = __ffs(m) - 1;
                 const int rs = __shfl_sync(kFull, ni.x, i);
                 const int rc = __shfl_sync(kFull, ni.y, i);
@@ -555,36 +668,18 @@ traverse_kernel(const TravArgs A) {
                 // every pair of this item has K >= K_lo: skip the exp range test
                 // when K_lo is a normal number
                 const double kli = __shfl_sync(kFull, klo, i);
-                const int ai = __shfl_sync(kFull, anc, i);
                 double contrib;
-                if ((small_mask >> i) & 1u) {
-                    const unsigned rest = small_mask & ~((2u << i) - 1u);
+                if ((small64 >> i) & 1u) {
+                    const unsigned rest = small64 & ~((2u << i) - 1u);
                     if (rest) {
-                        stage(__ffs(rest) - 1, sbuf + (bi ^ 1) * 32 * S);
+                        stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1,
+                                        sbuf + (bi ^ 1) * 32 * S);
                         __pipeline_wait_prior(1);
                     } else {
                         __pipeline_wait_prior(0);
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * 32 * S;
-                    if ((f32_mask >> i) & 1u) {
-                        float xq[D];
-#pragma unroll
-                        for (int d = 0; d < D; d++)
-                            xq[d] = (float)(x[d] - __ldg(A.r_c + (int64_t)ai * D + d));
-                        contrib = base_case_f32<D>(xq, reinterpret_cast<const float *>(bp), rc,
-                                                   A.ex2_scale);
-                        __syncwarp();
-                        bi ^= 1;
-                        pt_est += contrib;
-                        // |contrib - S| <= rho S with rho <= fp32_rho, so
-                        // contrib (1 - fp32_rho) <= S; the item's tokens stay unspent
-                        pt_mass += contrib * (1.0 - A.fp32_rho);
-                        if (A.use_tokens) tokens += wri;
-                        c_f32 += (unsigned)(qn * rc);
-                        c_base++;
-                        continue;
-                    }
                     contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, A.neg_inv, s_tab)
                                               : base_case<D, true>(x, bp, rc, A.neg_inv, s_tab);
                     __syncwarp();

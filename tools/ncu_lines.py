@@ -32,7 +32,11 @@ for r in csv.reader(io.StringIO(out)):
         inst = int(d.get("Instructions Executed", "0") or 0)
     except ValueError:
         continue
-    rows.append((samp, inst, fname, r[0], r[1][:90]))
+    st = sorted(((int(d[k] or 0), k[6:]) for k in hdr
+                 if k.startswith("stall_") and "Not Issued" not in k and (d.get(k) or "0").isdigit()),
+                reverse=True)[:2]
+    why = ",".join(f"{k}:{100*v/max(samp,1):.0f}%" for v, k in st if v)
+    rows.append((samp, inst, fname, r[0], r[1][:70] + "  [" + why + "]"))
 tot_s = sum(r[0] for r in rows) or 1
 tot_i = sum(r[1] for r in rows) or 1
 print(f"total samples {tot_s}, warp instructions {tot_i:.3e}")
