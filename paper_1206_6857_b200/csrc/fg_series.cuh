@@ -115,7 +115,7 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
     double lad[D][P];
 #pragma unroll
     for (int d = 0; d < D; d++) {
-        const double t = (x[d] - __ldg(c + d)) * inv_sc;
+        const double t = (x[d] - c[d]) * inv_sc;
         const double g = exp(-t * t);
         lad[d][0] = g;
         if (P > 1) lad[d][1] = 2.0 * t * g;
@@ -133,7 +133,7 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
             double v = lad[0][G.dig[k][0]];
 #pragma unroll
             for (int d = 1; d < D; d++) v *= lad[d][G.dig[k][d]];
-            acc = fma(v, __ldg(A + k), acc);
+            acc = fma(v, A[k], acc);
         }
     }
     return acc;
@@ -164,7 +164,7 @@ __device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
     double lad[3][P];
 #pragma unroll
     for (int d = 0; d < 3; d++) {
-        const double t = (x[d] - __ldg(c + d)) * inv_sc;
+        const double t = (x[d] - c[d]) * inv_sc;
         const double g = expf(-t * t);
         lad[d][0] = g;
         if (P > 1) lad[d][1] = 2.0 * t * g;
@@ -180,7 +180,7 @@ __device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
             double t2 = 0.0;
 #pragma unroll
             for (int cc = 0; a + b + cc < P; cc++) {
-                const double coef = (a + b + cc < p) ? __ldg(A + I.idx[a][b][cc]) : 0.0;
+                const double coef = (a + b + cc < p) ? A[I.idx[a][b][cc]] : 0.0;
                 t2 = fma(coef, lad[2][cc], t2);
             }
             t1 = fma(t2, lad[1][b], t1);

@@ -435,7 +435,7 @@ traverse_kernel(const TravArgs A) {
         double pt_est = 0.0, pt_mass = 0.0;                    // per point
         double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
-        int nser = 0;
+        int nh = 0, no = 0;  // deferred series items: Hermite from the front, others from the back
 
         // root entry
         double fsum;  // sum over the frontier of W_R * K_lo
@@ -515,7 +515,7 @@ traverse_kernel(const TravArgs A) {
             // ---- series prunes (summation_engine.py:352-399); the evaluation
             // itself is deferred to the end of the block (it never feeds a bound)
             unsigned ser_mask = 0;
-            if (A.use_series && nser + 32 <= A.stack_cap) {
+            if (A.use_series && nh + no + 32 <= A.stack_cap) {
                 int meth = 0, p = 0;
                 double bound = 0.0;
                 if (act && !fd) {
@@ -537,11 +537,16 @@ traverse_kernel(const TravArgs A) {
                 const double sreq = cand ? required_tokens(WR, bound, tok_scale)
                                          : CUDART_INF;
                 ser_mask = admit(cand, sreq, tokens);
+                const unsigned hm = __ballot_sync(kFull, ((ser_mask >> lane) & 1u) && meth == 2);
+                const unsigned om = ser_mask & ~hm;
                 if ((ser_mask >> lane) & 1u) {
                     settled = WR * klo;
-                    sl[nser + __popc(ser_mask & lt_mask)] = make_int2(node, p | (meth << 8));
+                    const int slot = meth == 2 ? nh + __popc(hm & lt_mask)
+                                               : A.stack_cap - 1 - no - __popc(om & lt_mask);
+                    sl[slot] = make_int2(node, p | (meth << 8));
                 }
-                nser += __popc(ser_mask);
+                nh += __popc(hm);
+                no += __popc(om);
             }
             node_mass += warp_sum(settled);
             node_est += warp_sum(est_add);
@@ -700,43 +705,70 @@ traverse_kernel(const TravArgs A) {
         // ---- deferred series contributions, then the post pass (dito_post, :253-281)
         unsigned c_dh = 0, c_dl = 0, c_h2l = 0;
         bool local_used = false;
-        if (nser > 0) {
+        if (nh + no > 0) {
             double qc[D];
 #pragma unroll
             for (int d = 0; d < D; d++) qc[d] = sqc[d];
-            for (int i = 0; i < nser; i++) {
-                const int2 e = sl[i];
+            // Hermite items (EVALM): each item's moments and centre are staged
+            // through a cp.async ring in the (now idle) FP64 staging buffer,
+            // kRing - 1 items ahead of the one being evaluated
+            constexpr int PF = default_plimit_c(D);
+            constexpr int kRing = 4;
+            const int slot = (A.K + D + 1) & ~1;
+            const bool ring = A.plimit == PF && kRing * slot <= 64 * S;
+            auto stage_item = [&](int k) {
+                const int node = sl[k].x;
+                double *dst = sbuf + (k % kRing) * slot;
+                const double *mom = A.r_mom + (int64_t)node * A.mom_K;
+                for (int q = lane; q < A.K; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
+                if (lane < D) __pipeline_memcpy_async(dst + A.K + lane, A.r_c + (int64_t)node * D + lane, 8);
+            };
+            if (ring) {
+#pragma unroll 1
+                for (int k = 0; k < kRing - 1; k++) {
+                    if (k < nh) stage_item(k);
+                    __pipeline_commit();
+                }
+            }
+            for (int i = 0; i < nh; i++) {
+                const int p = sl[i].y & 0xff;
+                if (ring) {
+                    if (i + kRing - 1 < nh) stage_item(i + kRing - 1);
+                    __pipeline_commit();
+                    __pipeline_wait_prior(kRing - 1);
+                    __syncwarp();
+                    const double *buf = sbuf + (i % kRing) * slot;
+                    if constexpr (D == 3) {
+                        pt_est += eval_far_fixed3<PF>(x, buf + A.K, buf, p, 1.0 / A.sc,
+                                                      [&](double v) { return fg_exp_fast(v, s_tab); });
+                    } else {
+                        pt_est += eval_far_fixed<D, PF>(x, buf + A.K, buf, p, 1.0 / A.sc);
+                    }
+                    __syncwarp();
+                } else {
+                    const int node = sl[i].x;
+                    pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)node * D,
+                                               A.r_mom + (int64_t)node * A.mom_K, p, A.kp[p], A.sc,
+                                               A.digits);
+                }
+            }
+            c_dh += nh;
+            // direct-local and H2L items accumulate into the block's local expansion
+            for (int k = 0; k < no; k++) {
+                const int2 e = sl[A.stack_cap - 1 - k];
                 const int meth = e.y >> 8, p = e.y & 0xff;
-                if (meth == 2) {
-                    constexpr int PF = default_plimit_c(D);
-                    if (A.plimit == PF) {
-                        if constexpr (D == 3) {
-                            pt_est += eval_far_fixed3<PF>(
-                                x, A.r_c + (int64_t)e.x * D, A.r_mom + (int64_t)e.x * A.mom_K, p,
-                                1.0 / A.sc, [&](double v) { return fg_exp_fast(v, s_tab); });
-                        } else {
-                            pt_est += eval_far_fixed<D, PF>(x, A.r_c + (int64_t)e.x * D,
-                                                            A.r_mom + (int64_t)e.x * A.mom_K, p,
-                                                            1.0 / A.sc);
-                        }
-                    } else
-                        pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)e.x * D,
-                                                   A.r_mom + (int64_t)e.x * A.mom_K, p, A.kp[p],
-                                                   A.sc, A.digits);
-                    c_dh++;
-                } else if (meth == 3) {
+                if (meth == 3) {
                     const int4 ni = A.r_ni[e.x];
                     accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], A.sc,
                                        A.digits, A.inv_fact, loc, false);
-                    local_used = true;
                     c_dl++;
                 } else {
                     h2l_warp_add<D>(A.r_mom + (int64_t)e.x * A.mom_K, A.r_c + (int64_t)e.x * D, qc,
                                     p, A.kp[p], p, A.kp[p], A.sc, A.digits, A.inv_fact, A.degrees,
                                     loc);
-                    local_used = true;
                     c_h2l++;
                 }
+                local_used = true;
                 __syncwarp();
             }
             if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, A.sc, A.digits);
