@@ -258,16 +258,21 @@ def run_ours(args):
     def step(record=True):
         vals_d.zero_()
         tree = build_tree_device(pts_d, w_d, 25)
-        for j, h in enumerate(wl.bandwidths):
-            tree.refresh_moments(h, pl)
-            cfg = fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, algorithm="dito")
-            if world == 1:
-                res = fg.dito_run(cfg, tree, tree, out=vals_d[j])
-            else:
+        if world == 1:
+            # the whole sweep in one engine call (refresh + run per bandwidth,
+            # stream-ordered, one synchronisation)
+            cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon, algorithm="dito")
+            results = fg.sweep_run(cfg, tree, tree, wl.bandwidths, out=vals_d)
+        else:
+            results = []
+            for j, h in enumerate(wl.bandwidths):
+                tree.refresh_moments(h, pl)
+                cfg = fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, algorithm="dito")
                 # this rank's query blocks, then the gather (NCCL all-reduce over
                 # disjoint supports) -- inside the timed step
-                res = run_sharded(cfg, tree, tree, vals_d[j], rank, world)
-            if record:
+                results.append(run_sharded(cfg, tree, tree, vals_d[j], rank, world))
+        if record:
+            for res in results:
                 stats["kernel_s"] += res.seconds
                 stats["pairs"] += res.counters.exact_pairs
                 stats["pairs32"] += res.counters.fp32_pairs
@@ -342,12 +347,8 @@ def run_ours(args):
         def e2e_step():
             store = fg.PointStore(wl.references, wl.weights)
             tree = fg.build_tree(store, 25)
-            out = []
-            for h in wl.bandwidths:
-                tree.refresh_moments(h, pl)
-                out.append(fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon),
-                                       tree, tree).values)
-            return out
+            cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon)
+            return [r.values for r in fg.sweep_run(cfg, tree, tree, wl.bandwidths)]
 
         with torch.cuda.stream(stream):
             e2e_step()

@@ -109,6 +109,15 @@ int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h,
  * run (reset + traverse + post, like summation_engine.py:447-452). */
 int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
            int32_t plimit, double *values, fg_counters *counters, double *seconds);
+/* Bandwidth sweep (the loop of run_sweep, cli_harness.py:246-283, for one
+ * algorithm): for each of the nh bandwidths (host or device array), refresh
+ * rtree's moments (FG_DITO) and run, all stream-ordered with a single
+ * synchronisation at the end.  values (nh x m) host or device, row j in
+ * original query order; counters and seconds (nh each, nullable).  rtree's
+ * moments are left at the last bandwidth. */
+int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
+                 double eps, int32_t mode, int32_t plimit, double *values, fg_counters *counters,
+                 double *seconds);
 /* Query-sharded run: only query blocks block_begin,
  * block_begin + block_stride, ... (< block_end) of qtree are processed;
  * values is written only at those blocks' queries (original order).  A

@@ -16,7 +16,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastgauss_b200.so")
+# FG_LIB selects an alternative in-tree build (engine variants for experiments)
+LIB_PATH = os.environ.get("FG_LIB") or os.path.join(_HERE, "libfastgauss_b200.so")
 
 FG_OK, FG_EINVAL, FG_ESTALE, FG_ECUDA, FG_EUNSUPPORTED = 0, 1, 2, 3, 4
 MODES = {"dfd": 1, "dfdo": 2, "dito": 3}
@@ -51,6 +52,7 @@ SIGNATURES = {
     "fg_run": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P],
     "fg_query_blocks": [_P, _P],
     "fg_run_range": [_P, _P, _F64, _F64, _I32, _I32, _I64, _I64, _I64, _P, _P, _P],
+    "fg_run_sweep": [_P, _P, _P, _I32, _F64, _I32, _I32, _P, _P, _P],
     "fg_launch_count": [_P],
     "fg_fp64_peak": [_P],
     "fg_ex2_peak": [_P],

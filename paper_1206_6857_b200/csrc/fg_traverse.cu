@@ -50,6 +50,9 @@ int g_ref_leaf = 32;
 int g_stack_cap = 4096;
 int g_fp32_base = 1;
 static constexpr double kFp32Share = 0.05;
+#ifndef FG_TRAV_MINB
+#define FG_TRAV_MINB 4  // resident 128-thread CTAs per SM the traversal is compiled for
+#endif
 
 // ---------------------------------------------------------- query blocks
 // A query block is a run of <= 32 consecutive tree-order points owned by one
@@ -242,7 +245,7 @@ template <int D>
 static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     // 4 resident CTAs of 128 threads per SM (<= 128 registers): measured best;
     // capping registers lower spills and runs slower
-    auto kern = traverse_kernel<D, 4>;
+    auto kern = traverse_kernel<D, FG_TRAV_MINB>;
     // resident-grid size, cached per (kernel, shared memory size)
     static thread_local const void *c_kern = nullptr;
     static thread_local size_t c_smem = 0;
@@ -307,7 +310,7 @@ double g_prime_eps = 0.0;
 
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
                   int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
-                  double *seconds) {
+                  double *seconds, const RunSink *sink) {
     FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
     FG_REQUIRE(eps >= 0.0, FG_EINVAL, "epsilon must be non-negative");
     FG_REQUIRE(mode >= FG_DFD && mode <= FG_DITO, FG_EINVAL, "unknown algorithm");
@@ -422,7 +425,8 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     const int64_t nb = b1 > b0 ? (b1 - b0 + A.stride - 1) / A.stride : 0;
     double prime_eps = g_prime_eps;
     if (const char *env = getenv("FG_PRIME_EPS")) prime_eps = atof(env);
-    cudaEventRecord(e0, stream());
+    const cudaEvent_t ev0 = sink ? sink->e0 : e0, ev1 = sink ? sink->e1 : e1;
+    cudaEventRecord(ev0, stream());
     if (nb > 0 && prime_eps > eps && eps > 0.0) {
         st = g_scr.prime.reserve(sizeof(double) * q.nqb);
         if (st == FG_OK) {
@@ -441,7 +445,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         if (q.qb_order_valid) A.order = q.qb_order.as<int>();
     }
     if (st == FG_OK && nb > 0) st = launch_dispatch(D, A, smem, nb);
-    cudaEventRecord(e1, stream());
+    cudaEventRecord(ev1, stream());
     if (st == FG_OK && A.cost) {
         // next run on this tree visits blocks heaviest-first (LPT order)
         const int nq = (int)q.nqb;
@@ -468,6 +472,12 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         } else if (st == FG_OK) {
             q.qb_order_valid = true;
         }
+    }
+    if (sink) {
+        FG_TRY(st);
+        FG_CUDA_TRY(cudaMemcpyAsync(sink->dcnt, g_scr.counters.p, sizeof(unsigned long long) * 8,
+                                    cudaMemcpyDeviceToDevice, stream()));
+        return FG_OK;
     }
     const char *dbg_path = getenv("FG_DEBUG_BLOCKS");
     for (int k = 0; k < 8; k++) cnt[k] = 0;

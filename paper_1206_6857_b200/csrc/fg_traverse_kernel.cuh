@@ -267,7 +267,7 @@ __device__ __forceinline__ float ex2_approx(float v) {
 //   da + 2^-17,  da = 2^-21 sqrt(D) M sqrt(a_c) / (sqrt2 h) + (4+D) u a_c
 // (the FP32 difference, squared distance and scaling; ex2.approx, measured
 // <= 2^-22.7 by tools/ex2_accuracy.cu; weight rounding; <= 63 additions per
-// FP32 accumulator); rho doubles that for safety.  a_max = -log K_lo is the
+// FP32 accumulator, of which there are eight); rho doubles that for safety.  a_max = -log K_lo is the
 // item's largest pair exponent (+inf when K_lo underflows).  Terms beyond a_c
 // (ex2 may flush them to zero) are worth at most w e^-80 and so are their
 // computed values: abs = 2 wr e^-80 when a_max > 80, plus 2^-140 for
@@ -324,42 +324,53 @@ __device__ __forceinline__ unsigned long long f2_ex2(unsigned long long v) {
 }
 
 // Stream one staged batch of `total` points (a multiple of 4): component c of
-// point j at fst[c * CAP + j], group g's offset record at gd[g * FD].
+// point j at fst[c * CAP + j], group g's offset record at gd[g * FD].  Groups
+// of 4 points go through as two packed pairs, two groups per iteration.
+template <int D>
+__device__ __forceinline__ void group_f32(const float (&xf)[D], const float *fst, const float *gd,
+                                          int j, unsigned long long s2, unsigned long long &acc_a,
+                                          unsigned long long &acc_b) {
+    constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>();
+    float dl[FD];
+#pragma unroll
+    for (int k = 0; k < FD; k += 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(gd + (j >> 2) * FD + k);
+        dl[k] = v.x; dl[k + 1] = v.y; dl[k + 2] = v.z; dl[k + 3] = v.w;
+    }
+    unsigned long long da, db;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const float q = xf[d] - dl[d];
+        const unsigned long long q2 = f2_pack(q, q);
+        const ulonglong2 c = *reinterpret_cast<const ulonglong2 *>(fst + d * CAP + j);
+        const unsigned long long fa = f2_sub(q2, c.x);
+        const unsigned long long fb = f2_sub(q2, c.y);
+        if (d == 0) {
+            da = f2_mul(fa, fa);
+            db = f2_mul(fb, fb);
+        } else {
+            da = f2_fma(fa, fa, da);
+            db = f2_fma(fb, fb, db);
+        }
+    }
+    const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(fst + D * CAP + j);
+    acc_a = f2_fma(f2_ex2(f2_mul(da, s2)), w.x, acc_a);
+    acc_b = f2_fma(f2_ex2(f2_mul(db, s2)), w.y, acc_b);
+}
+
 template <int D>
 __device__ __forceinline__ double batch_f32(const float (&xf)[D], const float *fst,
                                             const float *gd, int total, float ex2s) {
-    constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>();
     const unsigned long long s2 = f2_pack(ex2s, ex2s);
-    unsigned long long acc_a = 0ull, acc_b = 0ull;
-    for (int j = 0; j < total; j += 4) {
-        float dl[FD];
-#pragma unroll
-        for (int k = 0; k < FD; k += 4) {
-            const float4 v = *reinterpret_cast<const float4 *>(gd + (j >> 2) * FD + k);
-            dl[k] = v.x; dl[k + 1] = v.y; dl[k + 2] = v.z; dl[k + 3] = v.w;
-        }
-        unsigned long long da, db;
-#pragma unroll
-        for (int d = 0; d < D; d++) {
-            const float q = xf[d] - dl[d];
-            const unsigned long long q2 = f2_pack(q, q);
-            const float4 c = *reinterpret_cast<const float4 *>(fst + d * CAP + j);
-            const unsigned long long fa = f2_sub(q2, f2_pack(c.x, c.y));
-            const unsigned long long fb = f2_sub(q2, f2_pack(c.z, c.w));
-            if (d == 0) {
-                da = f2_mul(fa, fa);
-                db = f2_mul(fb, fb);
-            } else {
-                da = f2_fma(fa, fa, da);
-                db = f2_fma(fb, fb, db);
-            }
-        }
-        const float4 w = *reinterpret_cast<const float4 *>(fst + D * CAP + j);
-        acc_a = f2_fma(f2_ex2(f2_mul(da, s2)), f2_pack(w.x, w.y), acc_a);
-        acc_b = f2_fma(f2_ex2(f2_mul(db, s2)), f2_pack(w.z, w.w), acc_b);
+    unsigned long long a0 = 0ull, b0 = 0ull, a1 = 0ull, b1 = 0ull;
+    int j = 0;
+    for (; j + 8 <= total; j += 8) {
+        group_f32<D>(xf, fst, gd, j, s2, a0, b0);
+        group_f32<D>(xf, fst, gd, j + 4, s2, a1, b1);
     }
-    return ((double)f2_lo(acc_a) + (double)f2_hi(acc_a)) +
-           ((double)f2_lo(acc_b) + (double)f2_hi(acc_b));
+    if (j < total) group_f32<D>(xf, fst, gd, j, s2, a0, b0);
+    return (((double)f2_lo(a0) + (double)f2_hi(a0)) + ((double)f2_lo(b0) + (double)f2_hi(b0))) +
+           (((double)f2_lo(a1) + (double)f2_hi(a1)) + ((double)f2_lo(b1) + (double)f2_hi(b1)));
 }
 
 __device__ __forceinline__ int warp_excl_scan(int v) {

@@ -232,6 +232,9 @@ class KdTree:
     def refresh_moments(self, h: float, plimit: int) -> None:
         """Rebuild every node's far-field moments for bandwidth h (device)."""
         _lib.call("fg_moments_refresh", self._h, float(h), int(plimit))
+        self._moments_refreshed(h, plimit)
+
+    def _moments_refreshed(self, h: float, plimit: int) -> None:
         self.moments_bandwidth = h
         self.moments_order = plimit
         self._moments = None

@@ -166,6 +166,35 @@ def dito_run(config: RunConfig, qtree: KdTree, rtree: KdTree, audit: bool = Fals
     return _run_tree_algorithm(config, qtree, rtree, "dito", audit, out)
 
 
+def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
+              out=None) -> list:
+    """Run ``config.algorithm`` at every bandwidth in one device call.
+
+    The per-bandwidth loop of run_sweep (cli_harness.py:246-283): for DITO each
+    bandwidth refreshes ``rtree``'s moments first (they are left at the last
+    bandwidth).  ``config.bandwidth`` is ignored.  Returns one ResultVector per
+    bandwidth; with ``out`` (a CUDA tensor of shape (len(bandwidths), M)) the
+    values stay on the device and each ResultVector holds a row view.
+    """
+    if config.algorithm == "naive":
+        raise ValueError("sweep_run runs the tree algorithms; use naive_sum for naive")
+    hs = np.ascontiguousarray(np.atleast_1d(np.asarray(bandwidths, dtype=float)))
+    if hs.size == 0 or np.any(hs <= 0.0):
+        raise ValueError("bandwidths must be positive")
+    plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
+    nh = hs.shape[0]
+    vals = out if out is not None else np.empty((nh, qtree.n))
+    cnt = (_lib.fg_counters * nh)()
+    secs = np.zeros(nh)
+    _lib.call("fg_run_sweep", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
+              float(config.epsilon), _lib.MODES[config.algorithm], int(plimit), _lib.ptr(vals),
+              cnt, _lib.ptr(secs))
+    if config.algorithm == "dito":
+        rtree._moments_refreshed(float(hs[-1]), plimit)
+    return [ResultVector(vals[j], float(secs[j]), TraversalCounters._from_c(cnt[j]), None)
+            for j in range(nh)]
+
+
 def query_block_count(qtree: KdTree) -> int:
     """Number of 32-point query blocks (the unit of query sharding)."""
     nb = ctypes.c_int64()

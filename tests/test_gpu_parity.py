@@ -374,3 +374,41 @@ def test_fp32_base_cases_off_outside_fp32_range(fg, oracle):
     assert res.counters.fp32_pairs == 0 and res.counters.exact_pairs > 0
     exact = oracle.naive_sum(pts, pts, w, 0.03, threads=0)
     assert oracle.max_rel_error(res.values, exact) <= 0.01
+
+
+@pytest.mark.parametrize("alg", ["dfd", "dfdo", "dito"])
+def test_sweep_matches_single_runs(fg, alg):
+    """fg_run_sweep (one stream-ordered call for all bandwidths) gives exactly
+    the per-bandwidth runs of the same algorithm, host or device output."""
+    import torch
+
+    rng = np.random.default_rng(31)
+    pts = rng.random((8000, 3))
+    w = rng.uniform(0.5, 1.5, 8000)
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    hs = [0.003, 0.02, 0.08, 0.3]
+    cfg = fg.RunConfig(bandwidth=hs[0], epsilon=0.01, algorithm=alg)
+    sweep = fg.sweep_run(cfg, t, t, hs)
+    dev = torch.zeros(len(hs), 8000, dtype=torch.float64, device="cuda")
+    sweep_d = fg.sweep_run(cfg, t, t, hs, out=dev)
+    run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[alg]
+    for j, h in enumerate(hs):
+        if alg == "dito":
+            t.refresh_moments(h, fg.default_plimit(3))
+        single = run(fg.RunConfig(bandwidth=h, epsilon=0.01, algorithm=alg), t, t)
+        np.testing.assert_array_equal(sweep[j].values, single.values)
+        np.testing.assert_array_equal(dev[j].cpu().numpy(), single.values)
+        assert sweep[j].counters == single.counters
+        assert sweep_d[j].counters == single.counters
+        assert sweep[j].seconds > 0.0
+    if alg == "dito":
+        assert t.moments_bandwidth == hs[-1]
+
+
+def test_sweep_validation(fg):
+    t = fg.build_tree(fg.PointStore(np.random.default_rng(1).random((500, 2))), 25)
+    cfg = fg.RunConfig(bandwidth=0.1)
+    with pytest.raises(ValueError):
+        fg.sweep_run(cfg, t, t, [0.1, -1.0])
+    with pytest.raises(ValueError):
+        fg.sweep_run(cfg, t, t, [])
