@@ -524,55 +524,20 @@ int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32
         memcpy(hs.data(), bandwidths, sizeof(double) * nh);
     }
     for (double h : hs) FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
-    const int pl = plimit > 0 ? plimit : default_plimit(qtree->t.dim);
     const int64_t m = qtree->t.n;
     const bool out_dev = is_device_ptr(values);
     double *dout = values;
-    static DBuf s_out, s_cnt;
+    static DBuf s_out;
     if (!out_dev) {
         FG_TRY(s_out.reserve(sizeof(double) * m * nh));
         dout = s_out.as<double>();
     }
-    FG_TRY(s_cnt.reserve(sizeof(unsigned long long) * 8 * nh));
-    static thread_local std::vector<cudaEvent_t> evs;
-    while ((int)evs.size() < 2 * nh) {
-        cudaEvent_t e;
-        FG_CUDA_TRY(cudaEventCreate(&e));
-        evs.push_back(e);
-    }
-    // everything below is stream-ordered: each refresh overwrites the moments
-    // only after the previous run has read them; one synchronisation at the end
-    for (int j = 0; j < nh; j++) {
-        if (mode == FG_DITO) FG_TRY(moments_refresh(rtree->t, hs[j], pl));
-        const RunSink sink{s_cnt.as<unsigned long long>() + 8 * j, evs[2 * j], evs[2 * j + 1]};
-        FG_TRY(run_traversal(qtree->t, rtree->t, hs[j], eps, mode, pl, 0, -1, 1, dout + m * j,
-                             nullptr, nullptr, &sink));
-    }
-    if (!out_dev)
+    FG_TRY(run_sweep(qtree->t, rtree->t, hs.data(), nh, eps, mode, plimit, dout, counters,
+                     seconds));
+    if (!out_dev) {
         FG_CUDA_TRY(cudaMemcpyAsync(values, dout, sizeof(double) * m * nh, cudaMemcpyDeviceToHost,
                                     stream()));
-    std::vector<unsigned long long> hc(8 * (size_t)nh);
-    FG_CUDA_TRY(cudaMemcpyAsync(hc.data(), s_cnt.p, sizeof(unsigned long long) * 8 * nh,
-                                cudaMemcpyDeviceToHost, stream()));
-    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
-    for (int j = 0; j < nh; j++) {
-        const unsigned long long *c = hc.data() + 8 * j;
-        if (counters) {
-            fg_counters &o = counters[j];
-            o.pair_visits = (int64_t)c[0];
-            o.base_cases = (int64_t)c[1];
-            o.fd_prunes = (int64_t)c[2];
-            o.hermite_prunes = (int64_t)c[3];
-            o.local_prunes = (int64_t)c[4];
-            o.h2l_prunes = (int64_t)c[5];
-            o.exact_pairs = (int64_t)c[6];
-            o.fp32_pairs = (int64_t)c[7];
-        }
-        if (seconds) {
-            float ms = 0.f;
-            FG_CUDA_TRY(cudaEventElapsedTime(&ms, evs[2 * j], evs[2 * j + 1]));
-            seconds[j] = ms * 1e-3;
-        }
+        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     }
     return FG_OK;
 }

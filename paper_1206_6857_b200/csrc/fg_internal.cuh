@@ -176,18 +176,15 @@ int tree_export(const TreeDev &t, int64_t *perm, int64_t *start, int64_t *end, d
                 double *hi, double *center, double *weight, double *inf_radius,
                 int64_t *left, int64_t *right);
 int moments_refresh(TreeDev &t, double h, int plimit);
+int moments_multi(TreeDev &t, const double *hs, int nh, int plimit, DBuf &dst);
 int moments_export(const TreeDev &t, double *out);
 int query_blocks(TreeDev &t);
-// Asynchronous completion of a run (used by sweeps): the run's counters are
-// copied to dcnt[0..8) on the device and its kernel is bracketed by e0/e1;
-// run_traversal then returns without synchronising.
-struct RunSink {
-    unsigned long long *dcnt;
-    cudaEvent_t e0, e1;
-};
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
                   int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
-                  double *seconds, const RunSink *sink = nullptr);
+                  double *seconds);
+// all bandwidths of a sweep through shared launches (values: nh x m, device)
+int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int mode, int plimit,
+              double *d_values, fg_counters *counters, double *seconds);
 int preorder_map(const TreeDev &t, std::vector<int64_t> &pre);
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
               int dim, const double *hs, int nh, double *d_out);

@@ -170,6 +170,57 @@ int moments_refresh(TreeDev &t, double h, int plimit) {
     return FG_OK;
 }
 
+// Moments of several bandwidths side by side (sweeps): dst[j] = the moments
+// moments_refresh(t, hs[j], plimit) would produce, by the same rescaling of
+// the base moments (bit-identical to it).
+struct RatioList {
+    double r[32];
+};
+__global__ void rescale_factors_multi_kernel(int nh, int K, RatioList ratios,
+                                             const int *__restrict__ degrees,
+                                             double *__restrict__ fac) {
+    for (int i = threadIdx.x; i < nh * K; i += blockDim.x)
+        fac[i] = pow(ratios.r[i / K], (double)degrees[i % K]);
+}
+
+__global__ void moments_rescale_multi_kernel(int64_t total, int nh, int K,
+                                             const double *__restrict__ src,
+                                             const double *__restrict__ fac,
+                                             double *__restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const double v = src[i];
+    const int k = (int)(i % K);
+    for (int j = 0; j < nh; j++) dst[(int64_t)j * total + i] = v * fac[j * K + k];
+}
+
+int moments_multi(TreeDev &t, const double *hs, int nh, int plimit, DBuf &dst) {
+    FG_REQUIRE(nh >= 1 && nh <= 32, FG_EINVAL, "bad bandwidth count");
+    int st = FG_OK;
+    const SeriesTables *T = series_tables(t.dim, plimit, &st);
+    FG_TRY(st);
+    const int K = T->K;
+    if (!(t.mom0_valid && t.mom_K == K && t.mom_order == plimit))
+        FG_TRY(moments_refresh(t, hs[0], plimit));  // base moments at hs[0]
+    const int64_t total = t.nnodes * K;
+    FG_TRY(dst.reserve(sizeof(double) * total * nh));
+    static DBuf fac;
+    FG_TRY(fac.reserve(sizeof(double) * K * nh));
+    RatioList rl;
+    for (int j = 0; j < nh; j++) {
+        FG_REQUIRE(hs[j] > 0.0 && std::isfinite(hs[j]), FG_EINVAL, "bandwidth must be positive");
+        rl.r[j] = t.mom0_h / hs[j];
+    }
+    count_launch();
+    rescale_factors_multi_kernel<<<1, 256, 0, stream()>>>(nh, K, rl, T->degrees.as<int>(),
+                                                          fac.as<double>());
+    count_launch();
+    moments_rescale_multi_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream()>>>(
+        total, nh, K, t.mom0.as<double>(), fac.as<double>(), dst.as<double>());
+    FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
 int moments_export(const TreeDev &t, double *out) {
     FG_REQUIRE(t.mom_valid, FG_ESTALE, "no moments: call refresh_moments first");
     const int K = t.mom_K;

@@ -236,7 +236,7 @@ __global__ void iota_kernel(int *out, int n) {
 }
 
 struct TravScratch {
-    DBuf st_node, st_f, ser, work, counters, dbg, prime;
+    DBuf st_node, st_f, ser, work, counters, dbg;
     int grid = 0, cap = 0;
 };
 static TravScratch g_scr;
@@ -302,28 +302,22 @@ static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
     }
 }
 
-// Priming pass: a coarse run at eps1 gives estimates with
-// |est - G| <= eps1 G, hence G >= est / (1 + eps1) for every query.  The
-// per-block minimum of that bound primes the mass lower bound of the real run
-// (used as max(accumulated, primed)).  0 disables.
-double g_prime_eps = 0.0;
-
-int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
-                  int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
-                  double *seconds, const RunSink *sink) {
-    FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
+// Queue one traversal launch over nh bandwidths (tasks = (bandwidth, query
+// block) pairs, bandwidth-major), without synchronising.  moms[j] are the
+// reference moments for hs[j] (DITO), outs[j] the value vectors, dcnt the
+// nh x kCounters device counter block (zeroed here).  order/cost: LPT order
+// and per-block cost capture (single full runs only).
+static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
+                           const double *const *moms, double eps, int mode, int plimit,
+                           int64_t b0, int64_t b1, int64_t stride, double *const *outs,
+                           unsigned long long *dcnt, bool lpt) {
+    FG_REQUIRE(nh >= 1 && nh <= kMaxSweep, FG_EINVAL, "bad bandwidth count");
     FG_REQUIRE(eps >= 0.0, FG_EINVAL, "epsilon must be non-negative");
     FG_REQUIRE(mode >= FG_DFD && mode <= FG_DITO, FG_EINVAL, "unknown algorithm");
     FG_REQUIRE(q.dim == r.dim, FG_EINVAL, "query and reference dimensions differ");
+    for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const int D = q.dim;
-    if (plimit <= 0) plimit = default_plimit(D);
     const bool series = mode == FG_DITO;
-    if (series) {
-        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
-        FG_REQUIRE(r.mom_valid && r.mom_h == h && r.mom_order >= plimit, FG_ESTALE,
-                   "reference moments missing or stale; call refresh_moments for this "
-                   "bandwidth first");
-    }
     FG_TRY(query_blocks(q));
     if (b1 < 0 || b1 > q.nqb) b1 = q.nqb;
     if (b0 < 0) b0 = 0;
@@ -343,12 +337,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     A.b0 = b0;
     A.b1 = b1;
     A.stride = stride < 1 ? 1 : stride;
-    A.out = d_values;
-    A.h = h;
-    A.neg_inv = -0.5 / (h * h);
-    A.inv_h = 1.0 / h;
-    A.sc = kSqrt2 * h;
-    A.eps = eps;
+    A.nbl = b1 > b0 ? (b1 - b0 + A.stride - 1) / A.stride : 0;
     A.total_w = r.total_w;
     A.use_tokens = mode >= FG_DFDO;
     A.use_series = series;
@@ -359,7 +348,6 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         const char *env = getenv("FG_BFS_CAP");
         A.bfs_cap = env ? atoi(env) : g_stack_cap / 4;
     }
-    size_t smem = 0;
     if (series) {
         int st = FG_OK;
         const SeriesTables *T = series_tables(D, plimit, &st);
@@ -368,7 +356,6 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         A.digits = T->digits.as<uint8_t>();
         A.inv_fact = T->inv_fact.as<double>();
         A.degrees = T->degrees.as<int>();
-        A.r_mom = r.mom.as<double>();
         A.mom_K = r.mom_K;
         double ct[kMaxOrder + 1], cross[kMaxOrder + 1], floor_c;
         tail_tables(D, plimit, ct, cross, &floor_c);
@@ -379,7 +366,9 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         }
         A.floor_c = floor_c;
     }
-    // per warp: query box + centroid + local coefficients, then 2 x 32 staged points
+    // per warp: query box + centroid + local coefficients, 2 x 32 staged FP64
+    // points, the FP32 batch
+    size_t smem;
     {
         static const int f32d[9] = {0,
                                     f32_smem_doubles<1>(), f32_smem_doubles<2>(),
@@ -390,130 +379,192 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
                kTravWarps;
     }
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
-    FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * 8));
-    FG_CUDA_TRY(cudaMemsetAsync(g_scr.counters.p, 0, sizeof(unsigned long long) * 8, stream()));
     A.work = g_scr.work.as<unsigned long long>();
-    A.no_eager = getenv("FG_NO_EAGER") ? 1 : 0;
+    FG_CUDA_TRY(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * kCounters * nh, stream()));
     // FP32 base cases: a share kFp32Share of eps
     // is reserved for their rounding error, the rest drives the traversal
     int fp32 = g_fp32_base;
     if (const char *env = getenv("FG_FP32_BASE")) fp32 = atoi(env);
-    A.ex2_scale = (float)(-1.4426950408889634 / (2.0 * h * h));
-    if (!q.fp32_ok || !r.fp32_ok || !(fabsf(A.ex2_scale) < 1e30f) || !(eps > 0.0)) fp32 = 0;
+    if (!q.fp32_ok || !r.fp32_ok || !(eps > 0.0)) fp32 = 0;
+    for (int j = 0; j < nh; j++)
+        if (!(fabs(-1.4426950408889634 / (2.0 * hs[j] * hs[j])) < 1e30)) fp32 = 0;
     if (fp32) {
         FG_TRY(fp32_pack(r));
         A.r_pf = r.pf.as<float>();
         A.r_anchor = r.anchor.as<int>();
     }
-    A.fp32_rho = fp32 ? kFp32Share * eps : 0.0;
-    A.eps = fp32 ? (1.0 - kFp32Share) * eps : eps;
-    if (getenv("FG_DEBUG_BLOCKS")) {
+    A.nh = nh;
+    for (int j = 0; j < nh; j++) {
+        TravH &H = A.hp[j];
+        const double h = hs[j];
+        H.h = h;
+        H.neg_inv = -0.5 / (h * h);
+        H.inv_h = 1.0 / h;
+        H.sc = kSqrt2 * h;
+        H.inv_sc = 1.0 / H.sc;
+        H.fp32_rho = fp32 ? kFp32Share * eps : 0.0;
+        H.eps = fp32 ? (1.0 - kFp32Share) * eps : eps;
+        H.ex2_scale = (float)(-1.4426950408889634 / (2.0 * h * h));
+        H.r_mom = series ? moms[j] : nullptr;
+        H.out = outs[j];
+        H.counters = dcnt + (size_t)kCounters * j;
+    }
+    if (getenv("FG_DEBUG_BLOCKS") && nh == 1) {
         FG_TRY(g_scr.dbg.reserve(sizeof(unsigned long long) * 4 * q.nqb));
         FG_CUDA_TRY(cudaMemsetAsync(g_scr.dbg.p, 0, sizeof(unsigned long long) * 4 * q.nqb, stream()));
         A.dbg = g_scr.dbg.as<unsigned long long>();
     }
-    A.counters = g_scr.counters.as<unsigned long long>();
+    const bool full = b0 == 0 && b1 == q.nqb && A.stride == 1 && nh == 1 && lpt;
+    if (full && A.nbl > 1) {
+        FG_TRY(q.qb_cost.reserve(sizeof(unsigned long long) * q.nqb));
+        A.cost = q.qb_cost.as<unsigned long long>();
+        if (q.qb_order_valid) A.order = q.qb_order.as<int>();
+    }
+    if (A.nbl > 0) FG_TRY(launch_dispatch(D, A, smem, A.nbl * nh));
+    if (A.cost) {
+        // the next single run on this tree visits blocks heaviest-first (LPT
+        // order); keys are cycle counts, so bits 8..40 order them well enough
+        const int nq = (int)q.nqb;
+        size_t tmp_bytes = 0;
+        FG_TRY(q.qb_iota.reserve(sizeof(int) * nq));
+        const int *iota = q.qb_iota.as<int>();
+        count_launch();
+        iota_kernel<<<(nq + 255) / 256, 256, 0, stream()>>>(q.qb_iota.as<int>(), nq);
+        cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
+            nullptr, tmp_bytes, A.cost, (unsigned long long *)nullptr, iota, (int *)nullptr, nq,
+            8, 40, stream());
+        if (e == cudaSuccess) {
+            FG_TRY(q.qb_sort_tmp.reserve(tmp_bytes + 16));
+            FG_TRY(q.qb_keys.reserve(sizeof(unsigned long long) * nq));
+            FG_TRY(q.qb_order.reserve(sizeof(int) * nq));
+            e = cub::DeviceRadixSort::SortPairsDescending(
+                q.qb_sort_tmp.p, tmp_bytes, A.cost, q.qb_keys.as<unsigned long long>(), iota,
+                q.qb_order.as<int>(), nq, 8, 40, stream());
+        }
+        if (e != cudaSuccess) {
+            set_error(std::string("block order sort: ") + cudaGetErrorString(e));
+            return FG_ECUDA;
+        }
+        count_launch();
+        q.qb_order_valid = true;
+    }
+    return FG_OK;
+}
+
+static void fill_counters(const unsigned long long *c, fg_counters *o) {
+    o->pair_visits = (int64_t)c[0];
+    o->base_cases = (int64_t)c[1];
+    o->fd_prunes = (int64_t)c[2];
+    o->hermite_prunes = (int64_t)c[3];
+    o->local_prunes = (int64_t)c[4];
+    o->h2l_prunes = (int64_t)c[5];
+    o->exact_pairs = (int64_t)c[6];
+    o->fp32_pairs = (int64_t)c[7];
+}
+
+int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
+                  int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
+                  double *seconds) {
+    FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
+    const int D = q.dim;
+    if (plimit <= 0) plimit = default_plimit(D);
+    if (mode == FG_DITO) {
+        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
+        FG_REQUIRE(r.mom_valid && r.mom_h == h && r.mom_order >= plimit, FG_ESTALE,
+                   "reference moments missing or stale; call refresh_moments for this "
+                   "bandwidth first");
+    }
     // timing events and the pinned counter buffer are created once per thread
     static thread_local cudaEvent_t e0 = nullptr, e1 = nullptr;
     static thread_local unsigned long long *cnt = nullptr;
     if (!e0) {
         FG_CUDA_TRY(cudaEventCreate(&e0));
         FG_CUDA_TRY(cudaEventCreate(&e1));
-        FG_CUDA_TRY(cudaMallocHost(&cnt, sizeof(unsigned long long) * 8));
+        FG_CUDA_TRY(cudaMallocHost(&cnt, sizeof(unsigned long long) * kCounters));
     }
-    int st = FG_OK;
-    const int64_t nb = b1 > b0 ? (b1 - b0 + A.stride - 1) / A.stride : 0;
-    double prime_eps = g_prime_eps;
-    if (const char *env = getenv("FG_PRIME_EPS")) prime_eps = atof(env);
-    const cudaEvent_t ev0 = sink ? sink->e0 : e0, ev1 = sink ? sink->e1 : e1;
-    cudaEventRecord(ev0, stream());
-    if (nb > 0 && prime_eps > eps && eps > 0.0) {
-        st = g_scr.prime.reserve(sizeof(double) * q.nqb);
-        if (st == FG_OK) {
-            TravArgs A1 = A;
-            A1.eps = prime_eps;
-            A1.prime_out = g_scr.prime.as<double>();
-            A1.prime_scale = kMassSafety / (1.0 + prime_eps);
-            st = launch_dispatch(D, A1, smem, nb);
-            A.prime_in = g_scr.prime.as<double>();
-        }
-    }
-    const bool full = b0 == 0 && b1 == q.nqb && A.stride == 1;
-    if (st == FG_OK && full && nb > 1) {
-        st = q.qb_cost.reserve(sizeof(unsigned long long) * q.nqb);
-        if (st == FG_OK) A.cost = q.qb_cost.as<unsigned long long>();
-        if (q.qb_order_valid) A.order = q.qb_order.as<int>();
-    }
-    if (st == FG_OK && nb > 0) st = launch_dispatch(D, A, smem, nb);
-    cudaEventRecord(ev1, stream());
-    if (st == FG_OK && A.cost) {
-        // next run on this tree visits blocks heaviest-first (LPT order)
-        const int nq = (int)q.nqb;
-        size_t tmp_bytes = 0;
-        st = q.qb_iota.reserve(sizeof(int) * nq);
-        const int *iota = q.qb_iota.as<int>();
-        if (st == FG_OK) {
-            count_launch();
-            iota_kernel<<<(nq + 255) / 256, 256, 0, stream()>>>(q.qb_iota.as<int>(), nq);
-        }
-        cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
-            nullptr, tmp_bytes, A.cost, (unsigned long long *)nullptr, iota, (int *)nullptr, nq,
-            0, 64, stream());
-        if (e == cudaSuccess) st = q.qb_sort_tmp.reserve(tmp_bytes + 16);
-        if (e == cudaSuccess && st == FG_OK) st = q.qb_keys.reserve(sizeof(unsigned long long) * nq);
-        if (e == cudaSuccess && st == FG_OK) st = q.qb_order.reserve(sizeof(int) * nq);
-        if (e == cudaSuccess && st == FG_OK)
-            e = cub::DeviceRadixSort::SortPairsDescending(
-                q.qb_sort_tmp.p, tmp_bytes, A.cost, q.qb_keys.as<unsigned long long>(), iota,
-                q.qb_order.as<int>(), nq, 0, 64, stream());
-        if (e != cudaSuccess) {
-            set_error(std::string("block order sort: ") + cudaGetErrorString(e));
-            st = FG_ECUDA;
-        } else if (st == FG_OK) {
-            q.qb_order_valid = true;
-        }
-    }
-    if (sink) {
-        FG_TRY(st);
-        FG_CUDA_TRY(cudaMemcpyAsync(sink->dcnt, g_scr.counters.p, sizeof(unsigned long long) * 8,
-                                    cudaMemcpyDeviceToDevice, stream()));
-        return FG_OK;
-    }
-    const char *dbg_path = getenv("FG_DEBUG_BLOCKS");
-    for (int k = 0; k < 8; k++) cnt[k] = 0;
-    if (st == FG_OK) {
-        cudaError_t e = cudaMemcpyAsync(cnt, g_scr.counters.p, sizeof(unsigned long long) * 8,
-                                        cudaMemcpyDeviceToHost, stream());
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream());
-        if (e != cudaSuccess) {
-            set_error(std::string("traversal: ") + cudaGetErrorString(e));
-            st = FG_ECUDA;
-        }
-    }
-    if (st == FG_OK && seconds) {
+    FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * kCounters));
+    const double *mom = r.mom.as<double>();
+    FG_CUDA_TRY(cudaEventRecord(e0, stream()));
+    FG_TRY(queue_traversal(q, r, 1, &h, &mom, eps, mode, plimit, b0, b1, stride, &d_values,
+                           g_scr.counters.as<unsigned long long>(), true));
+    FG_CUDA_TRY(cudaEventRecord(e1, stream()));
+    FG_CUDA_TRY(cudaMemcpyAsync(cnt, g_scr.counters.p, sizeof(unsigned long long) * kCounters,
+                                cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    if (seconds) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e1);
         *seconds = ms * 1e-3;
     }
-    FG_TRY(st);
-    if (dbg_path && A.dbg) {
+    if (const char *dbg_path = getenv("FG_DEBUG_BLOCKS")) {
         std::vector<unsigned long long> hd(4 * q.nqb);
-        cudaMemcpy(hd.data(), A.dbg, sizeof(unsigned long long) * 4 * q.nqb, cudaMemcpyDeviceToHost);
-        FILE *f = fopen(dbg_path, "ab");
-        if (f) {
+        cudaMemcpy(hd.data(), g_scr.dbg.p, sizeof(unsigned long long) * 4 * q.nqb,
+                   cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(dbg_path, "ab")) {
             fwrite(hd.data(), sizeof(unsigned long long), hd.size(), f);
             fclose(f);
         }
     }
-    if (counters) {
-        counters->pair_visits = (int64_t)cnt[0];
-        counters->base_cases = (int64_t)cnt[1];
-        counters->fd_prunes = (int64_t)cnt[2];
-        counters->hermite_prunes = (int64_t)cnt[3];
-        counters->local_prunes = (int64_t)cnt[4];
-        counters->h2l_prunes = (int64_t)cnt[5];
-        counters->exact_pairs = (int64_t)cnt[6];
-        counters->fp32_pairs = (int64_t)cnt[7];
+    if (counters) fill_counters(cnt, counters);
+    return FG_OK;
+}
+
+int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int mode, int plimit,
+              double *d_values, fg_counters *counters, double *seconds) {
+    const int D = q.dim;
+    if (plimit <= 0) plimit = default_plimit(D);
+    FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
+    for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
+    const bool series = mode == FG_DITO;
+    static DBuf s_mom, s_cnt;
+    static thread_local std::vector<cudaEvent_t> evs;
+    const int nchunk = (nh + kMaxSweep - 1) / kMaxSweep;
+    while ((int)evs.size() < nchunk + 1) {
+        cudaEvent_t e;
+        FG_CUDA_TRY(cudaEventCreate(&e));
+        evs.push_back(e);
+    }
+    FG_TRY(s_cnt.reserve(sizeof(unsigned long long) * kCounters * nh));
+    FG_TRY(query_blocks(q));
+    const int64_t m = q.n;
+    FG_CUDA_TRY(cudaEventRecord(evs[0], stream()));
+    for (int c = 0; c < nchunk; c++) {
+        const int j0 = c * kMaxSweep, nj = std::min(kMaxSweep, nh - j0);
+        std::vector<const double *> moms(nj, nullptr);
+        std::vector<double *> outs(nj);
+        for (int j = 0; j < nj; j++) outs[j] = d_values + m * (j0 + j);
+        if (series) {
+            // every bandwidth's moments by the exact rescaling law from the
+            // tree's base moments (moments_refresh), materialised side by side
+            FG_TRY(moments_multi(r, hs + j0, nj, plimit, s_mom));
+            for (int j = 0; j < nj; j++)
+                moms[j] = s_mom.as<double>() + (size_t)j * r.nnodes * r.mom_K;
+        }
+        FG_TRY(queue_traversal(q, r, nj, hs + j0, moms.data(), eps, mode, plimit, 0, -1, 1,
+                               outs.data(), s_cnt.as<unsigned long long>() + kCounters * j0, false));
+        FG_CUDA_TRY(cudaEventRecord(evs[c + 1], stream()));
+    }
+    std::vector<unsigned long long> hc((size_t)kCounters * nh);
+    FG_CUDA_TRY(cudaMemcpyAsync(hc.data(), s_cnt.p, sizeof(unsigned long long) * kCounters * nh,
+                                cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    for (int c = 0; c < nchunk; c++) {
+        const int j0 = c * kMaxSweep, nj = std::min(kMaxSweep, nh - j0);
+        float ms = 0.f;
+        FG_CUDA_TRY(cudaEventElapsedTime(&ms, evs[c], evs[c + 1]));
+        // one launch serves nj bandwidths: split its time by their summed
+        // per-block cycles
+        double cyc = 0.0;
+        for (int j = 0; j < nj; j++) cyc += (double)hc[(size_t)kCounters * (j0 + j) + 8];
+        for (int j = 0; j < nj; j++) {
+            const double share = cyc > 0.0 ? hc[(size_t)kCounters * (j0 + j) + 8] / cyc : 1.0 / nj;
+            if (seconds) seconds[j0 + j] = ms * 1e-3 * share;
+            if (counters) fill_counters(hc.data() + (size_t)kCounters * (j0 + j), counters + j0 + j);
+        }
+    }
+    if (series) {
+        // leave the tree's moments at the last bandwidth (refresh semantics)
+        FG_TRY(moments_refresh(r, hs[nh - 1], plimit));
     }
     return FG_OK;
 }

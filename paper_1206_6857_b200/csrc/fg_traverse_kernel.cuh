@@ -18,6 +18,20 @@ constexpr int kTravWarps = kTravThreads / 32;
 // incrementally, so it carries <= (#updates) ulps of drift relative to G_min.
 constexpr double kMassSafety = 1.0 - 1e-10;
 
+// Per-bandwidth parameters of one launch (a launch serves up to kMaxSweep
+// bandwidths of a sweep; its tasks are (bandwidth, query block) pairs).
+constexpr int kMaxSweep = 24;
+constexpr int kCounters = 16;  // per-bandwidth device counter slots (9 used)
+struct TravH {
+    double h, neg_inv, inv_h, sc, inv_sc, eps;
+    double fp32_rho;              // relative error allowed per FP32 leaf item (0: FP64 only)
+    const double *r_mom;          // reference moments for this bandwidth
+    double *out;                  // values (original query order)
+    unsigned long long *counters; // kCounters slots: the 8 fg_counters fields, cycles
+    float ex2_scale;              // -log2(e) / (2 h^2)
+    int pad;
+};
+
 struct TravArgs {
     // reference tree (BFS numbering)
     const double *r_pw;
@@ -25,7 +39,6 @@ struct TravArgs {
     const double *r_box;
     const double *r_c;
     const double2 *r_wr;
-    const double *r_mom;
     int mom_K;
     // query blocks
     const double *q_pw;
@@ -35,9 +48,9 @@ struct TravArgs {
     const double *qb_rad;
     const int64_t *q_perm;
     long long b0, b1, stride;
-    double *out;
+    long long nbl;  // blocks per bandwidth in [b0, b1) at this stride
     // scalars
-    double h, neg_inv, inv_h, sc, eps, total_w, floor_c;
+    double total_w, floor_c;
     int use_tokens, use_series, plimit, K, ref_leaf;
     double ct[kMaxOrder + 1], cross[kMaxOrder + 1];
     int kp[kMaxOrder + 1];  // coefficient count for order p
@@ -51,18 +64,13 @@ struct TravArgs {
     int stack_cap;
     int bfs_cap;  // breadth-first while the frontier holds <= bfs_cap entries
     unsigned long long *work;
-    unsigned long long *counters;  // 7 counters
     unsigned long long *dbg;       // optional per-block (cycles, steps, visits, pairs)
-    int no_eager;                  // experiment: credit base cases with K_lo only
-    const double *prime_in;        // per-block primed lower bound on G (or null)
-    double *prime_out;             // coarse pass: write per-block bound instead of values
-    double prime_scale;            // safety / (1 + eps1)
-    const int *order;              // block visiting order (full runs) or null
+    const int *order;              // block visiting order (single full runs) or null
     unsigned long long *cost;      // per-block cycles of this run (or null)
-    double fp32_rho;               // relative error allowed per FP32 leaf item (0: FP64 only)
     const float *r_pf;             // FP32 records about each point's anchor (fp32_pack)
     const int *r_anchor;           // per point: its anchor node
-    float ex2_scale;               // -log2(e) / (2 h^2)
+    int nh;                        // bandwidths in this launch
+    TravH hp[kMaxSweep];
 };
 
 // Admit candidates in lane order under the token rule.  Unconditional
@@ -97,7 +105,7 @@ __device__ __forceinline__ double required_tokens(double wr, double err, double 
 // kernel bounds (summation_engine.py:315-328).
 template <int D>
 __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq, int node,
-                                             double &klo, double &khi, double &mn,
+                                             double neg_inv, double &klo, double &khi, double &mn,
                                              const double *s_tab) {
     const double *rbox = A.r_box + (int64_t)node * 2 * D;
     double mx = 0.0;
@@ -113,8 +121,8 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
         const double s = s1 > s2 ? s1 : s2;
         mx += s * s;
     }
-    khi = fg_exp_fast(mn * A.neg_inv, s_tab);
-    klo = fg_exp_fast(mx * A.neg_inv, s_tab);
+    khi = fg_exp_fast(mn * neg_inv, s_tab);
+    klo = fg_exp_fast(mx * neg_inv, s_tab);
 }
 
 // Exact contribution of reference points [rs, rs+rc) to this lane's query
@@ -235,7 +243,7 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
 //
 // The batch error is bounded by rho S + abs (fp32_item_bound; DESIGN.md
 // "FP32 base case"), S the exact sum.  An item joins only when rho <=
-// A.fp32_rho = phi * eps -- all FP32 items together then err by at most
+// H.fp32_rho = phi * eps -- all FP32 items together then err by at most
 // phi * eps * G(x_q) through their relative parts -- and when its own token
 // share covers abs, which is charged through the token rule
 // (summation_engine.py:157-188) like a prune's error.  The host runs the
@@ -274,7 +282,8 @@ __device__ __forceinline__ float ex2_approx(float v) {
 // subnormal rounding in the FP32 accumulation.
 template <int D>
 __device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const double *sq, int anc,
-                                                  double klo, double wr, double &abs_err) {
+                                                  double inv_h, double klo, double wr,
+                                                  double &abs_err) {
     const double a_max = klo > 0.0 ? -log(klo) : CUDART_INF;
     const double a_c = fmin(a_max, 80.0);
     abs_err = (a_max > 80.0 ? 2.0 * wr * 1.8048513878454153e-35 : 0.0) + 0x1.0p-140;
@@ -289,7 +298,7 @@ __device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const doubl
                          fmax(fabs(qlo - c), fabs(qhi - c))));
         M = fmax(M, fmax(fabs(c - cb), fmax(fabs(qlo - cb), fabs(qhi - cb))));
     }
-    const double da = 0x1.0p-21 * sqrt((double)D) * M * sqrt(a_c) * A.inv_h * 0.7071067811865476 +
+    const double da = 0x1.0p-21 * sqrt((double)D) * M * sqrt(a_c) * inv_h * 0.7071067811865476 +
                       (4.0 + D) * 0x1.0p-24 * a_c;
     return 2.0 * (da + 0x1.0p-17);
 }
@@ -413,16 +422,19 @@ traverse_kernel(const TravArgs A) {
     const unsigned lt_mask = (1u << lane) - 1u;
 
     for (;;) {
-        long long b = 0;
-        if (lane == 0) {
-            const long long i = (long long)atomicAdd(A.work, 1ULL);
-            b = i * A.stride + A.b0;
-            // full runs visit blocks in the given order (heaviest first, from
-            // the previous run's measured costs): shortens the tail
-            if (A.order && b < A.b1) b = A.order[b];
-        }
-        b = __shfl_sync(kFull, b, 0);
-        if (b >= A.b1) break;
+        // task = (bandwidth j, query block b), bandwidth-major: a warp that
+        // finishes early moves on to the next bandwidth's blocks, so only the
+        // launch's last tasks form a tail
+        long long t = 0;
+        if (lane == 0) t = (long long)atomicAdd(A.work, 1ULL);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= A.nbl * A.nh) break;
+        const int j = (int)(t / A.nbl);
+        long long b = (t - (long long)j * A.nbl) * A.stride + A.b0;
+        // single full runs visit blocks in the given order (heaviest first,
+        // from the previous run's measured costs): shortens the tail
+        if (A.order) b = __ldg(A.order + b);
+        const TravH &H = A.hp[j];
 
         const long long t_start = clock64();
         unsigned steps = 0;
@@ -440,9 +452,6 @@ traverse_kernel(const TravArgs A) {
 #pragma unroll
             for (int d = 0; d < D; d++) x[d] = sqc[d];
         }
-        // primed lower bound on G over the block (a coarse pass's estimates
-        // divided by 1 + its epsilon); used as max(accumulated, primed) only
-        const double gprime = A.prime_in ? A.prime_in[b] : 0.0;
         double pt_est = 0.0, pt_mass = 0.0;                    // per point
         double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
@@ -459,7 +468,7 @@ traverse_kernel(const TravArgs A) {
         const int cap = A.stack_cap;
         {
             double klo, khi, mn;
-            entry_bounds<D>(A, sq, 0, klo, khi, mn, s_tab);
+            entry_bounds<D>(A, sq, 0, H.neg_inv, klo, khi, mn, s_tab);
             if (lane == 0) {
                 sn[0] = 0;
                 skl[0] = klo;
@@ -502,12 +511,12 @@ traverse_kernel(const TravArgs A) {
             c_vis += nb;
             const double batch_sum = warp_sum(act ? WR * klo : 0.0);
             const double pmin = warp_min(valid ? pt_mass : CUDART_INF);
-            const double gmin = fmax((pmin + node_mass + fsum) * kMassSafety, gprime);
+            const double gmin = (pmin + node_mass + fsum) * kMassSafety;
 
             // ---- finite-difference prune (summation_engine.py:327-351)
             const double fd_err = 0.5 * WR * (khi - klo);
             // W / (eps G_min): one uniform division per step instead of one per entry
-            const double den = A.eps * gmin;
+            const double den = H.eps * gmin;
             const double tok_scale = den > 0.0 ? A.total_w / den : CUDART_INF;
             const double err_scale = den / A.total_w;  // eps G_min / W
             const double req = required_tokens(WR, fd_err, tok_scale);
@@ -531,8 +540,8 @@ traverse_kernel(const TravArgs A) {
                 double bound = 0.0;
                 if (act && !fd) {
                     const double maxerr = (WR + tokens) * err_scale;
-                    const double r_ref = wr.y * A.inv_h;
-                    const double r_qu = A.qb_rad[b] * A.inv_h;
+                    const double r_ref = wr.y * H.inv_h;
+                    const double r_qu = A.qb_rad[b] * H.inv_h;
                     const double rmin = r_ref < r_qu ? r_ref : r_qu;
                     double possible = sqrt(khi) * WR * A.floor_c;
                     if (rmin < 1.0) {
@@ -541,7 +550,7 @@ traverse_kernel(const TravArgs A) {
                         possible *= pw;
                     }
                     if (possible <= maxerr)
-                        select_method_gpu(mn, r_ref, r_qu, WR, (double)ni.y, D, A.h, maxerr,
+                        select_method_gpu(mn, r_ref, r_qu, WR, (double)ni.y, D, H.h, maxerr,
                                           A.plimit, A.ct, A.cross, A.kp, meth, p, bound);
                 }
                 const bool cand = meth != 0;
@@ -579,7 +588,7 @@ traverse_kernel(const TravArgs A) {
                 for (int c = 0; c < 2; c++) {
                     const int ch = c == 0 ? ni.z : ni.w;
                     double cl, chh, cm;
-                    entry_bounds<D>(A, sq, ch, cl, chh, cm, s_tab);
+                    entry_bounds<D>(A, sq, ch, H.neg_inv, cl, chh, cm, s_tab);
                     int slot = pos + c;
                     if (slot >= cap) slot -= cap;
                     if (slot >= cap) slot -= cap;
@@ -603,12 +612,12 @@ traverse_kernel(const TravArgs A) {
             unsigned f32_mask = 0;
             int anc = 0;
             double abs32 = 0.0;
-            if (A.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
+            if (H.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
                 bool use = false;
                 if ((small_mask >> lane) & 1u) {
                     anc = __ldg(A.r_anchor + ni.x);
-                    const double rho = fp32_item_bound<D>(A, sq, anc, klo, WR, abs32);
-                    use = rho <= A.fp32_rho && abs32 * tok_scale <= WR;
+                    const double rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, abs32);
+                    use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
             }
@@ -664,13 +673,13 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_commit();
                     __pipeline_wait_prior(0);
                     __syncwarp();
-                    sum32 += batch_f32<D>(xf, fst, gdl, total, A.ex2_scale);
+                    sum32 += batch_f32<D>(xf, fst, gdl, total, H.ex2_scale);
                     __syncwarp();
                 }
                 pt_est += sum32;
                 // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho, so
                 // sum32 (1 - fp32_rho) - sum(abs) <= S
-                pt_mass += fmax(sum32 * (1.0 - A.fp32_rho) - abs_sum, 0.0);
+                pt_mass += fmax(sum32 * (1.0 - H.fp32_rho) - abs_sum, 0.0);
             }
             const unsigned base64 = base_mask & ~f32_mask;
             const unsigned small64 = small_mask & ~f32_mask;
@@ -696,17 +705,16 @@ traverse_kernel(const TravArgs A) {
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * 32 * S;
-                    contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, A.neg_inv, s_tab)
-                                              : base_case<D, true>(x, bp, rc, A.neg_inv, s_tab);
+                    contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, H.neg_inv, s_tab)
+                                              : base_case<D, true>(x, bp, rc, H.neg_inv, s_tab);
                     __syncwarp();
                     bi ^= 1;
                 } else {
                     const double *rp = A.r_pw + (int64_t)rs * S;
-                    contrib = base_case<D, true>(x, rp, rc, A.neg_inv, s_tab);
+                    contrib = base_case<D, true>(x, rp, rc, H.neg_inv, s_tab);
                 }
                 pt_est += contrib;
-                if (A.no_eager) node_mass += wri * kli;
-                else pt_mass += contrib;
+                pt_mass += contrib;
                 if (A.use_tokens) tokens += wri;
                 c_base++;
                 c_pairs += (unsigned)(qn * rc);
@@ -730,7 +738,7 @@ traverse_kernel(const TravArgs A) {
             auto stage_item = [&](int k) {
                 const int node = sl[k].x;
                 double *dst = sbuf + (k % kRing) * slot;
-                const double *mom = A.r_mom + (int64_t)node * A.mom_K;
+                const double *mom = H.r_mom + (int64_t)node * A.mom_K;
                 for (int q = lane; q < A.K; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
                 if (lane < D) __pipeline_memcpy_async(dst + A.K + lane, A.r_c + (int64_t)node * D + lane, 8);
             };
@@ -750,16 +758,16 @@ traverse_kernel(const TravArgs A) {
                     __syncwarp();
                     const double *buf = sbuf + (i % kRing) * slot;
                     if constexpr (D == 3) {
-                        pt_est += eval_far_fixed3<PF>(x, buf + A.K, buf, p, 1.0 / A.sc,
+                        pt_est += eval_far_fixed3<PF>(x, buf + A.K, buf, p, H.inv_sc,
                                                       [&](double v) { return fg_exp_fast(v, s_tab); });
                     } else {
-                        pt_est += eval_far_fixed<D, PF>(x, buf + A.K, buf, p, 1.0 / A.sc);
+                        pt_est += eval_far_fixed<D, PF>(x, buf + A.K, buf, p, H.inv_sc);
                     }
                     __syncwarp();
                 } else {
                     const int node = sl[i].x;
                     pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)node * D,
-                                               A.r_mom + (int64_t)node * A.mom_K, p, A.kp[p], A.sc,
+                                               H.r_mom + (int64_t)node * A.mom_K, p, A.kp[p], H.sc,
                                                A.digits);
                 }
             }
@@ -770,44 +778,41 @@ traverse_kernel(const TravArgs A) {
                 const int meth = e.y >> 8, p = e.y & 0xff;
                 if (meth == 3) {
                     const int4 ni = A.r_ni[e.x];
-                    accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], A.sc,
+                    accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], H.sc,
                                        A.digits, A.inv_fact, loc, false);
                     c_dl++;
                 } else {
-                    h2l_warp_add<D>(A.r_mom + (int64_t)e.x * A.mom_K, A.r_c + (int64_t)e.x * D, qc,
-                                    p, A.kp[p], p, A.kp[p], A.sc, A.digits, A.inv_fact, A.degrees,
+                    h2l_warp_add<D>(H.r_mom + (int64_t)e.x * A.mom_K, A.r_c + (int64_t)e.x * D, qc,
+                                    p, A.kp[p], p, A.kp[p], H.sc, A.digits, A.inv_fact, A.degrees,
                                     loc);
                     c_h2l++;
                 }
                 local_used = true;
                 __syncwarp();
             }
-            if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, A.sc, A.digits);
+            if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, H.sc, A.digits);
         }
         const double val = pt_est + node_est;
-        if (A.prime_out) {
-            // |val - G| <= eps1 G  =>  G >= val / (1 + eps1) for every query
-            const double m = warp_min(valid ? val : CUDART_INF);
-            if (lane == 0) A.prime_out[b] = m * A.prime_scale;
-        } else if (valid) {
-            A.out[A.q_perm[qs + lane]] = val;
-        }
-        if (lane == 0 && A.cost) A.cost[b] = (unsigned long long)(clock64() - t_start);
+        if (valid) H.out[A.q_perm[qs + lane]] = val;
+        const unsigned long long cyc = (unsigned long long)(clock64() - t_start);
+        if (lane == 0 && A.cost) A.cost[b] = cyc;
         if (lane == 0 && A.dbg) {
-            A.dbg[4 * b + 0] = (unsigned long long)(clock64() - t_start);
+            A.dbg[4 * b + 0] = cyc;
             A.dbg[4 * b + 1] = steps;
             A.dbg[4 * b + 2] = c_vis;
             A.dbg[4 * b + 3] = c_pairs;
         }
         if (lane == 0) {
-            atomicAdd(A.counters + 0, (unsigned long long)c_vis);
-            atomicAdd(A.counters + 1, (unsigned long long)c_base);
-            atomicAdd(A.counters + 2, (unsigned long long)c_fd);
-            atomicAdd(A.counters + 3, (unsigned long long)c_dh);
-            atomicAdd(A.counters + 4, (unsigned long long)c_dl);
-            atomicAdd(A.counters + 5, (unsigned long long)c_h2l);
-            atomicAdd(A.counters + 6, (unsigned long long)c_pairs);
-            atomicAdd(A.counters + 7, (unsigned long long)c_f32);
+            unsigned long long *cn = H.counters;
+            atomicAdd(cn + 0, (unsigned long long)c_vis);
+            atomicAdd(cn + 1, (unsigned long long)c_base);
+            atomicAdd(cn + 2, (unsigned long long)c_fd);
+            atomicAdd(cn + 3, (unsigned long long)c_dh);
+            atomicAdd(cn + 4, (unsigned long long)c_dl);
+            atomicAdd(cn + 5, (unsigned long long)c_h2l);
+            atomicAdd(cn + 6, (unsigned long long)c_pairs);
+            atomicAdd(cn + 7, (unsigned long long)c_f32);
+            atomicAdd(cn + 8, cyc);
         }
         __syncwarp();
     }
