@@ -135,15 +135,23 @@ __device__ __forceinline__ double fg_exp_k(double x, const ExpK &K) {
     return __hiloint2double(__double2hiint(y) + ((k >> 8) << 20), __double2loint(y));
 }
 
-// full range: zero below -745.2, libdevice in the (rare) subnormal band
+// Full range without a slow path: below -708.3 the result is subnormal, so
+// exp(x) = exp(x + 64 ln2) 2^-64 with the first factor normal (the shifted
+// argument carries <= 2^-43 absolute rounding, i.e. <= 1.2e-13 relative, far
+// below the subnormal result's own resolution); zero below -745.2.
+constexpr double kExpShift = 44.361419555836500;  // 64 ln 2
 __device__ __forceinline__ double fg_exp_kc(double x, const ExpK &K) {
-    if (x < -708.3) return x < -745.2 ? 0.0 : exp(x);
-    return fg_exp_k(x, K);
+    const bool sub = x < -708.3;
+    double y = fg_exp_k(sub ? x + kExpShift : x, K);
+    if (sub) y *= 0x1.0p-64;
+    return x < -745.2 ? 0.0 : y;
 }
 
 __device__ __forceinline__ double fg_exp_fast(double x, const double *s_tab) {
-    if (x < -708.3) return x < -745.2 ? 0.0 : exp(x);
-    return fg_exp_normal(x, s_tab);
+    const bool sub = x < -708.3;
+    double y = fg_exp_normal(sub ? x + kExpShift : x, s_tab);
+    if (sub) y *= 0x1.0p-64;
+    return x < -745.2 ? 0.0 : y;
 }
 
 __device__ __forceinline__ double fg_exp(double x) { return exp(x); }

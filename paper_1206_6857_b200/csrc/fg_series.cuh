@@ -277,13 +277,12 @@ __device__ void h2l_warp_add(const double *__restrict__ A, const double *__restr
 
 // Smallest feasible order of each series method (the order scan of
 // error_bounds.py:196-225).  p == 0 marks an infeasible method.
-__device__ __forceinline__ void feasible_orders(double min_sq, double r_ref, double r_query,
-                                                double w_ref, double h, double maxerr,
-                                                int plimit, const double *ct,
+// base = an upper bound on W_R exp(-min_sq / 4h^2) (error_bounds.py:196).
+__device__ __forceinline__ void feasible_orders(double base, double r_ref, double r_query,
+                                                double maxerr, int plimit, const double *ct,
                                                 const double *cross, int &p_h, int &p_l,
                                                 int &p_t, double &e_h, double &e_l,
                                                 double &e_t) {
-    const double base = w_ref * exp(-0.25 * min_sq / (h * h));
     const double rr = r_ref, rq = r_query, sq = kSqrt2 * rq, sr = kSqrt2 * rr;
     p_h = p_l = p_t = 0;
     e_h = e_l = e_t = CUDART_INF;
@@ -325,16 +324,17 @@ __device__ __forceinline__ void feasible_orders(double min_sq, double r_ref, dou
 //   local      ~ N_R (32 D + ceil(K_p/32)(D + 1))
 //   H2L        ~ 32 D + ceil(K_p/32) K_p (D + 1)
 // Any feasible method keeps the error guarantee; only speed depends on this.
-__device__ __forceinline__ void select_method_gpu(double min_sq, double r_ref, double r_query,
-                                                  double w_ref, double n_ref, int dim,
-                                                  double h, double maxerr, int plimit,
-                                                  const double *ct, const double *cross,
-                                                  const int *kp, int &method, int &order,
-                                                  double &bound) {
+// base: an upper bound on W_R exp(-min_sq / 4h^2); the traversal passes
+// W_R sqrt(K_hi) from its own K_hi = exp(-min_sq / 2h^2) (see there).
+__device__ __forceinline__ void select_method_gpu(double base, double r_ref, double r_query,
+                                                  double n_ref, int dim, double maxerr,
+                                                  int plimit, const double *ct,
+                                                  const double *cross, const int *kp,
+                                                  int &method, int &order, double &bound) {
     int p_h, p_l, p_t;
     double e_h, e_l, e_t;
-    feasible_orders(min_sq, r_ref, r_query, w_ref, h, maxerr, plimit, ct, cross, p_h, p_l, p_t,
-                    e_h, e_l, e_t);
+    feasible_orders(base, r_ref, r_query, maxerr, plimit, ct, cross, p_h, p_l, p_t, e_h, e_l,
+                    e_t);
     const double d = (double)dim;
     double c_h = CUDART_INF, c_l = CUDART_INF, c_t = CUDART_INF;
     if (p_h) c_h = 32.0 * d + kp[p_h] * (d + 1.0);

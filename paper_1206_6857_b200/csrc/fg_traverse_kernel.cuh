@@ -192,27 +192,8 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             acc[u] = fma(CHECKED ? fg_exp_kc(d2[u] * neg_inv, K) : fg_exp_k(d2[u] * neg_inv, K),
                          w[u], acc[u]);
     }
-    double acc0 = acc[0], acc1 = acc[1];
-#pragma unroll
-    for (int u = 2; u < U; u++) acc0 += acc[u];
-    for (; j + 1 < rc; j += 2) {
-        double y0[D], y1[D], w0, w1;
-        read_point_w<D>(rp + (int64_t)j * S, y0, w0);
-        read_point_w<D>(rp + (int64_t)(j + 1) * S, y1, w1);
-        const double e0 = x[0] - y0[0], e1 = x[0] - y1[0];
-        double d0 = e0 * e0, d1 = e1 * e1;
-#pragma unroll
-        for (int d = 1; d < D; d++) {
-            const double f0 = x[d] - y0[d], f1 = x[d] - y1[d];
-            d0 = fma(f0, f0, d0);
-            d1 = fma(f1, f1, d1);
-        }
-        acc0 = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K),
-                   w0, acc0);
-        acc1 = fma(CHECKED ? fg_exp_kc(d1 * neg_inv, K) : fg_exp_k(d1 * neg_inv, K),
-                   w1, acc1);
-    }
-    if (j < rc) {
+#pragma unroll 1
+    for (; j < rc; j++) {
         double y0[D], w0;
         read_point_w<D>(rp + (int64_t)j * S, y0, w0);
         const double e0 = x[0] - y0[0];
@@ -222,10 +203,13 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
             const double f0 = x[d] - y0[d];
             d0 = fma(f0, f0, d0);
         }
-        acc0 = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K),
-                   w0, acc0);
+        acc[0] = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K), w0,
+                     acc[0]);
     }
-    return acc0 + acc1;
+    double s = acc[0];
+#pragma unroll
+    for (int u = 1; u < U; u++) s += acc[u];
+    return s;
 }
 
 // ---- FP32 base case --------------------------------------------------------
@@ -284,7 +268,11 @@ template <int D>
 __device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const double *sq, int anc,
                                                   double inv_h, double klo, double wr,
                                                   double &abs_err) {
-    const double a_max = klo > 0.0 ? -log(klo) : CUDART_INF;
+    // an upper bound on a_max = -ln K_lo (MUFU lg2: <= 2^-21 relative plus the
+    // FP32 rounding of K_lo, covered by the margins; +inf below FLT_MIN)
+    const float kf = (float)klo;
+    const double a_max = kf >= 1.17549435e-38f ? (double)(-__logf(kf)) * (1.0 + 0x1.0p-18) + 0x1.0p-18
+                                               : CUDART_INF;
     const double a_c = fmin(a_max, 80.0);
     abs_err = (a_max > 80.0 ? 2.0 * wr * 1.8048513878454153e-35 : 0.0) + 0x1.0p-140;
     const double *abox = A.r_box + (int64_t)anc * 2 * D;
@@ -543,15 +531,19 @@ traverse_kernel(const TravArgs A) {
                     const double r_ref = wr.y * H.inv_h;
                     const double r_qu = A.qb_rad[b] * H.inv_h;
                     const double rmin = r_ref < r_qu ? r_ref : r_qu;
-                    double possible = sqrt(khi) * WR * A.floor_c;
+                    // W_R exp(-min_sq / 4h^2) = W_R sqrt(K_hi), bounded above from
+                    // this engine's K_hi (<= 2.4e-14 relative error when normal,
+                    // <= 2^-1074 absolute when subnormal)
+                    const double base = WR * sqrt(khi + 0x1.0p-1073) * (1.0 + 0x1.0p-40);
+                    double possible = base * A.floor_c;
                     if (rmin < 1.0) {
                         double pw = 1.0;
                         for (int k = 0; k < A.plimit; k++) pw *= rmin;
                         possible *= pw;
                     }
                     if (possible <= maxerr)
-                        select_method_gpu(mn, r_ref, r_qu, WR, (double)ni.y, D, H.h, maxerr,
-                                          A.plimit, A.ct, A.cross, A.kp, meth, p, bound);
+                        select_method_gpu(base, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
+                                          A.ct, A.cross, A.kp, meth, p, bound);
                 }
                 const bool cand = meth != 0;
                 const double sreq = cand ? required_tokens(WR, bound, tok_scale)

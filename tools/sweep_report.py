@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--ref-leaf", type=int, default=0)
     ap.add_argument("--sub", type=int, default=2000)
     ap.add_argument("--naive", action="store_true", help="also time the full exhaustive kernel")
+    ap.add_argument("--sweep", action="store_true",
+                    help="one sweep_run over all bandwidths (after a warm-up sweep)")
     args = ap.parse_args()
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200 import _lib
@@ -41,6 +43,24 @@ def main():
     pl = fg.default_plimit(wl.dim)
     print(f"{wl.name} N={wl.n} D={wl.dim} build {t_build*1e3:.1f} ms nodes={rt.node_count} "
           f"levels={rt.levels}")
+    if args.sweep:
+        cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon, algorithm=args.algo)
+        fg.sweep_run(cfg, qt, rt, wl.bandwidths)
+        t0 = time.perf_counter()
+        results = fg.sweep_run(cfg, qt, rt, wl.bandwidths)
+        wall = time.perf_counter() - t0
+        for h, res in zip(wl.bandwidths, results):
+            exact = fg.naive_sum(qp[idx], wl.references, wl.weights, h).values
+            c = res.counters
+            print(json.dumps(dict(h=round(h, 6), kern_ms=round(res.seconds * 1e3, 3),
+                                  err=float(f"{oracle.max_rel_error(res.values[idx], exact):.3e}"),
+                                  exact_share=float(f"{c.exact_pairs / (wl.m * wl.n):.4f}"),
+                                  fp32_share=float(f"{c.fp32_pairs / (wl.m * wl.n):.4f}"),
+                                  visits=c.pair_visits, dh=c.hermite_prunes)), flush=True)
+        tot = sum(r.seconds for r in results)
+        print(f"sweep kernel ms {tot*1e3:.2f}, wall ms {wall*1e3:.2f}; effective pairs/s "
+              f"{wl.m * wl.n * len(wl.bandwidths) / wall:.3e}")
+        return
     tot = 0.0
     for h in wl.bandwidths:
         t0 = time.perf_counter()
