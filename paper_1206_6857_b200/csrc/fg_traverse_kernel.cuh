@@ -441,12 +441,14 @@ traverse_kernel(const TravArgs A) {
             for (int d = 0; d < D; d++) x[d] = sqc[d];
         }
         double pt_est = 0.0, pt_mass = 0.0;                    // per point
-        double node_est = 0.0, node_mass = 0.0, tokens = 0.0;  // per block (uniform)
+        double lane_est = 0.0;  // this lane's share of the node-level estimates
+        double tokens = 0.0;    // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
         int nh = 0, no = 0;  // deferred series items: Hermite from the front, others from the back
 
         // root entry
-        double fsum;  // sum over the frontier of W_R * K_lo
+        // mass = settled lower bounds + sum over the frontier of W_R * K_lo (uniform)
+        double mass;
         // Frontier: circular buffer [head, head + cnt) of capacity stack_cap.
         // Breadth-first (pop the oldest entries) while it holds fewer than
         // bfs_cap entries, so the frontier's K_lo bound tightens everywhere
@@ -463,7 +465,7 @@ traverse_kernel(const TravArgs A) {
                 skh[0] = khi;
                 smn[0] = mn;
             }
-            fsum = A.r_wr[0].x * klo;
+            mass = A.r_wr[0].x * klo;
         }
         __syncwarp();
 
@@ -497,9 +499,8 @@ traverse_kernel(const TravArgs A) {
             __syncwarp();
             const double WR = wr.x;
             c_vis += nb;
-            const double batch_sum = warp_sum(act ? WR * klo : 0.0);
             const double pmin = warp_min(valid ? pt_mass : CUDART_INF);
-            const double gmin = (pmin + node_mass + fsum) * kMassSafety;
+            const double gmin = (pmin + mass) * kMassSafety;
 
             // ---- finite-difference prune (summation_engine.py:327-351)
             const double fd_err = 0.5 * WR * (khi - klo);
@@ -560,8 +561,7 @@ traverse_kernel(const TravArgs A) {
                 nh += __popc(hm);
                 no += __popc(om);
             }
-            node_mass += warp_sum(settled);
-            node_est += warp_sum(est_add);
+            lane_est += est_add;
 
             // ---- descend or evaluate exactly (summation_engine.py:400-426)
             const bool rem = act && !fd && !((ser_mask >> lane) & 1u);
@@ -592,8 +592,11 @@ traverse_kernel(const TravArgs A) {
                 }
             }
             cnt += 2 * __popc(split_mask);
-            fsum = fsum - batch_sum + warp_sum(child_sum);
-            if (fsum < 0.0) fsum = 0.0;
+            // one reduction per step: popped entries leave the frontier, settled
+            // ones and pushed children enter the mass bound (base cases move
+            // into the per-point exact sums)
+            mass += warp_sum(settled + child_sum - (act ? WR * klo : 0.0));
+            if (mass < 0.0) mass = 0.0;
 
             // ---- exhaustive base cases, eager (dito_base, :221-250).  Items whose
             // FP32 error bound fits (decided lane-parallel, one item per lane) run
@@ -784,7 +787,7 @@ traverse_kernel(const TravArgs A) {
             }
             if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, H.sc, A.digits);
         }
-        const double val = pt_est + node_est;
+        const double val = pt_est + warp_sum(lane_est);
         if (valid) H.out[A.q_perm[qs + lane]] = val;
         const unsigned long long cyc = (unsigned long long)(clock64() - t_start);
         if (lane == 0 && A.cost) A.cost[b] = cyc;
