@@ -132,6 +132,7 @@ struct TreeDev {
     int levels = 0;
     double total_w = 0.0;
     std::vector<int64_t> level_begin;  // BFS node id range per level
+    DBuf level_begin_dev;              // the same, int, on the device
     DBuf pw;       // n x stride: coords then weight (tree order), padded
     DBuf perm;     // int64 n: tree position -> original index
     DBuf node_i;   // int4 nnodes: start, count, left, right (BFS ids, -1 = leaf)

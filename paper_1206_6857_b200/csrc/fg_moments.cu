@@ -12,10 +12,21 @@
 #include <vector>
 
 #include "fg_device.cuh"
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
 #include "fg_internal.cuh"
 #include "fg_series.cuh"
 
 namespace fg {
+namespace cg = cooperative_groups;
+// internal nodes with at most this many points get their moments directly
+// from their points, larger ones by H2H from their children (0: leaves only;
+// direct accumulation re-reads every point once per level, which measured
+// slower than H2H)
+constexpr int kDirectMax = 0;
+
 
 template <int D>
 __global__ void moments_leaf_kernel(int64_t node_begin, int64_t node_end,
@@ -28,7 +39,7 @@ __global__ void moments_leaf_kernel(int64_t node_begin, int64_t node_end,
     const int64_t node = node_begin + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (node >= node_end) return;
     const int4 ni = node_i[node];
-    if (ni.z >= 0) return;  // internal: handled by the H2H pass
+    if (ni.z >= 0 && ni.y > kDirectMax) return;  // large internal: H2H pass
     double c[D];
 #pragma unroll
     for (int d = 0; d < D; d++) c[d] = node_c[node * D + d];
@@ -36,49 +47,55 @@ __global__ void moments_leaf_kernel(int64_t node_begin, int64_t node_end,
                        mom + node * K, true);
 }
 
-// Internal nodes of one level: A = H2H(left) + H2H(right).
+// Internal nodes (> kDirectMax points), all levels bottom-up in ONE
+// cooperative launch (a grid barrier between levels): A = H2H(left) + H2H(right).
 template <int D>
-__global__ void moments_h2h_kernel(int64_t node_begin, int64_t node_end,
-                                   const int4 *__restrict__ node_i,
-                                   const double *__restrict__ node_c, int p, int K, double sc,
-                                   const uint8_t *__restrict__ digits,
-                                   const double *__restrict__ inv_fact,
-                                   const int *__restrict__ off, const int2 *__restrict__ ab,
-                                   double *__restrict__ mom) {
+__global__ void moments_h2h_coop_kernel(const int *__restrict__ level_begin, int levels,
+                                        const int4 *__restrict__ node_i,
+                                        const double *__restrict__ node_c, int p, int K, double sc,
+                                        const uint8_t *__restrict__ digits,
+                                        const double *__restrict__ inv_fact,
+                                        const int *__restrict__ off, const int2 *__restrict__ ab,
+                                        double *__restrict__ mom) {
+    cg::grid_group g = cg::this_grid();
     extern __shared__ double sh[];  // per warp: 2*K shift values
     const int lane = threadIdx.x & 31;
-    const int64_t node = node_begin + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int gwarps = gridDim.x * (blockDim.x >> 5);
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     double *shift = sh + (threadIdx.x >> 5) * 2 * K;
-    const bool live = node < node_end;
-    int4 ni = make_int4(0, 0, -1, -1);
-    if (live) ni = node_i[node];
-    const bool internal = live && ni.z >= 0;
-    if (internal) {
-        for (int c = 0; c < 2; c++) {
-            const int64_t ch = c == 0 ? ni.z : ni.w;
-            double pwt[D][2 * kMaxOrder];
+    for (int lv = levels - 1; lv >= 0; lv--) {
+        const int b = level_begin[lv], e = level_begin[lv + 1];
+        for (int node = b + gwarp; node < e; node += gwarps) {
+            const int4 ni = node_i[node];
+            if (ni.z < 0 || ni.y <= kDirectMax) continue;
+            for (int c = 0; c < 2; c++) {
+                const int64_t ch = c == 0 ? ni.z : ni.w;
+                double pwt[D][2 * kMaxOrder];
 #pragma unroll
-            for (int d = 0; d < D; d++)
-                power_ladder((node_c[ch * D + d] - node_c[node * D + d]) / sc, p - 1, pwt[d]);
-            for (int k = lane; k < K; k += 32)
-                shift[c * K + k] = product<D>(digits_of(digits, k), pwt) * inv_fact[k];
+                for (int d = 0; d < D; d++)
+                    power_ladder((node_c[ch * D + d] - node_c[(int64_t)node * D + d]) / sc, p - 1,
+                                 pwt[d]);
+                for (int k = lane; k < K; k += 32)
+                    shift[c * K + k] = product<D>(digits_of(digits, k), pwt) * inv_fact[k];
+            }
+            __syncwarp();
+            const double *Al = mom + (int64_t)ni.z * K;
+            const double *Ar = mom + (int64_t)ni.w * K;
+            for (int s = lane; s < K; s += 32) {
+                double l = 0.0, r = 0.0;
+                for (int q = off[s]; q < off[s + 1]; q++) {
+                    const int2 pr = ab[q];
+                    l += Al[pr.x] * shift[pr.y];
+                }
+                for (int q = off[s]; q < off[s + 1]; q++) {
+                    const int2 pr = ab[q];
+                    r += Ar[pr.x] * shift[K + pr.y];
+                }
+                mom[(int64_t)node * K + s] = l + r;
+            }
+            __syncwarp();
         }
-    }
-    __syncwarp();
-    if (!internal) return;
-    const double *Al = mom + (int64_t)ni.z * K;
-    const double *Ar = mom + (int64_t)ni.w * K;
-    for (int s = lane; s < K; s += 32) {
-        double l = 0.0, r = 0.0;
-        for (int q = off[s]; q < off[s + 1]; q++) {
-            const int2 pr = ab[q];
-            l += Al[pr.x] * shift[pr.y];
-        }
-        for (int q = off[s]; q < off[s + 1]; q++) {
-            const int2 pr = ab[q];
-            r += Ar[pr.x] * shift[K + pr.y];
-        }
-        mom[node * K + s] = l + r;
+        g.sync();
     }
 }
 
@@ -108,17 +125,40 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
             T.digits.as<uint8_t>(), T.inv_fact.as<double>(), dst.as<double>());
         FG_CUDA_TRY(cudaGetLastError());
     }
-    for (int lv = t.levels - 1; lv >= 0; lv--) {
-        const int64_t b = t.level_begin[lv], e = t.level_begin[lv + 1];
-        if (e <= b) continue;
-        const unsigned blocks = (unsigned)((e - b + warps_per_block - 1) / warps_per_block);
+    {
+        // one cooperative launch for the large internal nodes of every level
+        auto kern = moments_h2h_coop_kernel<D>;
+        const int threads = 32 * warps_per_block;
         const size_t smem = sizeof(double) * 2 * K * warps_per_block;
+        static int c_grid[9] = {0};
+        static size_t c_smem[9] = {0};
+        if (c_grid[D] == 0 || c_smem[D] != smem) {
+            int dev = 0, sms = 0, occ = 0;
+            FG_CUDA_TRY(cudaGetDevice(&dev));
+            FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            if (smem > 48 * 1024)
+                FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem));
+            FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            c_grid[D] = sms * std::max(1, std::min(occ, 2));
+            c_smem[D] = smem;
+        }
+        const int *lb = t.level_begin_dev.as<int>();
+        int levels = t.levels;
+        int p_ = p, K_ = K;
+        double sc_ = sc;
+        const int4 *ni = t.node_i.as<int4>();
+        const double *nc = t.node_c.as<double>();
+        const uint8_t *dg = T.digits.as<uint8_t>();
+        const double *ifa = T.inv_fact.as<double>();
+        const int *off = T.h2h_off.as<int>();
+        const int2 *ab = T.h2h_ab.as<int2>();
+        double *mom = dst.as<double>();
+        void *args[] = {(void *)&lb, &levels, (void *)&ni, (void *)&nc, &p_, &K_, &sc_,
+                        (void *)&dg, (void *)&ifa, (void *)&off, (void *)&ab, (void *)&mom};
         count_launch();
-        moments_h2h_kernel<D><<<blocks, 32 * warps_per_block, smem, stream()>>>(
-            b, e, t.node_i.as<int4>(), t.node_c.as<double>(), p, K, sc, T.digits.as<uint8_t>(),
-            T.inv_fact.as<double>(), T.h2h_off.as<int>(), T.h2h_ab.as<int2>(),
-            dst.as<double>());
-        FG_CUDA_TRY(cudaGetLastError());
+        FG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)kern, c_grid[D], threads, args, smem,
+                                                stream()));
     }
     return FG_OK;
 }

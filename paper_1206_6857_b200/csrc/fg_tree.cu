@@ -248,6 +248,9 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     std::vector<int> lb(levels + 1);
     FG_CUDA_TRY(cudaMemcpyAsync(lb.data(), B.level_begin.p, sizeof(int) * (levels + 1),
                                 cudaMemcpyDeviceToHost, stream()));
+    FG_TRY(t.level_begin_dev.reserve(sizeof(int) * (levels + 1)));
+    FG_CUDA_TRY(cudaMemcpyAsync(t.level_begin_dev.p, B.level_begin.p, sizeof(int) * (levels + 1),
+                                cudaMemcpyDeviceToDevice, stream()));
     // final packing
     FG_TRY(t.pw.reserve(sizeof(double) * n * packed_stride(D)));
     FG_TRY(t.perm.reserve(sizeof(int64_t) * n));
