@@ -41,7 +41,8 @@ constexpr int kPerThread = kChunk / kBuildThreads;  // 8
 constexpr int kMaxLevels = 1024;
 
 // control block (device): level state written by one thread between barriers
-enum { kNa = 0, kNchunks = 1, kNextBase = 2, kLevels = 3, kOverflow = 4, kCtl = 8 };
+enum { kNa = 0, kNchunks = 1, kNextBase = 2, kLevels = 3, kOverflow = 4, kSplit0 = 5, kCtl = 8 };
+// kSplit0..kSplit0+2: per-level split counters of the small-node phase (by level % 3)
 
 struct BuildBufs {
     DBuf x[2], w[2], idx[2];   // SoA coords (dim planes of n), weights, original index

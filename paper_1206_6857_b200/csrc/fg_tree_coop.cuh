@@ -6,6 +6,14 @@
 // A chunk finds its slot by binary search over the slots' chunk offsets, and
 // one 64-bit scan over the slots yields both the children's BFS ranks and
 // their chunk offsets.
+//
+// Once every active node fits one chunk (<= kChunk points), the rest of the
+// tree is built in the small-node phase: one warp owns a node for the whole
+// level (statistics, radius, split, stable partition) and allocates its
+// children with an atomic rank, so a level costs ONE grid barrier.  Ids stay
+// level-contiguous (BFS levels); their order within a level is the order of
+// allocation, which nothing downstream depends on (export maps to preorder
+// through the structure).
 #pragma once
 // (included inside namespace fg)
 
@@ -21,6 +29,156 @@ __device__ __forceinline__ int chunk_slot_of(const int *choff, int na, int c) {
         else hi = mid - 1;
     }
     return lo;
+}
+
+// Small-node phase (see the header comment): levels from `level` on, every
+// active node has <= kChunk points and one warp processes it start to finish.
+template <int D>
+__device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int level) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n = B.n;
+    const int gtid = blockIdx.x * kBuildThreads + threadIdx.x;
+    const int gwarps = gridDim.x * kBuildThreads / 32;
+    const int gwarp = gtid >> 5;
+    const int nmax = (int)B.nmax;
+    const unsigned lt = (1u << lane) - 1u;
+    if (level >= kMaxLevels) return;
+    int na = B.ctl[kNa];
+    int next_base = B.ctl[kNextBase];
+    if (gtid == 0) {
+        B.ctl[kSplit0 + level % 3] = 0;
+        B.ctl[kSplit0 + (level + 1) % 3] = 0;
+    }
+    g.sync();
+    for (; level < kMaxLevels && na > 0; level++) {
+        const int cur = level & 1;
+        const int *act = B.act[cur];
+        int *act_next = B.act[cur ^ 1];
+        const double *x = B.x[cur];
+        const double *w = B.w[cur];
+        const int *idx = B.idx[cur];
+        double *xn = B.x[cur ^ 1];
+        double *wn = B.w[cur ^ 1];
+        int *idxn = B.idx[cur ^ 1];
+        int *split_ctr = B.ctl + kSplit0 + level % 3;
+        // the counter of level + 1 was last read before the previous barrier
+        if (gtid == 0) B.ctl[kSplit0 + (level + 1) % 3] = 0;
+        for (int s = gwarp; s < na; s += gwarps) {
+            const int node = act[s];
+            int4 ni = B.node_i[node];
+            const int b = ni.x, e = ni.x + ni.y;
+            double lo[D], hi[D], sm[D], ws = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = CUDART_INF;
+                hi[d] = -CUDART_INF;
+                sm[d] = 0.0;
+            }
+            for (int i = b + lane; i < e; i += 32) {
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const double v = x[(int64_t)d * n + i];
+                    lo[d] = fmin(lo[d], v);
+                    hi[d] = fmax(hi[d], v);
+                    sm[d] += v;
+                }
+                ws += w[i];
+            }
+            int sd = 0;
+            double best = 0.0, ctr[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                lo[d] = warp_min(lo[d]);
+                hi[d] = warp_max(hi[d]);
+                sm[d] = warp_sum(sm[d]);
+                ctr[d] = sm[d] / (double)ni.y;
+                const double wd = hi[d] - lo[d];
+                if (d == 0 || wd > best) {
+                    best = wd;
+                    sd = d;
+                }
+            }
+            ws = warp_sum(ws);
+            const bool leafy = ni.y <= B.leaf || best == 0.0;
+            const double mid = 0.5 * (lo[sd] + hi[sd]);
+            double rad = 0.0;
+            int cnt = 0;
+            for (int i = b + lane; i < e; i += 32) {
+#pragma unroll
+                for (int d = 0; d < D; d++) rad = fmax(rad, fabs(x[(int64_t)d * n + i] - ctr[d]));
+                if (!leafy) cnt += x[(int64_t)sd * n + i] < mid ? 1 : 0;
+            }
+            rad = warp_max(rad);
+            const int nl = warp_sum(cnt);
+            const bool split = !leafy && nl > 0 && nl < ni.y;
+            if (lane < D) {
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    if (d == lane) {
+                        B.node_box[(int64_t)node * 2 * D + d] = lo[d];
+                        B.node_box[(int64_t)node * 2 * D + D + d] = hi[d];
+                        B.node_c[(int64_t)node * D + d] = ctr[d];
+                    }
+                }
+            }
+            if (lane == 0) B.node_wr[node] = make_double2(ws, rad);
+            if (!split) {
+                for (int i = b + lane; i < e; i += 32) {
+#pragma unroll
+                    for (int d = 0; d < D; d++) B.xf[(int64_t)d * n + i] = x[(int64_t)d * n + i];
+                    B.wf[i] = w[i];
+                    B.idxf[i] = idx[i];
+                }
+                continue;
+            }
+            // stable warp partition, 32 points per round, in order
+            int cl = 0, cr = 0;
+            for (int base = b; base < e; base += 32) {
+                const int i = base + lane;
+                const bool in = i < e;
+                const bool goes_left = in && x[(int64_t)sd * n + i] < mid;
+                const unsigned lm = __ballot_sync(kFull, goes_left);
+                const unsigned rm = __ballot_sync(kFull, in && !goes_left);
+                if (in) {
+                    const int dst = goes_left ? b + cl + __popc(lm & lt) : b + nl + cr + __popc(rm & lt);
+#pragma unroll
+                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = x[(int64_t)d * n + i];
+                    wn[dst] = w[i];
+                    idxn[dst] = idx[i];
+                }
+                cl += __popc(lm);
+                cr += __popc(rm);
+            }
+            int r = 0;
+            if (lane == 0) r = atomicAdd(split_ctr, 1);
+            r = __shfl_sync(kFull, r, 0);
+            const int L = next_base + 2 * r, R = L + 1;
+            if (lane == 0) {
+                if (R < nmax) {
+                    B.node_i[L] = make_int4(b, nl, -1, -1);
+                    B.node_i[R] = make_int4(b + nl, ni.y - nl, -1, -1);
+                    ni.z = L;
+                    ni.w = R;
+                    B.node_i[node] = ni;
+                    act_next[2 * r] = L;
+                    act_next[2 * r + 1] = R;
+                } else {
+                    B.ctl[kOverflow] = 1;
+                }
+            }
+        }
+        g.sync();
+        const int nsplit = *(volatile int *)split_ctr;
+        const bool overflow = *(volatile int *)(B.ctl + kOverflow) != 0;
+        if (gtid == 0) {
+            B.ctl[kLevels] = level + 1;
+            B.level_begin[level + 2] = next_base + 2 * nsplit;
+            B.ctl[kNextBase] = next_base + 2 * nsplit;
+            B.ctl[kNa] = overflow ? 0 : 2 * nsplit;
+        }
+        next_base += 2 * nsplit;
+        na = overflow ? 0 : 2 * nsplit;
+    }
 }
 
 template <int D>
@@ -43,11 +201,13 @@ build_coop_kernel(const BuildArgs B) {
     unsigned long long *val = reinterpret_cast<unsigned long long *>(B.part2) + 0;  // unused
     (void)val;
 
-    for (int level = 0; level < kMaxLevels; level++) {
+    int level = 0;
+    for (; level < kMaxLevels; level++) {
         const int cur = level & 1;
         const int na = B.ctl[kNa];
         if (na == 0) break;
         const int nchunks = B.ctl[kNchunks];
+        if (nchunks == na) break;  // every active node fits one chunk
         const int next_base = B.ctl[kNextBase];
         const int *act = B.act[cur];
         int *act_next = B.act[cur ^ 1];
@@ -337,4 +497,5 @@ build_coop_kernel(const BuildArgs B) {
         }
         g.sync();
     }
+    build_small_levels<D>(B, g, level);
 }
