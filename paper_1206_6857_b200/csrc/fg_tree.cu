@@ -53,8 +53,9 @@ struct BuildBufs {
     DBuf part;                 // per-chunk partial stats (3*dim+1 doubles)
     DBuf part2;                // per-chunk radius partial
     DBuf lcnt, loff;           // per-chunk left counts / left offsets within node
-    DBuf split_dim, split_mid, nleft, flag, rank, sval;
-    DBuf blk;                  // per-CTA scan totals
+    DBuf split_dim, split_mid, nleft, sval;
+    DBuf done;                 // last-done counters, 2 per slot, by level parity
+    DBuf lb_flag, lb_agg, lb_incl;  // per-CTA look-back state of the slot scan
     DBuf ctl, level_begin;
     DBuf bad;                  // validation flag
 };
@@ -73,8 +74,10 @@ struct BuildArgs {
     int *lcnt, *loff;
     int *split_dim;
     double *split_mid;
-    int *nleft, *flag, *rank;
-    unsigned long long *blk, *sval;
+    int *nleft;
+    unsigned long long *sval;
+    int *done, *lb_flag;
+    unsigned long long *lb_agg, *lb_incl;
     int *ctl, *level_begin;
     int4 *node_i;
     double *node_box, *node_c;
@@ -191,8 +194,6 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     A.split_dim = B.split_dim.as<int>();
     A.split_mid = B.split_mid.as<double>();
     A.nleft = B.nleft.as<int>();
-    A.flag = B.flag.as<int>();
-    A.rank = B.rank.as<int>();
     A.sval = B.sval.as<unsigned long long>();
     A.ctl = B.ctl.as<int>();
     A.level_begin = B.level_begin.as<int>();
@@ -235,8 +236,17 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
         grid_cache[D] = sms * std::max(1, std::min(occ, cap));
     }
     const int grid = grid_cache[D];
-    FG_TRY(B.blk.reserve(sizeof(unsigned long long) * (grid + 1)));
-    A.blk = B.blk.as<unsigned long long>();
+    FG_TRY(B.lb_flag.reserve(sizeof(int) * grid));
+    FG_TRY(B.lb_agg.reserve(sizeof(unsigned long long) * grid));
+    FG_TRY(B.lb_incl.reserve(sizeof(unsigned long long) * grid));
+    FG_CUDA_TRY(cudaMemsetAsync(B.lb_flag.p, 0, sizeof(int) * grid, stream()));
+    // level 0's slot (the root); later slots are zeroed when they are allocated
+    FG_CUDA_TRY(cudaMemsetAsync(B.done.p, 0, sizeof(int), stream()));
+    FG_CUDA_TRY(cudaMemsetAsync(B.done.as<int>() + nmax, 0, sizeof(int), stream()));
+    A.lb_flag = B.lb_flag.as<int>();
+    A.lb_agg = B.lb_agg.as<unsigned long long>();
+    A.lb_incl = B.lb_incl.as<unsigned long long>();
+    A.done = B.done.as<int>();
     void *args[] = {(void *)&A};
     count_launch();
     FG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_coop_kernel<D>, grid,
@@ -301,8 +311,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_TRY(B.split_dim.reserve(sizeof(int) * nmax));
     FG_TRY(B.split_mid.reserve(sizeof(double) * nmax));
     FG_TRY(B.nleft.reserve(sizeof(int) * nmax));
-    FG_TRY(B.flag.reserve(sizeof(int) * nmax));
-    FG_TRY(B.rank.reserve(sizeof(int) * nmax));
+    FG_TRY(B.done.reserve(sizeof(int) * 4 * nmax));
     FG_TRY(B.sval.reserve(sizeof(unsigned long long) * nmax));
     FG_TRY(B.ctl.reserve(sizeof(int) * kCtl));
     FG_TRY(B.level_begin.reserve(sizeof(int) * (kMaxLevels + 2)));

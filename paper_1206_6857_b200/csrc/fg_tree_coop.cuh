@@ -1,8 +1,11 @@
 // fg_tree_coop.cuh -- the single-launch cooperative kd-tree build kernel
-// (included by fg_tree.cu).  Seven grid-wide barriers per level:
-//   P2 chunk statistics | P3 node combine + split choice | P4 radius + left
-//   counts | P5 split decision | P6 stable scatter + scan phase 1 |
-//   scan phase 2 | scan phase 3 + child allocation.
+// (included by fg_tree.cu).  Three grid-wide barriers per level:
+//   A: chunk statistics; the warp that completes a node's last chunk (atomic
+//      count) combines the partials in chunk order and picks the split |
+//   B: chunk radius partials and left counts; the last warp of a node
+//      combines them, writes per-chunk left offsets and decides the split |
+//   C: scan over the slots with a decoupled look-back + child allocation,
+//      then the stable scatter.
 // A chunk finds its slot by binary search over the slots' chunk offsets, and
 // one 64-bit scan over the slots yields both the children's BFS ranks and
 // their chunk offsets.
@@ -185,21 +188,14 @@ template <int D>
 __global__ void __launch_bounds__(kBuildThreads)
 build_coop_kernel(const BuildArgs B) {
     cg::grid_group g = cg::this_grid();
-    __shared__ double sh[(kBuildThreads / 32) * (3 * D + 1)];
-    __shared__ union {
-        typename BlockScanInt::TempStorage i32;
-        typename BlockScanU64::TempStorage u64;
-    } scan_tmp;
-    __shared__ double shr[kBuildThreads / 32];
-    __shared__ int shc[kBuildThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ typename BlockScanU64::TempStorage scan_tmp;
+    __shared__ unsigned long long s_prefix;
+    const int lane = threadIdx.x & 31;
     const int64_t n = B.n;
     const int gtid = blockIdx.x * kBuildThreads + threadIdx.x;
     const int gwarps = gridDim.x * kBuildThreads / 32;
     const int gwarp = gtid >> 5;
     const int nmax = (int)B.nmax;
-    unsigned long long *val = reinterpret_cast<unsigned long long *>(B.part2) + 0;  // unused
-    (void)val;
 
     int level = 0;
     for (; level < kMaxLevels; level++) {
@@ -213,15 +209,19 @@ build_coop_kernel(const BuildArgs B) {
         int *act_next = B.act[cur ^ 1];
         const int *choff = B.choff + cur * nmax;
         int *choff_next = B.choff + (cur ^ 1) * nmax;
+        int *done_a = B.done + cur * 2 * nmax, *done_b = done_a + nmax;
+        int *done_next = B.done + (cur ^ 1) * 2 * nmax;
         const double *x = B.x[cur];
         const double *w = B.w[cur];
         const int *idx = B.idx[cur];
         auto chunk_end = [&](int s) { return s + 1 < na ? choff[s + 1] : nchunks; };
 
-        // ---- P2: per-chunk min / max / sum / weight
+        // ---- phase A: per-chunk min / max / sum / weight; the warp finishing a
+        // node's last chunk combines its partials (fixed order) and picks the split
         for (int c = gwarp; c < nchunks; c += gwarps) {
             const int s = chunk_slot_of(choff, na, c);
-            const int4 ni = B.node_i[act[s]];
+            const int node = act[s];
+            const int4 ni = B.node_i[node];
             const int cb = ni.x + (c - choff[s]) * kChunk;
             const int ce = min(cb + kChunk, ni.x + ni.y);
             double lo[D], hi[D], sm[D], ws = 0.0;
@@ -248,6 +248,8 @@ build_coop_kernel(const BuildArgs B) {
                 sm[d] = warp_sum(sm[d]);
             }
             ws = warp_sum(ws);
+            const int c0 = choff[s], c1 = chunk_end(s);
+            int last = 0;
             if (lane == 0) {
                 double *p = B.part + (int64_t)c * (3 * D + 1);
 #pragma unroll
@@ -257,31 +259,27 @@ build_coop_kernel(const BuildArgs B) {
                     p[2 * D + d] = sm[d];
                 }
                 p[3 * D] = ws;
+                __threadfence();
+                last = atomicAdd(done_a + s, 1) == c1 - c0 - 1;
             }
-        }
-        g.sync();
-
-        // ---- P3: combine chunk partials per node, choose the split (warp per slot)
-        for (int s = gwarp; s < na; s += gwarps) {
-            const int node = act[s];
-            const int4 ni = B.node_i[node];
-            double lo[D], hi[D], sm[D], ws = 0.0;
+            if (!__shfl_sync(kFull, last, 0)) continue;
+            __threadfence();
 #pragma unroll
             for (int d = 0; d < D; d++) {
                 lo[d] = CUDART_INF;
                 hi[d] = -CUDART_INF;
                 sm[d] = 0.0;
             }
-            const int c0 = choff[s], c1 = chunk_end(s);
-            for (int c = c0 + lane; c < c1; c += 32) {
-                const double *p = B.part + (int64_t)c * (3 * D + 1);
+            ws = 0.0;
+            for (int cc = c0 + lane; cc < c1; cc += 32) {
+                const double *p = B.part + (int64_t)cc * (3 * D + 1);
 #pragma unroll
                 for (int d = 0; d < D; d++) {
-                    lo[d] = fmin(lo[d], p[d]);
-                    hi[d] = fmax(hi[d], p[D + d]);
-                    sm[d] += p[2 * D + d];
+                    lo[d] = fmin(lo[d], __ldcg(p + d));
+                    hi[d] = fmax(hi[d], __ldcg(p + D + d));
+                    sm[d] += __ldcg(p + 2 * D + d);
                 }
-                ws += p[3 * D];
+                ws += __ldcg(p + 3 * D);
             }
 #pragma unroll
             for (int d = 0; d < D; d++) {
@@ -313,7 +311,10 @@ build_coop_kernel(const BuildArgs B) {
         }
         g.sync();
 
-        // ---- P4: per chunk inf-norm radius partial and left count
+        // ---- phase B: per-chunk inf-norm radius partial and left count; the
+        // warp finishing a node's last chunk combines them, writes the per-chunk
+        // left offsets and decides the split.  The slot's scan value packs
+        // (is_split, chunks of its two children).
         for (int c = gwarp; c < nchunks; c += gwarps) {
             const int s = chunk_slot_of(choff, na, c);
             const int node = act[s];
@@ -334,32 +335,29 @@ build_coop_kernel(const BuildArgs B) {
             }
             rad = warp_max(rad);
             cnt = warp_sum(cnt);
+            const int c0 = choff[s], c1 = chunk_end(s);
+            int last = 0;
             if (lane == 0) {
                 B.part2[c] = rad;
                 B.lcnt[c] = cnt;
+                __threadfence();
+                last = atomicAdd(done_b + s, 1) == c1 - c0 - 1;
             }
-        }
-        g.sync();
-
-        // ---- P5: radius, left count, per-chunk left offsets, final leaf test;
-        // the slot's scan value packs (is_split, chunks of its two children)
-        for (int s = gwarp; s < na; s += gwarps) {
-            const int node = act[s];
-            const int4 ni = B.node_i[node];
-            const int c0 = choff[s], c1 = chunk_end(s);
-            double rad = 0.0;
+            if (!__shfl_sync(kFull, last, 0)) continue;
+            __threadfence();
+            rad = 0.0;
             int run = 0;
             for (int base = c0; base < c1; base += 32) {
-                const int c = base + lane;
-                const int v = c < c1 ? B.lcnt[c] : 0;
-                if (c < c1) rad = fmax(rad, B.part2[c]);
+                const int cc = base + lane;
+                const int v = cc < c1 ? __ldcg(B.lcnt + cc) : 0;
+                if (cc < c1) rad = fmax(rad, __ldcg(B.part2 + cc));
                 int incl = v;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int t = __shfl_up_sync(kFull, incl, o);
                     if (lane >= o) incl += t;
                 }
-                if (c < c1) B.loff[c] = run + incl - v;
+                if (cc < c1) B.loff[cc] = run + incl - v;
                 run += __shfl_sync(kFull, incl, 31);
             }
             rad = warp_max(rad);
@@ -367,7 +365,6 @@ build_coop_kernel(const BuildArgs B) {
                 double2 wr = B.node_wr[node];
                 wr.y = rad;
                 B.node_wr[node] = wr;
-                const int sd = B.split_dim[s];
                 const bool split = sd >= 0 && run > 0 && run < ni.y;
                 if (!split) B.split_dim[s] = -1;
                 B.nleft[s] = run;
@@ -380,7 +377,85 @@ build_coop_kernel(const BuildArgs B) {
         }
         g.sync();
 
-        // ---- P6: stable scatter (leaves -> final arrays, splits -> next buffers)
+        // ---- phase C: (1) scan over the slots with a decoupled look-back (CTA b
+        // owns slots [b*per, (b+1)*per)) and child allocation; (2) the stable
+        // scatter of every chunk (leaves -> final arrays, splits -> next buffers)
+        {
+            const int nb = gridDim.x;
+            const int per = (na + nb - 1) / nb;
+            const int s0 = min(na, (int)blockIdx.x * per), s1 = min(na, s0 + per);
+            const int stamp = (level + 1) << 2;
+            unsigned long long local = 0, agg;
+            for (int s = s0 + threadIdx.x; s < s1; s += kBuildThreads) local += B.sval[s];
+            BlockScanU64(scan_tmp).ExclusiveSum(local, local, agg);
+            if (threadIdx.x == 0) {
+                B.lb_agg[blockIdx.x] = agg;
+                __threadfence();
+                atomicExch(B.lb_flag + blockIdx.x, stamp | 1);
+                unsigned long long prefix = 0;
+                for (int p = (int)blockIdx.x - 1; p >= 0; p--) {
+                    int f;
+                    do {
+                        f = *(volatile int *)(B.lb_flag + p);
+                    } while ((f & ~3) != stamp);
+                    __threadfence();
+                    if ((f & 3) == 2) {
+                        prefix += __ldcg(B.lb_incl + p);
+                        break;
+                    }
+                    prefix += __ldcg(B.lb_agg + p);
+                }
+                B.lb_incl[blockIdx.x] = prefix + agg;
+                __threadfence();
+                atomicExch(B.lb_flag + blockIdx.x, stamp | 2);
+                s_prefix = prefix;
+                if (blockIdx.x == nb - 1) {
+                    const unsigned long long total = prefix + agg;
+                    const int nsplit = (int)(total & 0xffffffffull);
+                    const int nchunks_next = (int)(total >> 32);
+                    if (next_base + 2 * nsplit > nmax) B.ctl[kOverflow] = 1;
+                    B.ctl[kNa] = B.ctl[kOverflow] ? 0 : 2 * nsplit;
+                    B.ctl[kNchunks] = nchunks_next;
+                    B.ctl[kNextBase] = next_base + 2 * nsplit;
+                    B.ctl[kLevels] = level + 1;
+                    // level l+1 spans [next_base, next_base + 2*nsplit): its end
+                    // is the start of level l+2
+                    B.level_begin[level + 2] = next_base + 2 * nsplit;
+                }
+            }
+            __syncthreads();
+            unsigned long long carry = s_prefix;
+            for (int base = s0; base < s1; base += kBuildThreads) {
+                const int s = base + threadIdx.x;
+                const unsigned long long v = s < s1 ? B.sval[s] : 0ull;
+                unsigned long long ex, t;
+                __syncthreads();
+                BlockScanU64(scan_tmp).ExclusiveSum(v, ex, t);
+                ex += carry;
+                carry += t;
+                if (s < s1 && (v & 1ull)) {
+                    const int r = (int)(ex & 0xffffffffull);
+                    const int coff = (int)(ex >> 32);
+                    const int node = act[s];
+                    int4 ni = B.node_i[node];
+                    const int L = next_base + 2 * r, R = L + 1;
+                    const int nl = B.nleft[s];
+                    if (R < nmax) {
+                        B.node_i[L] = make_int4(ni.x, nl, -1, -1);
+                        B.node_i[R] = make_int4(ni.x + nl, ni.y - nl, -1, -1);
+                        ni.z = L;
+                        ni.w = R;
+                        B.node_i[node] = ni;
+                        act_next[2 * r] = L;
+                        act_next[2 * r + 1] = R;
+                        choff_next[2 * r] = coff;
+                        choff_next[2 * r + 1] = coff + (nl + kChunk - 1) / kChunk;
+                        done_next[2 * r] = done_next[2 * r + 1] = 0;
+                        done_next[nmax + 2 * r] = done_next[nmax + 2 * r + 1] = 0;
+                    }
+                }
+            }
+        }
         for (int c = gwarp; c < nchunks; c += gwarps) {
             const int s = chunk_slot_of(choff, na, c);
             const int4 ni = B.node_i[act[s]];
@@ -421,78 +496,6 @@ build_coop_kernel(const BuildArgs B) {
                 }
                 nl += __popc(lm);
                 nr += __popc(rm);
-            }
-        }
-        // scan phase 1 over the slots: CTA b owns slots [b*per, (b+1)*per)
-        const int nb = gridDim.x;
-        const int per = (na + nb - 1) / nb;
-        const int s0 = blockIdx.x * per, s1 = min(na, s0 + per);
-        {
-            unsigned long long local = 0, tot;
-            for (int s = s0 + threadIdx.x; s < s1; s += kBuildThreads) local += B.sval[s];
-            __syncthreads();
-            BlockScanU64(scan_tmp.u64).ExclusiveSum(local, local, tot);
-            if (threadIdx.x == 0) B.blk[blockIdx.x] = tot;
-        }
-        g.sync();
-        // scan phase 2: CTA 0 scans the CTA totals
-        if (blockIdx.x == 0) {
-            unsigned long long carry = 0;
-            for (int base = 0; base < nb; base += kBuildThreads) {
-                const int i = base + threadIdx.x;
-                unsigned long long v = i < nb ? B.blk[i] : 0ull, ex, t;
-                __syncthreads();
-                BlockScanU64(scan_tmp.u64).ExclusiveSum(v, ex, t);
-                if (i < nb) B.blk[i] = carry + ex;
-                carry += t;
-            }
-            if (threadIdx.x == 0) B.blk[nb] = carry;
-        }
-        g.sync();
-        // scan phase 3 + child allocation: each split slot learns its rank r
-        // (children get BFS ids next_base + 2r, +1) and its children's chunk offsets
-        {
-            unsigned long long carry = B.blk[blockIdx.x];
-            const unsigned long long total = B.blk[nb];
-            const int nsplit = (int)(total & 0xffffffffull);
-            const int nchunks_next = (int)(total >> 32);
-            for (int base = s0; base < s1; base += kBuildThreads) {
-                const int s = base + threadIdx.x;
-                const unsigned long long v = s < s1 ? B.sval[s] : 0ull;
-                unsigned long long ex, t;
-                __syncthreads();
-                BlockScanU64(scan_tmp.u64).ExclusiveSum(v, ex, t);
-                ex += carry;
-                carry += t;
-                if (s < s1 && (v & 1ull)) {
-                    const int r = (int)(ex & 0xffffffffull);
-                    const int coff = (int)(ex >> 32);
-                    const int node = act[s];
-                    int4 ni = B.node_i[node];
-                    const int L = next_base + 2 * r, R = L + 1;
-                    const int nl = B.nleft[s];
-                    if (R < nmax) {
-                        B.node_i[L] = make_int4(ni.x, nl, -1, -1);
-                        B.node_i[R] = make_int4(ni.x + nl, ni.y - nl, -1, -1);
-                        ni.z = L;
-                        ni.w = R;
-                        B.node_i[node] = ni;
-                    }
-                    act_next[2 * r] = L;
-                    act_next[2 * r + 1] = R;
-                    choff_next[2 * r] = coff;
-                    choff_next[2 * r + 1] = coff + (nl + kChunk - 1) / kChunk;
-                }
-            }
-            if (gtid == 0) {
-                if (next_base + 2 * nsplit > nmax) B.ctl[kOverflow] = 1;
-                B.ctl[kNa] = B.ctl[kOverflow] ? 0 : 2 * nsplit;
-                B.ctl[kNchunks] = nchunks_next;
-                B.ctl[kNextBase] = next_base + 2 * nsplit;
-                B.ctl[kLevels] = level + 1;
-                // level l+1 spans [next_base, next_base + 2*nsplit): its end is the
-                // start of level l+2
-                B.level_begin[level + 2] = next_base + 2 * nsplit;
             }
         }
         g.sync();
