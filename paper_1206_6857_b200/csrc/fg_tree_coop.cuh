@@ -383,44 +383,58 @@ build_coop_kernel(const BuildArgs B) {
         {
             const int nb = gridDim.x;
             const int per = (na + nb - 1) / nb;
+            const int npart = (na + per - 1) / per;  // CTAs that own slots
             const int s0 = min(na, (int)blockIdx.x * per), s1 = min(na, s0 + per);
             const int stamp = (level + 1) << 2;
-            unsigned long long local = 0, agg;
-            for (int s = s0 + threadIdx.x; s < s1; s += kBuildThreads) local += B.sval[s];
-            BlockScanU64(scan_tmp).ExclusiveSum(local, local, agg);
-            if (threadIdx.x == 0) {
-                B.lb_agg[blockIdx.x] = agg;
-                __threadfence();
-                atomicExch(B.lb_flag + blockIdx.x, stamp | 1);
-                unsigned long long prefix = 0;
-                for (int p = (int)blockIdx.x - 1; p >= 0; p--) {
-                    int f;
-                    do {
-                        f = *(volatile int *)(B.lb_flag + p);
-                    } while ((f & ~3) != stamp);
+            unsigned long long local = 0, agg = 0;
+            if ((int)blockIdx.x < npart) {
+                for (int s = s0 + threadIdx.x; s < s1; s += kBuildThreads) local += B.sval[s];
+                BlockScanU64(scan_tmp).ExclusiveSum(local, local, agg);
+            }
+            if ((int)blockIdx.x < npart && threadIdx.x < 32) {
+                // warp-wide look-back over 32 predecessors at a time
+                if (lane == 0) {
+                    B.lb_agg[blockIdx.x] = agg;
                     __threadfence();
-                    if ((f & 3) == 2) {
-                        prefix += __ldcg(B.lb_incl + p);
-                        break;
-                    }
-                    prefix += __ldcg(B.lb_agg + p);
+                    atomicExch(B.lb_flag + blockIdx.x, stamp | 1);
                 }
-                B.lb_incl[blockIdx.x] = prefix + agg;
-                __threadfence();
-                atomicExch(B.lb_flag + blockIdx.x, stamp | 2);
-                s_prefix = prefix;
-                if (blockIdx.x == nb - 1) {
-                    const unsigned long long total = prefix + agg;
-                    const int nsplit = (int)(total & 0xffffffffull);
-                    const int nchunks_next = (int)(total >> 32);
-                    if (next_base + 2 * nsplit > nmax) B.ctl[kOverflow] = 1;
-                    B.ctl[kNa] = B.ctl[kOverflow] ? 0 : 2 * nsplit;
-                    B.ctl[kNchunks] = nchunks_next;
-                    B.ctl[kNextBase] = next_base + 2 * nsplit;
-                    B.ctl[kLevels] = level + 1;
-                    // level l+1 spans [next_base, next_base + 2*nsplit): its end
-                    // is the start of level l+2
-                    B.level_begin[level + 2] = next_base + 2 * nsplit;
+                unsigned long long prefix = 0;
+                for (int p_end = (int)blockIdx.x; p_end > 0; p_end -= 32) {
+                    const int p = p_end - 1 - lane;
+                    int f = stamp | 2;
+                    if (p >= 0) {
+                        do {
+                            f = *(volatile int *)(B.lb_flag + p);
+                        } while ((f & ~3) != stamp);
+                    }
+                    __threadfence();
+                    const unsigned inc = __ballot_sync(kFull, p < 0 || (f & 3) == 2);
+                    const int k = inc ? __ffs(inc) - 1 : 32;
+                    unsigned long long v = 0;
+                    if (p >= 0 && lane < k) v = __ldcg(B.lb_agg + p);
+                    else if (p >= 0 && lane == k) v = __ldcg(B.lb_incl + p);
+                    prefix += warp_sum(v);
+                    if (k < 32) break;
+                }
+                if (lane == 0) {
+                    B.lb_incl[blockIdx.x] = prefix + agg;
+                    __threadfence();
+                    atomicExch(B.lb_flag + blockIdx.x, stamp | 2);
+                    s_prefix = prefix;
+                    if ((int)blockIdx.x == npart - 1) {
+                        // the last owner holds the grand total: next level's control
+                        const unsigned long long total = prefix + agg;
+                        const int nsplit = (int)(total & 0xffffffffull);
+                        const int nchunks_next = (int)(total >> 32);
+                        if (next_base + 2 * nsplit > nmax) B.ctl[kOverflow] = 1;
+                        B.ctl[kNa] = B.ctl[kOverflow] ? 0 : 2 * nsplit;
+                        B.ctl[kNchunks] = nchunks_next;
+                        B.ctl[kNextBase] = next_base + 2 * nsplit;
+                        B.ctl[kLevels] = level + 1;
+                        // level l+1 spans [next_base, next_base + 2*nsplit): its
+                        // end is the start of level l+2
+                        B.level_begin[level + 2] = next_base + 2 * nsplit;
+                    }
                 }
             }
             __syncthreads();
