@@ -13,6 +13,8 @@
 namespace fg {
 
 constexpr int kTravThreads = 128;
+// largest FP32 base item (and anchor) in points; FP64 items are staged when <= 32
+constexpr int kAnchorMax = 64;
 constexpr int kTravWarps = kTravThreads / 32;
 // Relative safety margin on the running mass bound: the frontier sum is kept
 // incrementally, so it carries <= (#updates) ulps of drift relative to G_min.
@@ -603,7 +605,7 @@ traverse_kernel(const TravArgs A) {
             // as one FP32 batch; the rest (FP64) are staged one by one into shared
             // memory with cp.async, double-buffered so the next item's points load
             // while this one computes (leaves of > 32 points read global memory).
-            const unsigned small_mask = __ballot_sync(kFull, ni.y <= 32) & base_mask;
+            const unsigned small_mask = __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask;
             unsigned f32_mask = 0;
             int anc = 0;
             double abs32 = 0.0;
@@ -654,14 +656,16 @@ traverse_kernel(const TravArgs A) {
                         const int rs = __shfl_sync(kFull, ni.x, i);
                         const int rc = __shfl_sync(kFull, ni.y, i);
                         const int o = __shfl_sync(kFull, off, i) - base;
-                        if (lane < rc) {
-                            const float *src = A.r_pf + (int64_t)(rs + lane) * F;
+                        for (int l = lane; l < ((rc + 3) & ~3); l += 32) {
+                            if (l < rc) {
+                                const float *src = A.r_pf + (int64_t)(rs + l) * F;
 #pragma unroll
-                            for (int c = 0; c <= D; c++)
-                                __pipeline_memcpy_async(fst + c * CAP + o + lane, src + c, 4);
-                        } else if (lane < ((rc + 3) & ~3)) {
+                                for (int c = 0; c <= D; c++)
+                                    __pipeline_memcpy_async(fst + c * CAP + o + l, src + c, 4);
+                            } else {
 #pragma unroll
-                            for (int c = 0; c <= D; c++) fst[c * CAP + o + lane] = 0.f;
+                                for (int c = 0; c <= D; c++) fst[c * CAP + o + l] = 0.f;
+                            }
                         }
                         total = o + ((rc + 3) & ~3);
                     }
@@ -677,7 +681,7 @@ traverse_kernel(const TravArgs A) {
                 pt_mass += fmax(sum32 * (1.0 - H.fp32_rho) - abs_sum, 0.0);
             }
             const unsigned base64 = base_mask & ~f32_mask;
-            const unsigned small64 = small_mask & ~f32_mask;
+            const unsigned small64 = __ballot_sync(kFull, ni.y <= 32) & base_mask & ~f32_mask;
             int bi = 0;
             if (small64) stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(small64) - 1, sbuf);
             for (unsigned m = base64; m; m &= m - 1) {
