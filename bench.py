@@ -123,8 +123,9 @@ class ClockSampler:
 
 def profiled_traffic():
     """dram read+write bytes per launch of the dominant kernel, from the
-    committed `ncu --set full` summary (profiles/, one C2 h=0.1126 launch of
-    this same bench command).  Null when no summary is present."""
+    committed `ncu --set full` summary (profiles/, one traversal launch of this
+    same bench command: the whole 10-bandwidth sweep of one step).  Null when
+    no summary is present."""
     import glob
     import re
 
@@ -140,7 +141,7 @@ def profiled_traffic():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[m.group(2)]
         tot += float(m.group(1)) * scale
     return {"bytes_per_launch": tot, "source": os.path.basename(files[-1]),
-            "launch": "C2 bandwidth index 6 (h=0.1126)"}
+            "launch": "one C2 step's sweep launch (10 bandwidths)"}
 
 
 # ------------------------------------------------------------ CPU side

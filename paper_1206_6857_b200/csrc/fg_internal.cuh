@@ -141,6 +141,10 @@ struct TreeDev {
     DBuf node_wr;  // double2 nnodes: weight, inf_radius
     // moments (bandwidth-dependent), K per node, BFS numbering
     DBuf mom, mom0;
+    // direct-moment work items (node, chunk): bandwidth-independent
+    bool mom_items_valid = false;
+    int mom_nitems = 0;
+    DBuf mom_items, mom_off;
     int mom_order = 0, mom_K = 0;
     double mom_h = 0.0, mom0_h = 0.0;
     bool mom_valid = false, mom0_valid = false;

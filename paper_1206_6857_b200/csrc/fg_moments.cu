@@ -1,10 +1,8 @@
 // fg_moments.cu -- K5: far-field moments per reference node
 // (replaces KdTree.refresh_moments, spatial_index.py:171-197).
 //
-// Direct accumulation at the leaves (accumulate_far_field,
-// series_expansion.py:76-92) and exact H2H shifts bottom-up level by level
-// (translate_h2h + add_far_field, :139-164), one warp per node with lanes
-// owning coefficients.  The first refresh for a given order is kept as a base
+// Direct chunked accumulation for every node (see moments_direct).  The first
+// refresh for a given order is kept as a base
 // (h0); later refreshes at other bandwidths apply the exact rescaling law
 // A_a(h) = (h0/h)^{|a|} A_a(h0), pinned by the reference's
 // tests/test_spatial_index.py:147-162, as one elementwise kernel.
@@ -12,7 +10,7 @@
 #include <vector>
 
 #include "fg_device.cuh"
-#include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 
@@ -20,84 +18,7 @@
 #include "fg_series.cuh"
 
 namespace fg {
-namespace cg = cooperative_groups;
-// internal nodes with at most this many points get their moments directly
-// from their points, larger ones by H2H from their children (0: leaves only;
-// direct accumulation re-reads every point once per level, which measured
-// slower than H2H)
-constexpr int kDirectMax = 0;
 
-
-template <int D>
-__global__ void moments_leaf_kernel(int64_t node_begin, int64_t node_end,
-                                    const int4 *__restrict__ node_i,
-                                    const double *__restrict__ node_c,
-                                    const double *__restrict__ pw, int p, int K, double sc,
-                                    const uint8_t *__restrict__ digits,
-                                    const double *__restrict__ inv_fact,
-                                    double *__restrict__ mom) {
-    const int64_t node = node_begin + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    if (node >= node_end) return;
-    const int4 ni = node_i[node];
-    if (ni.z >= 0 && ni.y > kDirectMax) return;  // large internal: H2H pass
-    double c[D];
-#pragma unroll
-    for (int d = 0; d < D; d++) c[d] = node_c[node * D + d];
-    accumulate_warp<D>(0, pw, ni.x, (int64_t)ni.x + ni.y, c, p, K, sc, digits, inv_fact,
-                       mom + node * K, true);
-}
-
-// Internal nodes (> kDirectMax points), all levels bottom-up in ONE
-// cooperative launch (a grid barrier between levels): A = H2H(left) + H2H(right).
-template <int D>
-__global__ void moments_h2h_coop_kernel(const int *__restrict__ level_begin, int levels,
-                                        const int4 *__restrict__ node_i,
-                                        const double *__restrict__ node_c, int p, int K, double sc,
-                                        const uint8_t *__restrict__ digits,
-                                        const double *__restrict__ inv_fact,
-                                        const int *__restrict__ off, const int2 *__restrict__ ab,
-                                        double *__restrict__ mom) {
-    cg::grid_group g = cg::this_grid();
-    extern __shared__ double sh[];  // per warp: 2*K shift values
-    const int lane = threadIdx.x & 31;
-    const int gwarps = gridDim.x * (blockDim.x >> 5);
-    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    double *shift = sh + (threadIdx.x >> 5) * 2 * K;
-    for (int lv = levels - 1; lv >= 0; lv--) {
-        const int b = level_begin[lv], e = level_begin[lv + 1];
-        for (int node = b + gwarp; node < e; node += gwarps) {
-            const int4 ni = node_i[node];
-            if (ni.z < 0 || ni.y <= kDirectMax) continue;
-            for (int c = 0; c < 2; c++) {
-                const int64_t ch = c == 0 ? ni.z : ni.w;
-                double pwt[D][2 * kMaxOrder];
-#pragma unroll
-                for (int d = 0; d < D; d++)
-                    power_ladder((node_c[ch * D + d] - node_c[(int64_t)node * D + d]) / sc, p - 1,
-                                 pwt[d]);
-                for (int k = lane; k < K; k += 32)
-                    shift[c * K + k] = product<D>(digits_of(digits, k), pwt) * inv_fact[k];
-            }
-            __syncwarp();
-            const double *Al = mom + (int64_t)ni.z * K;
-            const double *Ar = mom + (int64_t)ni.w * K;
-            for (int s = lane; s < K; s += 32) {
-                double l = 0.0, r = 0.0;
-                for (int q = off[s]; q < off[s + 1]; q++) {
-                    const int2 pr = ab[q];
-                    l += Al[pr.x] * shift[pr.y];
-                }
-                for (int q = off[s]; q < off[s + 1]; q++) {
-                    const int2 pr = ab[q];
-                    r += Ar[pr.x] * shift[K + pr.y];
-                }
-                mom[(int64_t)node * K + s] = l + r;
-            }
-            __syncwarp();
-        }
-        g.sync();
-    }
-}
 
 __global__ void rescale_factors_kernel(int K, double ratio, const int *__restrict__ degrees,
                                        double *__restrict__ fac) {
@@ -111,55 +32,215 @@ __global__ void moments_rescale_kernel(int64_t total, int K, const double *__res
     dst[i] = src[i] * fac[i % K];
 }
 
+// ---- direct chunked moments ----------------------------------------------
+// Every node's moments straight from its points, A_a = (1/a!) sum_r w_r u_r^a
+// with u = (x_r - c)/(sqrt2 h) (accumulate_far_field, series_expansion.py:76-92,
+// for every node; mathematically identical to the reference's leaf moments +
+// translate_h2h bottom-up, spatial_index.py:171-197).  Work items are
+// (node, chunk of kMomChunk points); a warp sums one item with lanes owning
+// coefficients and per-point power tables staged in shared memory, and a
+// second pass adds each node's chunk partials in chunk order (deterministic).
+// No level-by-level dependency: two launches for the whole tree.
+constexpr int kMomChunk = 256;
+constexpr int kMomWarps = 8;
+constexpr int kMomKPL = kMaxK / 32;  // coefficients per lane
+
+__global__ void mom_items_count_kernel(int64_t nn, const int4 *__restrict__ node_i,
+                                       int *__restrict__ cnt) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v < nn) cnt[v] = (node_i[v].y + kMomChunk - 1) / kMomChunk;
+}
+
+__global__ void mom_items_fill_kernel(int64_t nn, const int4 *__restrict__ node_i,
+                                      const int *__restrict__ off, int2 *__restrict__ items) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= nn) return;
+    const int c = (node_i[v].y + kMomChunk - 1) / kMomChunk;
+    for (int j = 0; j < c; j++) items[off[v] + j] = make_int2((int)v, j);
+}
+
+template <int D>
+__global__ void __launch_bounds__(32 * kMomWarps)
+mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__restrict__ node_i,
+                   const double *__restrict__ node_c, const double *__restrict__ pw, int p,
+                   int K, double sc, const uint8_t *__restrict__ digits,
+                   double *__restrict__ partial) {
+    constexpr int S = packed_stride(D);
+    extern __shared__ double sh[];  // per warp: 32 points x D x p powers (weight folded in d=0)
+    const int lane = threadIdx.x & 31;
+    const int P = p;
+    double *tab = sh + (threadIdx.x >> 5) * 32 * D * kMaxOrder;
+    const int gwarps = gridDim.x * kMomWarps;
+    // per owned coefficient: table offsets d * kMaxOrder + digit_d
+    int toff[kMomKPL][D];
+#pragma unroll
+    for (int j = 0; j < kMomKPL; j++) {
+        const int k = lane + 32 * j;
+        const uint64_t dg = k < K ? digits_of(digits, k) : 0;
+#pragma unroll
+        for (int d = 0; d < D; d++) toff[j][d] = d * kMaxOrder + digit(dg, d);
+    }
+    for (int it = blockIdx.x * kMomWarps + (threadIdx.x >> 5); it < nitems; it += gwarps) {
+        const int2 item = items[it];
+        const int4 ni = node_i[item.x];
+        double c[D];
+#pragma unroll
+        for (int d = 0; d < D; d++) c[d] = node_c[(int64_t)item.x * D + d];
+        const int b = ni.x + item.y * kMomChunk, e = min(b + kMomChunk, ni.x + ni.y);
+        double acc[kMomKPL];
+#pragma unroll
+        for (int j = 0; j < kMomKPL; j++) acc[j] = 0.0;
+        double yn[D], wn = 0.0;  // next batch's point, loaded one batch ahead
+        if (b + lane < e) load_point_w<D>(pw + (int64_t)(b + lane) * S, yn, wn);
+        for (int base = b; base < e; base += 32) {
+            const int i = base + lane;
+            double y[D], w = wn;
+#pragma unroll
+            for (int d = 0; d < D; d++) y[d] = yn[d];
+            if (i + 32 < e) load_point_w<D>(pw + (int64_t)(i + 32) * S, yn, wn);
+            if (i < e) {
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const double u = (y[d] - c[d]) / sc;
+                    double v = d == 0 ? w : 1.0;
+                    double *row = tab + (lane * D + d) * kMaxOrder;
+                    for (int k = 0; k < P; k++) {
+                        row[k] = v;
+                        v *= u;
+                    }
+                }
+            }
+            __syncwarp();
+            const int nv = min(32, e - base);
+            int q = 0;
+            // two points per round: independent product chains
+            for (; q + 1 < nv; q += 2) {
+                const double *t0 = tab + q * D * kMaxOrder, *t1 = t0 + D * kMaxOrder;
+#pragma unroll
+                for (int j = 0; j < kMomKPL; j++) {
+                    if (32 * j < K) {
+                        double v0 = t0[toff[j][0]], v1 = t1[toff[j][0]];
+#pragma unroll
+                        for (int d = 1; d < D; d++) {
+                            v0 *= t0[toff[j][d]];
+                            v1 *= t1[toff[j][d]];
+                        }
+                        acc[j] += v0 + v1;
+                    }
+                }
+            }
+            if (q < nv) {
+                const double *t0 = tab + q * D * kMaxOrder;
+#pragma unroll
+                for (int j = 0; j < kMomKPL; j++) {
+                    if (32 * j < K) {
+                        double v0 = t0[toff[j][0]];
+#pragma unroll
+                        for (int d = 1; d < D; d++) v0 *= t0[toff[j][d]];
+                        acc[j] += v0;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < kMomKPL; j++) {
+            const int k = lane + 32 * j;
+            if (k < K) partial[(int64_t)it * K + k] = acc[j];
+        }
+    }
+}
+
+// One CTA (8 warps) per node: warp w sums items w, w+8, ... of the node, then
+// the 8 warp sums are added in warp order (deterministic).
+__global__ void __launch_bounds__(256)
+mom_combine_kernel(const int *__restrict__ off, const double *__restrict__ partial, int K,
+                   const double *__restrict__ inv_fact, double *__restrict__ mom) {
+    __shared__ double sh[8][kMaxK];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t v = blockIdx.x;
+    const int i0 = off[v], i1 = off[v + 1];
+    if (i1 - i0 == 1) {  // single chunk: copy
+        for (int k = threadIdx.x; k < K; k += 256)
+            mom[v * K + k] = partial[(int64_t)i0 * K + k] * inv_fact[k];
+        return;
+    }
+    for (int k = lane; k < K; k += 32) {
+        double s = 0.0;
+#pragma unroll 4
+        for (int it = i0 + wid; it < i1; it += 8) s += partial[(int64_t)it * K + k];
+        sh[wid][k] = s;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < K; k += 256) {
+        double s = sh[0][k];
+#pragma unroll
+        for (int w = 1; w < 8; w++) s += sh[w][k];
+        mom[v * K + k] = s * inv_fact[k];
+    }
+}
+
+// items of a tree (bandwidth-independent, built once per tree)
+static int mom_items(TreeDev &t) {
+    if (t.mom_items_valid) return FG_OK;
+    const int64_t nn = t.nnodes;
+    FG_TRY(t.mom_off.reserve(sizeof(int) * (nn + 1)));
+    int *off = t.mom_off.as<int>();
+    FG_CUDA_TRY(cudaMemsetAsync(off + nn, 0, sizeof(int), stream()));
+    const unsigned blocks = (unsigned)((nn + 255) / 256);
+    count_launch();
+    mom_items_count_kernel<<<blocks, 256, 0, stream()>>>(nn, t.node_i.as<int4>(), off);
+    size_t tmp = 0;
+    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, off, off, (int)(nn + 1), stream()));
+    static DBuf s_tmp;
+    FG_TRY(s_tmp.reserve(tmp + 16));
+    count_launch();
+    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(s_tmp.p, tmp, off, off, (int)(nn + 1), stream()));
+    int total = 0;
+    FG_CUDA_TRY(cudaMemcpyAsync(&total, off + nn, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    FG_TRY(t.mom_items.reserve(sizeof(int2) * std::max(total, 1)));
+    count_launch();
+    mom_items_fill_kernel<<<blocks, 256, 0, stream()>>>(nn, t.node_i.as<int4>(), off,
+                                                        t.mom_items.as<int2>());
+    FG_CUDA_TRY(cudaGetLastError());
+    t.mom_nitems = total;
+    t.mom_items_valid = true;
+    return FG_OK;
+}
+
 template <int D>
 static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst) {
     const int K = T.K, p = T.order;
     const double sc = kSqrt2 * h;
-    const int warps_per_block = 8;
+    FG_TRY(mom_items(t));
+    static DBuf s_partial;
+    FG_TRY(s_partial.reserve(sizeof(double) * (size_t)t.mom_nitems * K));
+    const size_t smem = sizeof(double) * 32 * D * kMaxOrder * kMomWarps;
+    auto kern = mom_partial_kernel<D>;
+    static int c_grid[kMaxDim + 1] = {0};
+    if (!c_grid[D]) {
+        int dev = 0, sms = 0, occ = 0;
+        FG_CUDA_TRY(cudaGetDevice(&dev));
+        FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (smem > 48 * 1024)
+            FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+        FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kMomWarps, smem));
+        c_grid[D] = sms * std::max(occ, 1);
+    }
+    const int grid = std::max(1, std::min(c_grid[D], (t.mom_nitems + kMomWarps - 1) / kMomWarps));
+    count_launch();
+    kern<<<grid, 32 * kMomWarps, smem, stream()>>>(t.mom_nitems, t.mom_items.as<int2>(),
+                                                  t.node_i.as<int4>(), t.node_c.as<double>(),
+                                                  t.pw.as<double>(), p, K, sc,
+                                                  T.digits.as<uint8_t>(), s_partial.as<double>());
+    FG_CUDA_TRY(cudaGetLastError());
     const int64_t nn = t.nnodes;
-    {
-        const unsigned blocks = (unsigned)((nn + warps_per_block - 1) / warps_per_block);
-        count_launch();
-        moments_leaf_kernel<D><<<blocks, 32 * warps_per_block, 0, stream()>>>(
-            0, nn, t.node_i.as<int4>(), t.node_c.as<double>(), t.pw.as<double>(), p, K, sc,
-            T.digits.as<uint8_t>(), T.inv_fact.as<double>(), dst.as<double>());
-        FG_CUDA_TRY(cudaGetLastError());
-    }
-    {
-        // one cooperative launch for the large internal nodes of every level
-        auto kern = moments_h2h_coop_kernel<D>;
-        const int threads = 32 * warps_per_block;
-        const size_t smem = sizeof(double) * 2 * K * warps_per_block;
-        static int c_grid[9] = {0};
-        static size_t c_smem[9] = {0};
-        if (c_grid[D] == 0 || c_smem[D] != smem) {
-            int dev = 0, sms = 0, occ = 0;
-            FG_CUDA_TRY(cudaGetDevice(&dev));
-            FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            if (smem > 48 * 1024)
-                FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem));
-            FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-            c_grid[D] = sms * std::max(1, std::min(occ, 2));
-            c_smem[D] = smem;
-        }
-        const int *lb = t.level_begin_dev.as<int>();
-        int levels = t.levels;
-        int p_ = p, K_ = K;
-        double sc_ = sc;
-        const int4 *ni = t.node_i.as<int4>();
-        const double *nc = t.node_c.as<double>();
-        const uint8_t *dg = T.digits.as<uint8_t>();
-        const double *ifa = T.inv_fact.as<double>();
-        const int *off = T.h2h_off.as<int>();
-        const int2 *ab = T.h2h_ab.as<int2>();
-        double *mom = dst.as<double>();
-        void *args[] = {(void *)&lb, &levels, (void *)&ni, (void *)&nc, &p_, &K_, &sc_,
-                        (void *)&dg, (void *)&ifa, (void *)&off, (void *)&ab, (void *)&mom};
-        count_launch();
-        FG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)kern, c_grid[D], threads, args, smem,
-                                                stream()));
-    }
+    count_launch();
+    mom_combine_kernel<<<(unsigned)nn, 256, 0, stream()>>>(
+        t.mom_off.as<int>(), s_partial.as<double>(), K, T.inv_fact.as<double>(), dst.as<double>());
+    FG_CUDA_TRY(cudaGetLastError());
     return FG_OK;
 }
 

@@ -339,6 +339,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     t.qb_valid = false;
     t.fp32_ok = !(bad & 4);
     t.pf_valid = false;
+    t.mom_items_valid = false;
     switch (dim) {
         case 1: return build_levels<1>(n, leaf, B, t);
         case 2: return build_levels<2>(n, leaf, B, t);

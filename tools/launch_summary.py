@@ -20,7 +20,7 @@ for k, v in data:
     n = n.split("<")[0] if "cub::" in n else n
     tot[n][0] += 1
     tot[n][1] += v
-print(f"launches {len(data)}, summed kernel time {sum(v for _, v in data):.3f} ms")
+print(f"launches {len(data)}, summed kernel time {sum(v for _, v in data) / 1e3:.3f} ms")
 for n, (c, v) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
-    per = f"  per step {v / steps:8.3f} ms" if steps else ""
-    print(f"{n[:64]:64s} n={c:5d} ms={v:9.3f}{per}")
+    per = f"  per step {v / steps:8.1f} us" if steps else ""
+    print(f"{n[:64]:64s} n={c:5d} us={v:10.1f}{per}")
