@@ -14,7 +14,7 @@ import math
 import numpy as np
 
 from .spatial_index import KdTree, PointStore, build_tree
-from .summation_engine import RunConfig, dfd_run, dfdo_run, dito_run
+from .summation_engine import RunConfig, sweep_run
 
 
 def max_rel_error(estimates, exact) -> float:
@@ -29,37 +29,34 @@ def max_rel_error(estimates, exact) -> float:
     return float(err.max()) if err.size else 0.0
 
 
-_RUNS = {"dfd": dfd_run, "dfdo": dfdo_run, "dito": dito_run}
-
-
-def lscv_score(tree: KdTree, h: float, epsilon: float = 1e-3, algorithm: str = "dfd") -> float:
-    """LSCV score of a Gaussian KDE with unit weights (cli_harness.py:128-137):
+def lscv_scores(tree: KdTree, hs, epsilon: float = 1e-3, algorithm: str = "dfd") -> list:
+    """LSCV scores of a Gaussian KDE with unit weights (cli_harness.py:128-137):
 
         (2 pi 2h^2)^(-D/2) sum G_{sqrt2 h} / n^2
           - 2 (2 pi h^2)^(-D/2) (sum G_h - n) / (n (n-1))
 
-    from two monochromatic device runs (the self term is removed by `- n`).
+    for every h in ``hs``; all 2 len(hs) monochromatic sums run as one device
+    sweep (the self term is removed by `- n`).
     """
     n, dim = tree.n, tree.dim
-    run = _RUNS[algorithm]
-    vals = []
-    for hh in (math.sqrt(2.0) * h, h):
-        if algorithm == "dito":
-            tree.refresh_moments(hh, _default_plimit(dim))
-        vals.append(run(RunConfig(bandwidth=hh, epsilon=epsilon, algorithm=algorithm),
-                        tree, tree).values)
-    conv, near = vals
-    norm_conv = (2.0 * math.pi * 2.0 * h * h) ** (-0.5 * dim)
-    norm_near = (2.0 * math.pi * h * h) ** (-0.5 * dim)
-    integral_sq = norm_conv * float(conv.sum()) / (n * n)
-    leave_one_out = norm_near * 2.0 * float(near.sum() - n) / (n * (n - 1))
-    return integral_sq - leave_one_out
+    hs = [float(h) for h in hs]
+    bws = [b for h in hs for b in (math.sqrt(2.0) * h, h)]
+    res = sweep_run(RunConfig(bandwidth=bws[0], epsilon=epsilon, algorithm=algorithm), tree,
+                    tree, bws)
+    out = []
+    for i, h in enumerate(hs):
+        conv, near = res[2 * i].values, res[2 * i + 1].values
+        norm_conv = (2.0 * math.pi * 2.0 * h * h) ** (-0.5 * dim)
+        norm_near = (2.0 * math.pi * h * h) ** (-0.5 * dim)
+        integral_sq = norm_conv * float(conv.sum()) / (n * n)
+        leave_one_out = norm_near * 2.0 * float(near.sum() - n) / (n * (n - 1))
+        out.append(integral_sq - leave_one_out)
+    return out
 
 
-def _default_plimit(dim):
-    from .spatial_index import default_plimit
-
-    return default_plimit(dim)
+def lscv_score(tree: KdTree, h: float, epsilon: float = 1e-3, algorithm: str = "dfd") -> float:
+    """LSCV score at one bandwidth (see :func:`lscv_scores`)."""
+    return lscv_scores(tree, [h], epsilon, algorithm)[0]
 
 
 def select_bandwidth(points, seed: int = 0, epsilon: float = 1e-3, max_points: int = 2000,
@@ -85,14 +82,14 @@ def select_bandwidth(points, seed: int = 0, epsilon: float = 1e-3, max_points: i
         return lscv_score(tree, h, epsilon, algorithm)
 
     grid = np.geomspace(1e-3 * scale, 0.5 * scale, 14)
-    scores = [score(h) for h in grid]
+    scores = lscv_scores(tree, grid, epsilon, algorithm)  # the whole grid in one sweep
     best = int(np.argmin(scores))
     a = math.log(grid[max(best - 1, 0)])
     b = math.log(grid[min(best + 1, len(grid) - 1)])
     invphi = 0.5 * (math.sqrt(5.0) - 1.0)
     c = b - invphi * (b - a)
     d = a + invphi * (b - a)
-    fc, fd = score(math.exp(c)), score(math.exp(d))
+    fc, fd = lscv_scores(tree, [math.exp(c), math.exp(d)], epsilon, algorithm)
     while b - a > 0.02:
         if fc < fd:
             b, d, fd = d, c, fc

@@ -241,9 +241,74 @@ def make_lscv():
     np.savez_compressed(os.path.join(HERE, "lscv.npz"), **rec)
 
 
+def make_cli():
+    """Report formats, CSV ingestion and the dataset generators of the reference's
+    cli_harness.py / datasets.py, rendered by the reference itself."""
+    import json
+    import tempfile
+
+    from fastgauss import cli_harness as ch
+    from fastgauss import datasets as ds
+
+    rec = {"reports": [], "loads": [], "datasets": {}}
+    rows = [("naive", 0.5, 0.05, 0.12345, 0.0, {}),
+            ("dfd", 0.5, 0.05, 0.0123456, 0.00123, {"pair_visits": 10, "base_cases": 3,
+                                                    "fd_prunes": 4, "hermite_prunes": 0,
+                                                    "local_prunes": 0, "h2l_prunes": 0}),
+            ("naive", 1.0, 0.1, 0.2, 0.0, {}),
+            ("dfd", 1.0, 0.1, 1.5e-4, 2.5e-7, {"pair_visits": 7, "base_cases": 1,
+                                               "fd_prunes": 5, "hermite_prunes": 2,
+                                               "local_prunes": 1, "h2l_prunes": 0})]
+    for verified in (True, False):
+        rrows = [ch.SweepRow(a, m, h, s, (e if verified else None), c) for a, m, h, s, e, c in rows]
+        totals = {"naive": 0.32345, "dfd": 0.0124956}
+        rep = ch.SweepReport(0.1, 0.01, "ref.csv", None, (0.5, 1.0), ("naive", "dfd"), rrows,
+                             totals, verified)
+        rec["reports"].append({
+            "verified": verified,
+            "rows": [[a, m, h, s, (e if verified else None), c] for a, m, h, s, e, c in rows],
+            "totals": totals,
+            "table": ch._format_table(rep), "csv": ch._format_csv(rep),
+            "json": json.dumps(ch.report_to_dict(rep), indent=2) + "\n"})
+    cases = {
+        "plain": ("0.1,0.2\n0.3,0.4\n\n0.5,0.6\n", {}),
+        "header": ("x,y\n1,2\n3,4\n", {"header": True}),
+        "weights": ("0,0,2\n1,1,0.5\n", {"has_weights": True}),
+        "rescale": ("1,5,2\n3,5,4\n2,5,8\n", {"rescale": True}),
+        "ragged": ("1,2\n3\n", {}),
+        "nonnumeric": ("1,2\n3,abc\n", {}),
+        "empty": ("\n\n", {}),
+        "bad_weights": ("0,0,-1\n1,1,1\n", {"has_weights": True}),
+        "weights_one_col": ("1\n2\n", {"has_weights": True}),
+    }
+    with tempfile.TemporaryDirectory() as td:
+        for name, (text, kw) in cases.items():
+            path = os.path.join(td, "data.csv")
+            with open(path, "w") as fh:
+                fh.write(text)
+            entry = {"name": name, "text": text, "kw": kw}
+            try:
+                st = ch.load_points(path, **kw)
+                entry["points"] = st.points.tolist()
+                entry["weights"] = st.weights.tolist()
+            except ch.LoadError as exc:
+                entry["error"] = str(exc).replace(path, "<path>")
+            rec["loads"].append(entry)
+    rec["datasets"] = {
+        "uniform": ds.uniform_points(5, 3, 7).tolist(),
+        "clustered": ds.clustered_points(6, 2, 3).tolist(),
+        "hierarchical": ds.hierarchical_clusters(6, 2, 4).tolist(),
+        "duplicated": ds.duplicated_points(10, 2, 5).tolist(),
+    }
+    with open(os.path.join(HERE, "cli.json"), "w") as fh:
+        json.dump(rec, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["trees", "moments", "series", "bounds", "runs", "subsamples",
-                             "c1", "lscv"]
+                             "c1", "lscv", "cli"]
+    if "cli" in which:
+        make_cli()
     if "trees" in which:
         print("trees", make_trees())
     if "moments" in which:
