@@ -55,6 +55,17 @@ typedef struct {
 
 typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_index.py:144) */
 
+/* one audit-ledger event (ResultVector.audit, summation_engine.py:107-119;
+ * recorded at :250, :350, :394-398): kind 0 base case, 1 FD prune, 2 Hermite,
+ * 3 direct local, 4 H2L; the query block (see fg_query_block_ranges), the
+ * traversal step and item lane (ordering within the block); W_R, the error
+ * bound charged through the token rule, G_min at the decision, token flow
+ * (required tokens: negative = credit). */
+typedef struct {
+    int32_t kind, qblock, seq, lane;
+    double w_ref, bound, mass_lo, token_flow;
+} fg_audit_event;
+
 int fg_version(void);
 const char *fg_last_error(void);
 /* diagnostics: number of kernels this library has launched so far, and
@@ -124,6 +135,14 @@ int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32
  * query block is 32 consecutive tree-order points; fg_query_blocks reports
  * the block count. */
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks);
+/* tree-order start and point count of every query block (host arrays) */
+int fg_query_block_ranges(fg_tree *qtree, int32_t *starts, int32_t *counts);
+/* fg_run with the audit ledger (the reference's audit=True): up to capacity
+ * events copied to `events` (host), *nevents = events recorded (re-run with a
+ * larger capacity when it exceeds capacity; pair_visits always suffices). */
+int fg_run_audit(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+                 int32_t plimit, double *values, fg_counters *counters, double *seconds,
+                 fg_audit_event *events, int64_t capacity, int64_t *nevents);
 int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
                  int32_t plimit, int64_t block_begin, int64_t block_end, int64_t block_stride,
                  double *values, fg_counters *counters, double *seconds);

@@ -51,6 +51,8 @@ SIGNATURES = {
     "fg_moments_export": [_P, _P, _P, _P, _P],
     "fg_run": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P],
     "fg_query_blocks": [_P, _P],
+    "fg_query_block_ranges": [_P, _P, _P],
+    "fg_run_audit": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P, _P, _I64, _P],
     "fg_run_range": [_P, _P, _F64, _F64, _I32, _I32, _I64, _I64, _I64, _P, _P, _P],
     "fg_run_sweep": [_P, _P, _P, _I32, _F64, _I32, _I32, _P, _P, _P],
     "fg_launch_count": [_P],

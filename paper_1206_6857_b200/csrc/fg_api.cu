@@ -542,6 +542,53 @@ int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32
     return FG_OK;
 }
 
+int fg_query_block_ranges(fg_tree *qtree, int32_t *starts, int32_t *counts) {
+    FG_REQUIRE(qtree && starts && counts, FG_EINVAL, "null argument");
+    FG_TRY(query_blocks(qtree->t));
+    const int64_t nb = qtree->t.nqb;
+    std::vector<int2> rg(nb);
+    FG_CUDA_TRY(cudaMemcpyAsync(rg.data(), qtree->t.qb_range.p, sizeof(int2) * nb,
+                                cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    for (int64_t i = 0; i < nb; i++) {
+        starts[i] = rg[i].x;
+        counts[i] = rg[i].y;
+    }
+    return FG_OK;
+}
+
+int fg_run_audit(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
+                 int32_t plimit, double *values, fg_counters *counters, double *seconds,
+                 fg_audit_event *events, int64_t capacity, int64_t *nevents) {
+    FG_REQUIRE(qtree && rtree && values && nevents, FG_EINVAL, "null argument");
+    FG_REQUIRE(capacity >= 0 && (capacity == 0 || events), FG_EINVAL, "bad event buffer");
+    static DBuf s_ev, s_cnt, s_out;
+    FG_TRY(s_ev.reserve(sizeof(fg_audit_event) * std::max<int64_t>(capacity, 1)));
+    FG_TRY(s_cnt.reserve(sizeof(unsigned long long)));
+    const AuditSink sink{s_ev.p, s_cnt.as<unsigned long long>(), (long long)capacity};
+    const int64_t m = qtree->t.n;
+    const bool out_dev = is_device_ptr(values);
+    double *dout = values;
+    if (!out_dev) {
+        FG_TRY(s_out.reserve(sizeof(double) * m));
+        dout = s_out.as<double>();
+    }
+    FG_TRY(run_traversal(qtree->t, rtree->t, h, eps, mode, plimit, 0, -1, 1, dout, counters,
+                         seconds, &sink));
+    unsigned long long n = 0;
+    FG_CUDA_TRY(cudaMemcpyAsync(&n, s_cnt.p, sizeof(n), cudaMemcpyDeviceToHost, stream()));
+    if (!out_dev)
+        FG_CUDA_TRY(cudaMemcpyAsync(values, dout, sizeof(double) * m, cudaMemcpyDeviceToHost,
+                                    stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    const int64_t keep = std::min<int64_t>((int64_t)n, capacity);
+    if (keep > 0)
+        FG_CUDA_TRY(cudaMemcpy(events, s_ev.p, sizeof(fg_audit_event) * keep,
+                               cudaMemcpyDeviceToHost));
+    *nevents = (int64_t)n;
+    return FG_OK;
+}
+
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks) {
     FG_REQUIRE(qtree && nblocks, FG_EINVAL, "null argument");
     FG_TRY(query_blocks(qtree->t));

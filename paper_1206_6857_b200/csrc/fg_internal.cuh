@@ -184,9 +184,15 @@ int moments_refresh(TreeDev &t, double h, int plimit);
 int moments_multi(TreeDev &t, const double *hs, int nh, int plimit, DBuf &dst);
 int moments_export(const TreeDev &t, double *out);
 int query_blocks(TreeDev &t);
+// optional audit ledger of a single run (device buffers)
+struct AuditSink {
+    void *events;                 // AuditEvent[cap] (fg_audit_event layout)
+    unsigned long long *count;    // events recorded (may exceed cap)
+    long long cap;
+};
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
                   int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
-                  double *seconds);
+                  double *seconds, const AuditSink *audit = nullptr);
 // all bandwidths of a sweep through shared launches (values: nh x m, device)
 int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int mode, int plimit,
               double *d_values, fg_counters *counters, double *seconds);

@@ -241,11 +241,11 @@ struct TravScratch {
 };
 static TravScratch g_scr;
 
-template <int D>
+template <int D, bool AUDIT>
 static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     // 4 resident CTAs of 128 threads per SM (<= 128 registers): measured best;
     // capping registers lower spills and runs slower
-    auto kern = traverse_kernel<D, FG_TRAV_MINB>;
+    auto kern = traverse_kernel<D, FG_TRAV_MINB, AUDIT>;
     // resident-grid size, cached per (kernel, shared memory size)
     static thread_local const void *c_kern = nullptr;
     static thread_local size_t c_smem = 0;
@@ -288,18 +288,23 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     return FG_OK;
 }
 
-static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
+template <bool AUDIT>
+static int launch_dispatch_t(int D, TravArgs &A, size_t smem, int64_t nb) {
     switch (D) {
-        case 1: return launch_traverse<1>(A, smem, nb);
-        case 2: return launch_traverse<2>(A, smem, nb);
-        case 3: return launch_traverse<3>(A, smem, nb);
-        case 4: return launch_traverse<4>(A, smem, nb);
-        case 5: return launch_traverse<5>(A, smem, nb);
-        case 6: return launch_traverse<6>(A, smem, nb);
-        case 7: return launch_traverse<7>(A, smem, nb);
-        case 8: return launch_traverse<8>(A, smem, nb);
+        case 1: return launch_traverse<1, AUDIT>(A, smem, nb);
+        case 2: return launch_traverse<2, AUDIT>(A, smem, nb);
+        case 3: return launch_traverse<3, AUDIT>(A, smem, nb);
+        case 4: return launch_traverse<4, AUDIT>(A, smem, nb);
+        case 5: return launch_traverse<5, AUDIT>(A, smem, nb);
+        case 6: return launch_traverse<6, AUDIT>(A, smem, nb);
+        case 7: return launch_traverse<7, AUDIT>(A, smem, nb);
+        case 8: return launch_traverse<8, AUDIT>(A, smem, nb);
         default: return FG_EUNSUPPORTED;
     }
+}
+
+static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
+    return A.audit ? launch_dispatch_t<true>(D, A, smem, nb) : launch_dispatch_t<false>(D, A, smem, nb);
 }
 
 // Queue one traversal launch over nh bandwidths (tasks = (bandwidth, query
@@ -310,7 +315,7 @@ static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
 static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
                            const double *const *moms, double eps, int mode, int plimit,
                            int64_t b0, int64_t b1, int64_t stride, double *const *outs,
-                           unsigned long long *dcnt, bool lpt) {
+                           unsigned long long *dcnt, bool lpt, const AuditSink *audit = nullptr) {
     FG_REQUIRE(nh >= 1 && nh <= kMaxSweep, FG_EINVAL, "bad bandwidth count");
     FG_REQUIRE(eps >= 0.0, FG_EINVAL, "epsilon must be non-negative");
     FG_REQUIRE(mode >= FG_DFD && mode <= FG_DITO, FG_EINVAL, "unknown algorithm");
@@ -409,6 +414,13 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         H.out = outs[j];
         H.counters = dcnt + (size_t)kCounters * j;
     }
+    if (audit) {
+        FG_REQUIRE(nh == 1, FG_EINVAL, "the audit ledger records single runs");
+        A.audit = reinterpret_cast<AuditEvent *>(audit->events);
+        A.audit_count = audit->count;
+        A.audit_cap = audit->cap;
+        FG_CUDA_TRY(cudaMemsetAsync(audit->count, 0, sizeof(unsigned long long), stream()));
+    }
     if (getenv("FG_DEBUG_BLOCKS") && nh == 1) {
         FG_TRY(g_scr.dbg.reserve(sizeof(unsigned long long) * 4 * q.nqb));
         FG_CUDA_TRY(cudaMemsetAsync(g_scr.dbg.p, 0, sizeof(unsigned long long) * 4 * q.nqb, stream()));
@@ -464,7 +476,7 @@ static void fill_counters(const unsigned long long *c, fg_counters *o) {
 
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
                   int64_t b0, int64_t b1, int64_t stride, double *d_values, fg_counters *counters,
-                  double *seconds) {
+                  double *seconds, const AuditSink *audit) {
     FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
     const int D = q.dim;
     if (plimit <= 0) plimit = default_plimit(D);
@@ -486,7 +498,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     const double *mom = r.mom.as<double>();
     FG_CUDA_TRY(cudaEventRecord(e0, stream()));
     FG_TRY(queue_traversal(q, r, 1, &h, &mom, eps, mode, plimit, b0, b1, stride, &d_values,
-                           g_scr.counters.as<unsigned long long>(), true));
+                           g_scr.counters.as<unsigned long long>(), !audit, audit));
     FG_CUDA_TRY(cudaEventRecord(e1, stream()));
     FG_CUDA_TRY(cudaMemcpyAsync(cnt, g_scr.counters.p, sizeof(unsigned long long) * kCounters,
                                 cudaMemcpyDeviceToHost, stream()));

@@ -34,6 +34,15 @@ struct TravH {
     int pad;
 };
 
+// One audit-ledger event (summation_engine.py:250, 350, 394-398): kind 0 base
+// case, 1 FD prune, 2 Hermite, 3 direct local, 4 H2L; the query block, the
+// step of its traversal and the lane (item) for ordering; W_R, the error
+// bound charged through the token rule, G_min at the decision, token flow.
+struct AuditEvent {
+    int kind, qblock, seq, lane;
+    double w_ref, bound, mass_lo, flow;
+};
+
 struct TravArgs {
     // reference tree (BFS numbering)
     const double *r_pw;
@@ -71,9 +80,38 @@ struct TravArgs {
     unsigned long long *cost;      // per-block cycles of this run (or null)
     const float *r_pf;             // FP32 records about each point's anchor (fp32_pack)
     const int *r_anchor;           // per point: its anchor node
+    AuditEvent *audit;             // ledger (AUDIT kernels only)
+    unsigned long long *audit_count;
+    long long audit_cap;
     int nh;                        // bandwidths in this launch
     TravH hp[kMaxSweep];
 };
+
+// Append the events of the lanes in `mask` (each lane passes its own fields).
+__device__ __forceinline__ void audit_append(const TravArgs &A, unsigned mask, int kind, int qb,
+                                             int seq, double wr, double bound, double mass_lo,
+                                             double flow) {
+    const int lane = threadIdx.x & 31;
+    if (!mask) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(A.audit_count, (unsigned long long)__popc(mask));
+    base = __shfl_sync(kFull, base, 0);
+    if ((mask >> lane) & 1u) {
+        const unsigned long long i = base + __popc(mask & ((1u << lane) - 1u));
+        if ((long long)i < A.audit_cap) {
+            AuditEvent e;
+            e.kind = kind;
+            e.qblock = qb;
+            e.seq = seq;
+            e.lane = lane;
+            e.w_ref = wr;
+            e.bound = bound;
+            e.mass_lo = mass_lo;
+            e.flow = flow;
+            A.audit[i] = e;
+        }
+    }
+}
 
 // Admit candidates in lane order under the token rule.  Unconditional
 // candidates (req <= 0) bank their surplus first; the rest are taken greedily
@@ -383,7 +421,7 @@ __device__ __forceinline__ int warp_excl_scan(int v) {
     return s - v;
 }
 
-template <int D, int MINB>
+template <int D, int MINB, bool AUDIT>
 __global__ void __launch_bounds__(kTravThreads, MINB)
 traverse_kernel(const TravArgs A) {
     constexpr int S = packed_stride(D);
@@ -516,6 +554,8 @@ traverse_kernel(const TravArgs A) {
             else fd_mask = __ballot_sync(kFull, act && req <= 0.0);
             const bool fd = (fd_mask >> lane) & 1u;
             c_fd += __popc(fd_mask);
+            if constexpr (AUDIT)
+                audit_append(A, fd_mask, 1, (int)b, (int)steps, WR, fd_err, gmin, req);
             double settled = 0.0, est_add = 0.0;
             if (fd) {
                 const double dl = WR * klo, du = WR * khi - WR;
@@ -552,6 +592,8 @@ traverse_kernel(const TravArgs A) {
                 const double sreq = cand ? required_tokens(WR, bound, tok_scale)
                                          : CUDART_INF;
                 ser_mask = admit(cand, sreq, tokens);
+                if constexpr (AUDIT)
+                    audit_append(A, ser_mask, meth, (int)b, (int)steps, WR, bound, gmin, sreq);
                 const unsigned hm = __ballot_sync(kFull, ((ser_mask >> lane) & 1u) && meth == 2);
                 const unsigned om = ser_mask & ~hm;
                 if ((ser_mask >> lane) & 1u) {
@@ -617,6 +659,12 @@ traverse_kernel(const TravArgs A) {
                     use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
+            }
+            if constexpr (AUDIT) {
+                // FP32 items charge their absolute error part to the tokens
+                audit_append(A, f32_mask, 0, (int)b, (int)steps, WR, abs32, gmin,
+                             abs32 * tok_scale - WR);
+                audit_append(A, base_mask & ~f32_mask, 0, (int)b, (int)steps, WR, 0.0, gmin, -WR);
             }
             if (f32_mask) {
                 constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>(), F = fstride<D>();

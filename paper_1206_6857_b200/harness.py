@@ -100,3 +100,34 @@ def select_bandwidth(points, seed: int = 0, epsilon: float = 1e-3, max_points: i
             d = a + invphi * (b - a)
             fd = score(math.exp(d))
     return math.exp(0.5 * (a + b))
+
+
+def telescoping_audit(ledger, qtree: KdTree, exact, epsilon: float) -> dict:
+    """Theorem-2 telescoping check over an audit ledger and the
+    accounting invariant, per query node of the ledger:
+
+    * worst_ratio = max over query blocks of  sum(bound) / (eps * min_q G(q)),
+      G the exact sums (original order); <= 1 is the guarantee.  Every bound
+      is an absolute error bound for every query of its block;
+    * weight_error = max relative deviation of sum(W_R) from n_blocks * W:
+      every reference's weight is settled exactly once per query block.
+    """
+    from .summation_engine import query_block_nodes
+
+    e = qtree.arrays()
+    exact_tree = np.asarray(exact, dtype=float)[e["perm"]]
+    blocks_per_node = np.bincount(query_block_nodes(qtree), minlength=len(e["start"]))
+    bound = {}
+    wsum = {}
+    for kind, v, w_ref, bd, _, _ in ledger:
+        bound[v] = bound.get(v, 0.0) + bd
+        wsum[v] = wsum.get(v, 0.0) + w_ref
+    total_w = float(e["weight"][0])
+    worst, werr = 0.0, 0.0
+    for v, b in bound.items():
+        g = float(exact_tree[e["start"][v]:e["end"][v]].min())
+        k = int(blocks_per_node[v])
+        if b > 0.0:
+            worst = max(worst, b / (k * epsilon * g) if g > 0.0 else float("inf"))
+        werr = max(werr, abs(wsum[v] - k * total_w) / (k * total_w))
+    return {"worst_ratio": worst, "weight_error": werr, "query_nodes": len(bound)}

@@ -117,18 +117,75 @@ def naive_sum(queries, references, weights, h, out=None) -> ResultVector:
     return ResultVector(vals, time.perf_counter() - t0, counters)
 
 
+# fg_audit_event (include/fastgauss_b200.h)
+AUDIT_DTYPE = np.dtype([("kind", np.int32), ("qblock", np.int32), ("seq", np.int32),
+                        ("lane", np.int32), ("w_ref", np.float64), ("bound", np.float64),
+                        ("mass_lo", np.float64), ("token_flow", np.float64)])
+AUDIT_KINDS = ("base", "fd", "hermite", "local", "h2l")
+
+
+def query_block_nodes(qtree: KdTree) -> np.ndarray:
+    """Preorder node index (Node.index) of every query block: the maximal node
+    with <= 32 points it is (or, for a larger leaf cut into runs, lies in)."""
+    nb = query_block_count(qtree)
+    starts = np.empty(nb, np.int32)
+    counts = np.empty(nb, np.int32)
+    _lib.call("fg_query_block_ranges", qtree.handle, _lib.ptr(starts), _lib.ptr(counts))
+    e = qtree.arrays()
+    # the deepest node containing each block's range (node ranges nest)
+    depth_order = np.argsort(e["end"] - e["start"], kind="stable")
+    out = np.full(nb, -1, np.int64)
+    for v in depth_order[::-1]:  # largest first; later (smaller) nodes overwrite
+        lo = np.searchsorted(starts, e["start"][v], side="left")
+        hi = np.searchsorted(starts, e["end"][v], side="left")
+        sel = np.arange(lo, hi)
+        sel = sel[starts[sel] + counts[sel] <= e["end"][v]]
+        out[sel] = v
+    return out
+
+
+def _audit_run(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: str, plimit: int,
+               vals) -> tuple:
+    """One run with the device ledger (fg_run_audit); returns the ledger in the
+    reference's tuple form (kind, query node index, W_R, bound, mass_lo at the
+    decision, token flow), ordered by query node, step and item."""
+    cnt = _lib.fg_counters()
+    secs = ctypes.c_double()
+    cap = 1 << 16
+    while True:
+        ev = np.empty(cap, AUDIT_DTYPE)
+        n = ctypes.c_int64()
+        _lib.call("fg_run_audit", qtree.handle, rtree.handle, float(config.bandwidth),
+                  float(config.epsilon), _lib.MODES[mode], int(plimit), _lib.ptr(vals),
+                  ctypes.byref(cnt), ctypes.byref(secs), ev.ctypes.data, cap, ctypes.byref(n))
+        if n.value <= cap:
+            break
+        cap = n.value
+    ev = ev[:n.value]
+    ev = ev[np.lexsort((ev["lane"], ev["seq"], ev["qblock"]))]
+    nodes = query_block_nodes(qtree)
+    ledger = [(AUDIT_KINDS[k], int(nodes[b]), float(w), float(bd), float(ml), float(fl))
+              for k, b, w, bd, ml, fl in zip(ev["kind"], ev["qblock"], ev["w_ref"],
+                                               ev["bound"], ev["mass_lo"], ev["token_flow"])]
+    return cnt, secs.value, ledger, ev
+
+
 def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: str,
                         audit: bool, out=None, block_range=None) -> ResultVector:
     """summation_engine.py:431-455 on the device."""
-    if audit:
-        raise NotImplementedError(
-            "the device engine does not record an audit ledger (SURVEY 8(f) item 3)")
+    if audit and block_range is not None:
+        raise ValueError("the audit ledger records full runs")
     plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
     if mode == "dito" and (rtree.moments_bandwidth != config.bandwidth or
                            rtree.moments_order is None or rtree.moments_order < plimit):
         raise RuntimeError("reference moments missing or stale; call refresh_moments "
                            "for this bandwidth first")
     vals = out if out is not None else np.empty(qtree.n)
+    if audit:
+        cnt, secs, ledger, _ = _audit_run(config, qtree, rtree, mode, plimit, vals)
+        if out is None:
+            qtree._set_run_values(vals)
+        return ResultVector(vals, secs, TraversalCounters._from_c(cnt), ledger)
     cnt = _lib.fg_counters()
     secs = ctypes.c_double()
     if block_range is None:

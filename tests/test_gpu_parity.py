@@ -412,3 +412,39 @@ def test_sweep_validation(fg):
         fg.sweep_run(cfg, t, t, [0.1, -1.0])
     with pytest.raises(ValueError):
         fg.sweep_run(cfg, t, t, [])
+
+
+@pytest.mark.parametrize("alg", ["dfd", "dfdo", "dito"])
+def test_audit_ledger(fg, oracle, alg):
+    """audit=True (summation_engine.py:107-119): the device ledger has one event
+    per settled (query block, reference node) pair, its kinds match the
+    counters, every reference weight is accounted exactly once per query block
+     and the charged bounds telescope to <= eps G_min.
+    Values are bit-identical to the unaudited run."""
+    from paper_1206_6857_b200.harness import telescoping_audit
+
+    rng = np.random.default_rng(17)
+    pts = np.vstack([rng.random((3000, 3)), 0.5 + 0.02 * rng.standard_normal((1000, 3))])
+    w = rng.uniform(0.5, 1.5, pts.shape[0])
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    exact = oracle.naive_sum(pts, pts, w, 0.04, threads=0)
+    for h, eps in ((0.04, 0.01), (0.2, 1e-3)):
+        exact = oracle.naive_sum(pts, pts, w, h, threads=0)
+        t.refresh_moments(h, fg.default_plimit(3))
+        run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[alg]
+        cfg = fg.RunConfig(bandwidth=h, epsilon=eps, algorithm=alg)
+        plain = run(cfg, t, t)
+        res = run(cfg, t, t, audit=True)
+        np.testing.assert_array_equal(res.values, plain.values)
+        c = res.counters
+        assert c == plain.counters
+        kinds = [e[0] for e in res.audit]
+        assert kinds.count("fd") == c.fd_prunes
+        assert kinds.count("base") == c.base_cases
+        assert kinds.count("hermite") == c.hermite_prunes
+        assert kinds.count("local") == c.local_prunes
+        assert kinds.count("h2l") == c.h2l_prunes
+        rep = telescoping_audit(res.audit, t, exact, eps)
+        assert rep["weight_error"] <= 1e-9, rep
+        assert rep["worst_ratio"] <= 1.0, rep
+        assert rep["query_nodes"] > 0
