@@ -232,7 +232,7 @@ def run_ours(args):
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200 import _lib
     from paper_1206_6857_b200.spatial_index import build_tree_device
-    from paper_1206_6857_b200.distributed import run_sharded
+    from paper_1206_6857_b200.distributed import run_sharded, run_sharded_sweep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -259,19 +259,15 @@ def run_ours(args):
     def step(record=True):
         vals_d.zero_()
         tree = build_tree_device(pts_d, w_d, 25)
+        # the whole sweep in one engine call (moments for every bandwidth + one
+        # traversal launch, one synchronisation); with N ranks each runs its
+        # query blocks, then one NCCL all-reduce over disjoint supports gathers
+        # every bandwidth's values -- inside the timed step
+        cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon, algorithm="dito")
         if world == 1:
-            # the whole sweep in one engine call (refresh + run per bandwidth,
-            # stream-ordered, one synchronisation)
-            cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon, algorithm="dito")
             results = fg.sweep_run(cfg, tree, tree, wl.bandwidths, out=vals_d)
         else:
-            results = []
-            for j, h in enumerate(wl.bandwidths):
-                tree.refresh_moments(h, pl)
-                cfg = fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, algorithm="dito")
-                # this rank's query blocks, then the gather (NCCL all-reduce over
-                # disjoint supports) -- inside the timed step
-                results.append(run_sharded(cfg, tree, tree, vals_d[j], rank, world))
+            results = run_sharded_sweep(cfg, tree, tree, wl.bandwidths, vals_d, rank, world)
         if record:
             for res in results:
                 stats["kernel_s"] += res.seconds

@@ -129,6 +129,12 @@ int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
 int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
                  double eps, int32_t mode, int32_t plimit, double *values, fg_counters *counters,
                  double *seconds);
+/* the sweep on query blocks block_begin, +block_stride, ... (< block_end)
+ * only; other entries of values are kept */
+int fg_run_sweep_range(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
+                       double eps, int32_t mode, int32_t plimit, int64_t block_begin,
+                       int64_t block_end, int64_t block_stride, double *values,
+                       fg_counters *counters, double *seconds);
 /* Query-sharded run: only query blocks block_begin,
  * block_begin + block_stride, ... (< block_end) of qtree are processed;
  * values is written only at those blocks' queries (original order).  A

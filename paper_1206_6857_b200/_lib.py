@@ -55,6 +55,7 @@ SIGNATURES = {
     "fg_run_audit": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P, _P, _I64, _P],
     "fg_run_range": [_P, _P, _F64, _F64, _I32, _I32, _I64, _I64, _I64, _P, _P, _P],
     "fg_run_sweep": [_P, _P, _P, _I32, _F64, _I32, _I32, _P, _P, _P],
+    "fg_run_sweep_range": [_P, _P, _P, _I32, _F64, _I32, _I32, _I64, _I64, _I64, _P, _P, _P],
     "fg_launch_count": [_P],
     "fg_fp64_peak": [_P],
     "fg_ex2_peak": [_P],

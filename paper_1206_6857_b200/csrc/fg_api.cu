@@ -512,9 +512,9 @@ int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode, i
     return run_impl(qtree, rtree, h, eps, mode, plimit, 0, -1, 1, values, counters, seconds);
 }
 
-int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
-                 double eps, int32_t mode, int32_t plimit, double *values, fg_counters *counters,
-                 double *seconds) {
+static int sweep_impl(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
+                      double eps, int32_t mode, int32_t plimit, int64_t b0, int64_t b1,
+                      int64_t stride, double *values, fg_counters *counters, double *seconds) {
     FG_REQUIRE(qtree && rtree && bandwidths && values, FG_EINVAL, "null argument");
     FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
     std::vector<double> hs(nh);
@@ -526,20 +526,41 @@ int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32
     for (double h : hs) FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
     const int64_t m = qtree->t.n;
     const bool out_dev = is_device_ptr(values);
+    const bool partial = b0 > 0 || stride > 1 || (b1 >= 0 && b1 < (m + 31) / 32);
     double *dout = values;
     static DBuf s_out;
     if (!out_dev) {
         FG_TRY(s_out.reserve(sizeof(double) * m * nh));
         dout = s_out.as<double>();
+        if (partial)  // keep the caller's other entries
+            FG_CUDA_TRY(cudaMemcpyAsync(dout, values, sizeof(double) * m * nh,
+                                        cudaMemcpyHostToDevice, stream()));
     }
     FG_TRY(run_sweep(qtree->t, rtree->t, hs.data(), nh, eps, mode, plimit, dout, counters,
-                     seconds));
+                     seconds, b0, b1, stride));
     if (!out_dev) {
         FG_CUDA_TRY(cudaMemcpyAsync(values, dout, sizeof(double) * m * nh, cudaMemcpyDeviceToHost,
                                     stream()));
         FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     }
     return FG_OK;
+}
+
+int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
+                 double eps, int32_t mode, int32_t plimit, double *values, fg_counters *counters,
+                 double *seconds) {
+    return sweep_impl(qtree, rtree, bandwidths, nh, eps, mode, plimit, 0, -1, 1, values,
+                      counters, seconds);
+}
+
+int fg_run_sweep_range(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
+                       double eps, int32_t mode, int32_t plimit, int64_t block_begin,
+                       int64_t block_end, int64_t block_stride, double *values,
+                       fg_counters *counters, double *seconds) {
+    FG_REQUIRE(block_begin >= 0 && block_end >= block_begin, FG_EINVAL, "bad block range");
+    FG_REQUIRE(block_stride >= 1, FG_EINVAL, "block stride must be >= 1");
+    return sweep_impl(qtree, rtree, bandwidths, nh, eps, mode, plimit, block_begin, block_end,
+                      block_stride, values, counters, seconds);
 }
 
 int fg_query_block_ranges(fg_tree *qtree, int32_t *starts, int32_t *counts) {

@@ -195,7 +195,8 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
                   double *seconds, const AuditSink *audit = nullptr);
 // all bandwidths of a sweep through shared launches (values: nh x m, device)
 int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int mode, int plimit,
-              double *d_values, fg_counters *counters, double *seconds);
+              double *d_values, fg_counters *counters, double *seconds, int64_t b0 = 0,
+              int64_t b1 = -1, int64_t stride = 1);
 int preorder_map(const TreeDev &t, std::vector<int64_t> &pre);
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
               int dim, const double *hs, int nh, double *d_out);

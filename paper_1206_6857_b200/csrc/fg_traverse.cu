@@ -522,7 +522,8 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
 }
 
 int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int mode, int plimit,
-              double *d_values, fg_counters *counters, double *seconds) {
+              double *d_values, fg_counters *counters, double *seconds, int64_t b0, int64_t b1,
+              int64_t stride) {
     const int D = q.dim;
     if (plimit <= 0) plimit = default_plimit(D);
     FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
@@ -552,7 +553,7 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
             for (int j = 0; j < nj; j++)
                 moms[j] = s_mom.as<double>() + (size_t)j * r.nnodes * r.mom_K;
         }
-        FG_TRY(queue_traversal(q, r, nj, hs + j0, moms.data(), eps, mode, plimit, 0, -1, 1,
+        FG_TRY(queue_traversal(q, r, nj, hs + j0, moms.data(), eps, mode, plimit, b0, b1, stride,
                                outs.data(), s_cnt.as<unsigned long long>() + kCounters * j0, false));
         FG_CUDA_TRY(cudaEventRecord(evs[c + 1], stream()));
     }

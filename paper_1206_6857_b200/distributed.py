@@ -72,3 +72,20 @@ def run_sharded(config, qtree, rtree, out, rank: int, world: int, group=None):
     res = run_blocks(config, qtree, rtree, b0, b1, stride, out=out)
     gather_disjoint(out, group)
     return res
+
+
+def run_sharded_sweep(config, qtree, rtree, bandwidths, out, rank: int, world: int, group=None):
+    """The whole bandwidth sweep on this rank's query blocks (one engine call,
+    one traversal launch), then ONE collective over all bandwidths' values.
+
+    ``out`` is a float64 tensor (len(bandwidths), M) on this rank's device
+    (zeroed here).  Returns this rank's ResultVectors.
+    """
+    from .summation_engine import query_block_count, sweep_run
+
+    nb = query_block_count(qtree)
+    out.zero_()
+    res = sweep_run(config, qtree, rtree, bandwidths, out=out,
+                    block_range=shard_blocks(nb, rank, world))
+    gather_disjoint(out, group)
+    return res

@@ -224,7 +224,7 @@ def dito_run(config: RunConfig, qtree: KdTree, rtree: KdTree, audit: bool = Fals
 
 
 def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
-              out=None) -> list:
+              out=None, block_range=None) -> list:
     """Run ``config.algorithm`` at every bandwidth in one device call.
 
     The per-bandwidth loop of run_sweep (cli_harness.py:246-283): for DITO each
@@ -232,6 +232,8 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
     bandwidth).  ``config.bandwidth`` is ignored.  Returns one ResultVector per
     bandwidth; with ``out`` (a CUDA tensor of shape (len(bandwidths), M)) the
     values stay on the device and each ResultVector holds a row view.
+    ``block_range`` = (begin, end, stride) restricts the sweep to those query
+    blocks (sharding; the other entries of ``out`` are kept).
     """
     if config.algorithm == "naive":
         raise ValueError("sweep_run runs the tree algorithms; use naive_sum for naive")
@@ -240,12 +242,19 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
         raise ValueError("bandwidths must be positive")
     plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
     nh = hs.shape[0]
-    vals = out if out is not None else np.empty((nh, qtree.n))
+    vals = out if out is not None else (np.empty((nh, qtree.n)) if block_range is None
+                                        else np.zeros((nh, qtree.n)))
     cnt = (_lib.fg_counters * nh)()
     secs = np.zeros(nh)
-    _lib.call("fg_run_sweep", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
-              float(config.epsilon), _lib.MODES[config.algorithm], int(plimit), _lib.ptr(vals),
-              cnt, _lib.ptr(secs))
+    if block_range is None:
+        _lib.call("fg_run_sweep", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
+                  float(config.epsilon), _lib.MODES[config.algorithm], int(plimit),
+                  _lib.ptr(vals), cnt, _lib.ptr(secs))
+    else:
+        b0, b1, stride = block_range
+        _lib.call("fg_run_sweep_range", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
+                  float(config.epsilon), _lib.MODES[config.algorithm], int(plimit), int(b0),
+                  int(b1), int(stride), _lib.ptr(vals), cnt, _lib.ptr(secs))
     if config.algorithm == "dito":
         rtree._moments_refreshed(float(hs[-1]), plimit)
     return [ResultVector(vals[j], float(secs[j]), TraversalCounters._from_c(cnt[j]), None)

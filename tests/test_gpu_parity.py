@@ -448,3 +448,33 @@ def test_audit_ledger(fg, oracle, alg):
         assert rep["weight_error"] <= 1e-9, rep
         assert rep["worst_ratio"] <= 1.0, rep
         assert rep["query_nodes"] > 0
+
+
+def test_sharded_sweep_reproduces_full_sweep(fg):
+    """Block shards of a sweep (one launch per rank), run one after another,
+    sum to exactly the unsharded sweep for every bandwidth."""
+    import torch
+
+    from paper_1206_6857_b200.distributed import shard_blocks
+    from paper_1206_6857_b200.summation_engine import query_block_count
+
+    rng = np.random.default_rng(23)
+    pts = rng.random((15000, 3))
+    t = fg.build_tree(fg.PointStore(pts, rng.uniform(0.5, 1.5, 15000)), 25)
+    hs = [0.01, 0.05, 0.2]
+    cfg = fg.RunConfig(bandwidth=hs[0], epsilon=0.01)
+    full = torch.zeros(3, 15000, dtype=torch.float64, device="cuda")
+    fg.sweep_run(cfg, t, t, hs, out=full)
+    nb = query_block_count(t)
+    for world in (2, 5):
+        acc = torch.zeros_like(full)
+        for rank in range(world):
+            part = torch.zeros_like(full)
+            fg.sweep_run(cfg, t, t, hs, out=part, block_range=shard_blocks(nb, rank, world))
+            assert torch.count_nonzero(acc * part) == 0
+            acc += part
+        assert torch.equal(acc, full)
+    # host output keeps the untouched entries
+    host = np.full((3, 15000), -1.0)
+    fg.sweep_run(cfg, t, t, hs, out=host, block_range=shard_blocks(nb, 1, 4))
+    assert np.all(host[:, :] != 0.0) and np.any(host == -1.0)
