@@ -137,6 +137,7 @@ naive_kernel(const double *__restrict__ q, int64_t m, const double *__restrict__
             double2 *dst = reinterpret_cast<double2 *>(tile);
             for (int k = threadIdx.x; k < cnt * S / 2; k += kNaiveThreads) dst[k] = __ldg(src + k);
         }
+        __syncthreads();  // the tile is complete before anyone reads a record
         // tile box -> skip the tile (every exp underflows to exactly 0), run the
         // range-test-free exp (every argument >= -708), or the checked exp
         double tlo[D], thi[D];

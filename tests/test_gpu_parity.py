@@ -478,3 +478,19 @@ def test_sharded_sweep_reproduces_full_sweep(fg):
     host = np.full((3, 15000), -1.0)
     fg.sweep_run(cfg, t, t, hs, out=host, block_range=shard_blocks(nb, 1, 4))
     assert np.all(host[:, :] != 0.0) and np.any(host == -1.0)
+
+
+@pytest.mark.parametrize("D", [5, 7, 8])
+def test_naive_mixed_range_tiles(fg, oracle, D):
+    """Heavy-tailed data at mid bandwidths: reference tiles mix pairs whose
+    exponent is below the FP64 range with normal ones (checked-exp path)."""
+    rng = np.random.default_rng(90 + D)
+    n = 6000
+    ref = rng.standard_t(3, size=(n, D)) * rng.uniform(0.5, 2.0, D)
+    q = ref[rng.choice(n, 300, replace=False)]
+    w = np.ones(n)
+    for h in (0.3, 1.0, 2.0):
+        got = fg.naive_sum(q, ref, w, h).values
+        exact = oracle.naive_sum(q, ref, w, h, threads=0)
+        assert np.all(np.isfinite(got))
+        assert rel(got, exact) <= 1e-12, (D, h)
