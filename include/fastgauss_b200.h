@@ -138,7 +138,8 @@ int fg_run_sweep_range(fg_tree *qtree, fg_tree *rtree, const double *bandwidths,
 /* Query-sharded run: only query blocks block_begin,
  * block_begin + block_stride, ... (< block_end) of qtree are processed;
  * values is written only at those blocks' queries (original order).  A
- * query block is 32 consecutive tree-order points; fg_query_blocks reports
+ * query block is <= 64 consecutive tree-order points (a maximal tree node);
+ * fg_query_blocks reports
  * the block count. */
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks);
 /* tree-order start and point count of every query block (host arrays) */

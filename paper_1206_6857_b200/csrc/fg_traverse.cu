@@ -4,7 +4,7 @@
 //  summation_engine.py:157-455; best_method, error_bounds.py:168-230).
 //
 // Work decomposition:
-//  * The query side is cut into blocks of <= 32 consecutive tree-order points
+//  * The query side is cut into blocks of <= 64 consecutive tree-order points
 //    (a query "node" with a tight box, centroid and inf-radius).  One warp owns
 //    one block at a time; lane j holds query point j in registers.  Warps pull
 //    blocks from an atomic counter (persistent kernel), so every block is
@@ -55,10 +55,11 @@ static constexpr double kFp32Share = 0.05;
 #endif
 
 // ---------------------------------------------------------- query blocks
-// A query block is a run of <= 32 consecutive tree-order points owned by one
-// warp.  Mode 0 (default): the maximal kd-tree nodes with <= 32 points (tight
-// node boxes; leaves larger than 32 -- duplicate points -- are cut into runs
-// of 32).  Mode 1: fixed runs of 32 points regardless of node boundaries.
+// A query block is a run of <= kQBlock (64) consecutive tree-order points owned
+// by one warp (lane l holds points l and l + 32).  Mode 0 (default): the
+// maximal kd-tree nodes with <= kQBlock points (tight node boxes; larger
+// leaves -- duplicate points -- are cut into runs).  Mode 1: fixed runs
+// regardless of node boundaries.
 int g_qblock_mode = 0;
 
 template <int D>
@@ -71,15 +72,28 @@ __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
     if (b >= nqb) return;
     const int2 rg = range[b];
     const int cnt = rg.y;
-    const bool v = lane < cnt;
-    double x[D];
-    if (v) load_point<D>(pw + ((int64_t)rg.x + lane) * S, x);
+    bool v[kQPL];
+    double x[kQPL][D];
+#pragma unroll
+    for (int qi = 0; qi < kQPL; qi++) {
+        v[qi] = lane + 32 * qi < cnt;
+        if (v[qi]) load_point<D>(pw + ((int64_t)rg.x + lane + 32 * qi) * S, x[qi]);
+    }
     double c[D];
 #pragma unroll
     for (int d = 0; d < D; d++) {
-        const double lo = warp_min(v ? x[d] : CUDART_INF);
-        const double hi = warp_max(v ? x[d] : -CUDART_INF);
-        const double sm = warp_sum(v ? x[d] : 0.0);
+        double lo = CUDART_INF, hi = -CUDART_INF, sm = 0.0;
+#pragma unroll
+        for (int qi = 0; qi < kQPL; qi++) {
+            if (v[qi]) {
+                lo = fmin(lo, x[qi][d]);
+                hi = fmax(hi, x[qi][d]);
+                sm += x[qi][d];
+            }
+        }
+        lo = warp_min(lo);
+        hi = warp_max(hi);
+        sm = warp_sum(sm);
         c[d] = sm / cnt;
         if (lane == 0) {
             box[b * 2 * D + d] = lo;
@@ -88,9 +102,12 @@ __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
         }
     }
     double r = 0.0;
-    if (v) {
 #pragma unroll
-        for (int d = 0; d < D; d++) r = fmax(r, fabs(x[d] - c[d]));
+    for (int qi = 0; qi < kQPL; qi++) {
+        if (v[qi]) {
+#pragma unroll
+            for (int d = 0; d < D; d++) r = fmax(r, fabs(x[qi][d] - c[d]));
+        }
     }
     r = warp_max(r);
     if (lane == 0) rad[b] = r;
@@ -100,9 +117,12 @@ static void block_ranges(const TreeDev &t, std::vector<int2> &out) {
     out.clear();
     const char *env = getenv("FG_QBLOCK_MODE");
     const int mode = env ? atoi(env) : g_qblock_mode;
+    // experiment knob: smaller query blocks
+    const char *lenv = getenv("FG_QBLOCK_LIMIT");
+    const int lim = lenv ? std::max(1, std::min(kQBlock, atoi(lenv))) : kQBlock;
     if (mode == 1) {
-        for (int64_t s = 0; s < t.n; s += 32)
-            out.push_back(make_int2((int)s, (int)std::min<int64_t>(32, t.n - s)));
+        for (int64_t s = 0; s < t.n; s += lim)
+            out.push_back(make_int2((int)s, (int)std::min<int64_t>(lim, t.n - s)));
         return;
     }
     std::vector<int4> ni(t.nnodes);
@@ -112,8 +132,8 @@ static void block_ranges(const TreeDev &t, std::vector<int2> &out) {
         const int v = stack.back();
         stack.pop_back();
         const int4 e = ni[v];
-        if (e.y <= 32 || e.z < 0) {
-            for (int s = 0; s < e.y; s += 32) out.push_back(make_int2(e.x + s, std::min(32, e.y - s)));
+        if (e.y <= lim || e.z < 0) {
+            for (int s = 0; s < e.y; s += lim) out.push_back(make_int2(e.x + s, std::min(lim, e.y - s)));
         } else {
             stack.push_back(e.w);
             stack.push_back(e.z);

@@ -13,6 +13,10 @@
 namespace fg {
 
 constexpr int kTravThreads = 128;
+// queries per lane: a query block has up to 32 * kQPL points (lane l holds
+// queries l and l + 32)
+constexpr int kQPL = 2;
+constexpr int kQBlock = 32 * kQPL;
 // largest FP32 base item (and anchor) in points; FP64 items are staged when <= 32
 constexpr int kAnchorMax = 64;
 constexpr int kTravWarps = kTravThreads / 32;
@@ -410,6 +414,18 @@ __device__ __forceinline__ double batch_f32(const float (&xf)[D], const float *f
            (((double)f2_lo(a1) + (double)f2_hi(a1)) + ((double)f2_lo(b1) + (double)f2_hi(b1)));
 }
 
+// query slot qi of a lane without dynamic register indexing (keeps the
+// per-lane arrays out of local memory inside non-unrolled loops)
+template <int D>
+__device__ __forceinline__ void pick_query(const double (&x)[kQPL][D], int qi, double (&xq)[D]) {
+#pragma unroll
+    for (int d = 0; d < D; d++) xq[d] = qi ? x[1][d] : x[0][d];
+}
+__device__ __forceinline__ void add_slot(double (&acc)[kQPL], int qi, double v) {
+    if (qi) acc[1] += v;
+    else acc[0] += v;
+}
+
 __device__ __forceinline__ int warp_excl_scan(int v) {
     const int lane = threadIdx.x & 31;
     int s = v;
@@ -468,19 +484,26 @@ traverse_kernel(const TravArgs A) {
         unsigned steps = 0;
         const int2 rg = A.qb_range[b];
         const int qs = rg.x, qn = rg.y;
-        const bool valid = lane < qn;
+        const int nq = qn > 32 ? 2 : 1;  // query slots in use (warp-uniform)
+        bool valid[kQPL];
         if (lane < 2 * D) sq[lane] = A.qb_box[b * 2 * D + lane];
         if (lane < D) sqc[lane] = A.qb_c[b * D + lane];
         if (A.use_series)
             for (int k = lane; k < A.K; k += 32) loc[k] = 0.0;
         __syncwarp();
-        double x[D];
-        if (valid) load_point<D>(A.q_pw + (int64_t)(qs + lane) * S, x);
-        else {
+        double x[kQPL][D];
 #pragma unroll
-            for (int d = 0; d < D; d++) x[d] = sqc[d];
+        for (int qi = 0; qi < kQPL; qi++) {
+            valid[qi] = lane + 32 * qi < qn;
+            if (valid[qi]) load_point<D>(A.q_pw + (int64_t)(qs + lane + 32 * qi) * S, x[qi]);
+            else {
+#pragma unroll
+                for (int d = 0; d < D; d++) x[qi][d] = sqc[d];
+            }
         }
-        double pt_est = 0.0, pt_mass = 0.0;                    // per point
+        double pt_est[kQPL], pt_mass[kQPL];  // per point
+#pragma unroll
+        for (int qi = 0; qi < kQPL; qi++) pt_est[qi] = pt_mass[qi] = 0.0;
         double lane_est = 0.0;  // this lane's share of the node-level estimates
         double tokens = 0.0;    // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
@@ -539,7 +562,8 @@ traverse_kernel(const TravArgs A) {
             __syncwarp();
             const double WR = wr.x;
             c_vis += nb;
-            const double pmin = warp_min(valid ? pt_mass : CUDART_INF);
+            const double pmin = warp_min(fmin(valid[0] ? pt_mass[0] : CUDART_INF,
+                                              valid[1] ? pt_mass[1] : CUDART_INF));
             const double gmin = (pmin + mass) * kMassSafety;
 
             // ---- finite-difference prune (summation_engine.py:327-351)
@@ -681,10 +705,8 @@ traverse_kernel(const TravArgs A) {
                 const double abs_sum = warp_sum(mine ? abs32 : 0.0);
                 c_f32 += (unsigned)qn * (unsigned)warp_sum(mine ? ni.y : 0);
                 c_base += __popc(f32_mask);
-                float xf[D];
-#pragma unroll
-                for (int d = 0; d < D; d++) xf[d] = (float)(x[d] - sqc[d]);
-                double sum32 = 0.0;
+                double sum32[kQPL] = {0.0, 0.0};
+                static_assert(kQPL == 2, "pick_query/add_slot assume two query slots");
                 unsigned todo = f32_mask;
                 while (todo) {
                     // the next run of whole items that fits the staging area
@@ -720,13 +742,24 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_commit();
                     __pipeline_wait_prior(0);
                     __syncwarp();
-                    sum32 += batch_f32<D>(xf, fst, gdl, total, H.ex2_scale);
+#pragma unroll 1
+                    for (int qi = 0; qi < nq; qi++) {
+                        double xq[D];
+                        pick_query<D>(x, qi, xq);
+                        float xf[D];
+#pragma unroll
+                        for (int d = 0; d < D; d++) xf[d] = (float)(xq[d] - sqc[d]);
+                        add_slot(sum32, qi, batch_f32<D>(xf, fst, gdl, total, H.ex2_scale));
+                    }
                     __syncwarp();
                 }
-                pt_est += sum32;
-                // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho, so
-                // sum32 (1 - fp32_rho) - sum(abs) <= S
-                pt_mass += fmax(sum32 * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+#pragma unroll
+                for (int qi = 0; qi < kQPL; qi++) {
+                    pt_est[qi] += sum32[qi];
+                    // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho, so
+                    // sum32 (1 - fp32_rho) - sum(abs) <= S
+                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                }
             }
             const unsigned base64 = base_mask & ~f32_mask;
             const unsigned small64 = __ballot_sync(kFull, ni.y <= 32) & base_mask & ~f32_mask;
@@ -740,7 +773,7 @@ traverse_kernel(const TravArgs A) {
                 // every pair of this item has K >= K_lo: skip the exp range test
                 // when K_lo is a normal number
                 const double kli = __shfl_sync(kFull, klo, i);
-                double contrib;
+                double contrib[kQPL] = {0.0, 0.0};
                 if ((small64 >> i) & 1u) {
                     const unsigned rest = small64 & ~((2u << i) - 1u);
                     if (rest) {
@@ -752,16 +785,30 @@ traverse_kernel(const TravArgs A) {
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * 32 * S;
-                    contrib = kli >= 2.3e-308 ? base_case<D, false>(x, bp, rc, H.neg_inv, s_tab)
-                                              : base_case<D, true>(x, bp, rc, H.neg_inv, s_tab);
+#pragma unroll 1
+                    for (int qi = 0; qi < nq; qi++) {
+                        double xq[D];
+                        pick_query<D>(x, qi, xq);
+                        add_slot(contrib, qi,
+                                 kli >= 2.3e-308 ? base_case<D, false>(xq, bp, rc, H.neg_inv, s_tab)
+                                                 : base_case<D, true>(xq, bp, rc, H.neg_inv, s_tab));
+                    }
                     __syncwarp();
                     bi ^= 1;
                 } else {
                     const double *rp = A.r_pw + (int64_t)rs * S;
-                    contrib = base_case<D, true>(x, rp, rc, H.neg_inv, s_tab);
+#pragma unroll 1
+                    for (int qi = 0; qi < nq; qi++) {
+                        double xq[D];
+                        pick_query<D>(x, qi, xq);
+                        add_slot(contrib, qi, base_case<D, true>(xq, rp, rc, H.neg_inv, s_tab));
+                    }
                 }
-                pt_est += contrib;
-                pt_mass += contrib;
+#pragma unroll
+                for (int qi = 0; qi < kQPL; qi++) {
+                    pt_est[qi] += contrib[qi];
+                    pt_mass[qi] += contrib[qi];
+                }
                 if (A.use_tokens) tokens += wri;
                 c_base++;
                 c_pairs += (unsigned)(qn * rc);
@@ -804,18 +851,31 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_wait_prior(kRing - 1);
                     __syncwarp();
                     const double *buf = sbuf + (i % kRing) * slot;
-                    if constexpr (D == 3) {
-                        pt_est += eval_far_fixed3<PF>(x, buf + A.K, buf, p, H.inv_sc,
-                                                      [&](double v) { return fg_exp_fast(v, s_tab); });
-                    } else {
-                        pt_est += eval_far_fixed<D, PF>(x, buf + A.K, buf, p, H.inv_sc);
+#pragma unroll 1
+                    for (int qi = 0; qi < nq; qi++) {
+                        double xq[D];
+                        pick_query<D>(x, qi, xq);
+                        if constexpr (D == 3) {
+                            add_slot(pt_est, qi,
+                                     eval_far_fixed3<PF>(xq, buf + A.K, buf, p, H.inv_sc,
+                                                         [&](double v) { return fg_exp_fast(v, s_tab); }));
+                        } else {
+                            add_slot(pt_est, qi,
+                                     eval_far_fixed<D, PF>(xq, buf + A.K, buf, p, H.inv_sc));
+                        }
                     }
                     __syncwarp();
                 } else {
                     const int node = sl[i].x;
-                    pt_est += eval_far_lane<D>(x, A.r_c + (int64_t)node * D,
-                                               H.r_mom + (int64_t)node * A.mom_K, p, A.kp[p], H.sc,
-                                               A.digits);
+#pragma unroll 1
+                    for (int qi = 0; qi < nq; qi++) {
+                        double xq[D];
+                        pick_query<D>(x, qi, xq);
+                        add_slot(pt_est, qi,
+                                 eval_far_lane<D>(xq, A.r_c + (int64_t)node * D,
+                                                  H.r_mom + (int64_t)node * A.mom_K, p, A.kp[p],
+                                                  H.sc, A.digits));
+                    }
                 }
             }
             c_dh += nh;
@@ -837,10 +897,19 @@ traverse_kernel(const TravArgs A) {
                 local_used = true;
                 __syncwarp();
             }
-            if (local_used) pt_est += eval_local_lane<D>(x, qc, loc, A.plimit, A.K, H.sc, A.digits);
+            if (local_used) {
+#pragma unroll 1
+                for (int qi = 0; qi < nq; qi++) {
+                    double xq[D];
+                    pick_query<D>(x, qi, xq);
+                    add_slot(pt_est, qi, eval_local_lane<D>(xq, qc, loc, A.plimit, A.K, H.sc, A.digits));
+                }
+            }
         }
-        const double val = pt_est + warp_sum(lane_est);
-        if (valid) H.out[A.q_perm[qs + lane]] = val;
+        const double node_est = warp_sum(lane_est);
+#pragma unroll
+        for (int qi = 0; qi < kQPL; qi++)
+            if (valid[qi]) H.out[A.q_perm[qs + lane + 32 * qi]] = pt_est[qi] + node_est;
         const unsigned long long cyc = (unsigned long long)(clock64() - t_start);
         if (lane == 0 && A.cost) A.cost[b] = cyc;
         if (lane == 0 && A.dbg) {

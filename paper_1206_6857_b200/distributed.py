@@ -3,7 +3,7 @@
 Every rank holds the full reference tree (rebuilt locally; the device build is
 deterministic, so trees are bit-identical across ranks) and processes the
 query blocks ``rank, rank + world, rank + 2*world, ...`` -- a round-robin deal
-of the 32-point blocks in tree order, i.e. a spatially uniform sample per
+of the (<= 64-point) blocks in tree order, i.e. a spatially uniform sample per
 rank, which balances the strongly density-dependent per-block cost.  Each
 rank writes only its blocks' queries into a zero vector; one collective sum
 over these disjoint supports assembles the full result exactly (x + 0 == x),
@@ -22,7 +22,7 @@ def shard_blocks(nblocks: int, rank: int, world: int):
     return rank, nblocks, world
 
 
-def query_block_ranges(start, end, left, right, limit: int = 32):
+def query_block_ranges(start, end, left, right, limit: int = 64):
     """Host restatement of the engine's query blocks (fg_traverse.cu:
     block_ranges, mode 0): the maximal tree nodes with <= ``limit`` points, in
     tree order; leaves larger than ``limit`` are cut into runs of ``limit``.

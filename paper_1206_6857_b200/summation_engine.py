@@ -126,7 +126,7 @@ AUDIT_KINDS = ("base", "fd", "hermite", "local", "h2l")
 
 def query_block_nodes(qtree: KdTree) -> np.ndarray:
     """Preorder node index (Node.index) of every query block: the maximal node
-    with <= 32 points it is (or, for a larger leaf cut into runs, lies in)."""
+    with <= 64 points it is (or, for a larger leaf cut into runs, lies in)."""
     nb = query_block_count(qtree)
     starts = np.empty(nb, np.int32)
     counts = np.empty(nb, np.int32)
@@ -262,7 +262,7 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
 
 
 def query_block_count(qtree: KdTree) -> int:
-    """Number of 32-point query blocks (the unit of query sharding)."""
+    """Number of query blocks (<= 64 points each; the unit of query sharding)."""
     nb = ctypes.c_int64()
     _lib.call("fg_query_blocks", qtree.handle, ctypes.byref(nb))
     return nb.value

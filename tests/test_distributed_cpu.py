@@ -64,7 +64,7 @@ def test_blocks_partition_queries():
         t = oracle.Tree(pts, None, leaf)
         ex = t.export()
         ranges = D.query_block_ranges(ex["start"], ex["end"], ex["left"], ex["right"])
-        assert all(1 <= c <= 32 for _, c in ranges)
+        assert all(1 <= c <= 64 for _, c in ranges)
         pos = np.concatenate([np.arange(s, s + c) for s, c in ranges])
         np.testing.assert_array_equal(pos, np.arange(n))  # tree order, exact cover
         for world in (1, 2, 3, 8):
