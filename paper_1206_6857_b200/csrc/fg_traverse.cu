@@ -400,7 +400,7 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
                                     f32_smem_doubles<3>(), f32_smem_doubles<4>(),
                                     f32_smem_doubles<5>(), f32_smem_doubles<6>(),
                                     f32_smem_doubles<7>(), f32_smem_doubles<8>()};
-        smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 64 * packed_stride(D) + f32d[D]) *
+        smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32d[D]) *
                kTravWarps;
     }
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));

@@ -17,7 +17,8 @@ constexpr int kTravThreads = 128;
 // queries l and l + 32)
 constexpr int kQPL = 2;
 constexpr int kQBlock = 32 * kQPL;
-// largest FP32 base item (and anchor) in points; FP64 items are staged when <= 32
+// largest FP32 base item (and anchor) in points; FP64 items up to the same
+// size are staged in shared memory (two buffers of kAnchorMax records)
 constexpr int kAnchorMax = 64;
 constexpr int kTravWarps = kTravThreads / 32;
 // Relative safety margin on the running mass bound: the frontier sum is kept
@@ -181,9 +182,9 @@ __device__ __forceinline__ void stage_points(const double *__restrict__ pw, int 
     const int lane = threadIdx.x & 31;
     const int rs = __shfl_sync(kFull, ni_x, i);
     const int rc = __shfl_sync(kFull, ni_y, i);
-    if (lane < rc) {
-        const double *src = pw + (int64_t)(rs + lane) * S;
-        double *dst = buf + lane * S;
+    for (int l = lane; l < rc; l += 32) {
+        const double *src = pw + (int64_t)(rs + l) * S;
+        double *dst = buf + l * S;
 #pragma unroll
         for (int q = 0; q < S / 2; q++) __pipeline_memcpy_async(dst + 2 * q, src + 2 * q, 16);
     }
@@ -452,11 +453,11 @@ traverse_kernel(const TravArgs A) {
     // a double buffer of 2 x 32 staged FP64 reference points, then the FP32
     // batch (transposed records and per-group offsets)
     const int head = (3 * D + A.K + 1) & ~1;
-    double *sq = smem + wib * (head + 64 * S + f32_smem_doubles<D>());
+    double *sq = smem + wib * (head + 2 * kAnchorMax * S + f32_smem_doubles<D>());
     double *sqc = sq + 2 * D;
     double *loc = sq + 3 * D;
     double *sbuf = sq + head;
-    float *fst = reinterpret_cast<float *>(sbuf + 64 * S);
+    float *fst = reinterpret_cast<float *>(sbuf + 2 * kAnchorMax * S);
     float *gdl = fst + f32_cap<D>() * (D + 1);
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
@@ -670,7 +671,7 @@ traverse_kernel(const TravArgs A) {
             // FP32 error bound fits (decided lane-parallel, one item per lane) run
             // as one FP32 batch; the rest (FP64) are staged one by one into shared
             // memory with cp.async, double-buffered so the next item's points load
-            // while this one computes (leaves of > 32 points read global memory).
+            // while this one computes (leaves of > 64 points read global memory).
             const unsigned small_mask = __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask;
             unsigned f32_mask = 0;
             int anc = 0;
@@ -762,7 +763,7 @@ traverse_kernel(const TravArgs A) {
                 }
             }
             const unsigned base64 = base_mask & ~f32_mask;
-            const unsigned small64 = __ballot_sync(kFull, ni.y <= 32) & base_mask & ~f32_mask;
+            const unsigned small64 = __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask & ~f32_mask;
             int bi = 0;
             if (small64) stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(small64) - 1, sbuf);
             for (unsigned m = base64; m; m &= m - 1) {
@@ -778,13 +779,13 @@ traverse_kernel(const TravArgs A) {
                     const unsigned rest = small64 & ~((2u << i) - 1u);
                     if (rest) {
                         stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1,
-                                        sbuf + (bi ^ 1) * 32 * S);
+                                        sbuf + (bi ^ 1) * kAnchorMax * S);
                         __pipeline_wait_prior(1);
                     } else {
                         __pipeline_wait_prior(0);
                     }
                     __syncwarp();
-                    const double *bp = sbuf + bi * 32 * S;
+                    const double *bp = sbuf + bi * kAnchorMax * S;
 #pragma unroll 1
                     for (int qi = 0; qi < nq; qi++) {
                         double xq[D];
@@ -828,7 +829,7 @@ traverse_kernel(const TravArgs A) {
             constexpr int PF = default_plimit_c(D);
             constexpr int kRing = 4;
             const int slot = (A.K + D + 1) & ~1;
-            const bool ring = A.plimit == PF && kRing * slot <= 64 * S;
+            const bool ring = A.plimit == PF && kRing * slot <= 2 * kAnchorMax * S;
             auto stage_item = [&](int k) {
                 const int node = sl[k].x;
                 double *dst = sbuf + (k % kRing) * slot;
