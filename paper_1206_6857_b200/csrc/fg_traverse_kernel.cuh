@@ -300,26 +300,27 @@ __device__ __forceinline__ float ex2_approx(float v) {
 // every query of the block.  With M bounding |x - c_b|, |c_a - c_b|,
 // |x - c_a| and |y - c_a| per coordinate, each coordinate difference carries
 // at most 4 u M of rounding (u = 2^-24) before its own rounding, so a term
-// with exponent a <= a_c = min(a_max, 80) has relative error at most
-//   da + 2^-17,  da = 2^-21 sqrt(D) M sqrt(a_c) / (sqrt2 h) + (4+D) u a_c
-// (the FP32 difference, squared distance and scaling; ex2.approx, measured
-// <= 2^-22.7 by tools/ex2_accuracy.cu; weight rounding; <= 63 additions per
-// FP32 accumulator, of which there are eight); rho doubles that for safety.  a_max = -log K_lo is the
-// item's largest pair exponent (+inf when K_lo underflows).  Terms beyond a_c
-// (ex2 may flush them to zero) are worth at most w e^-80 and so are their
-// computed values: abs = 2 wr e^-80 when a_max > 80, plus 2^-140 for
-// subnormal rounding in the FP32 accumulation.
+// with exponent a has an exponent error (= relative error) of at most
+//   da(a) = C1 sqrt(a) + C2 a,  C1 = 2^-21 sqrt(D) M / (sqrt2 h),  C2 = (4+D) u
+// (the FP32 difference, squared distance and scaling), plus 2^-17 for
+// ex2.approx (measured <= 2^-22.7 by tools/ex2_accuracy.cu), weight rounding
+// and <= 63 additions per FP32 accumulator (eight of them); rho doubles that
+// for safety.  The relative part is only claimed up to a cut a_c: the largest
+// exponent with rho(a_c) <= rho_max, capped at 80 and at a_max = -ln K_lo,
+// the item's largest pair exponent.  Terms beyond a_c (ex2 may flush them)
+// are worth at most w e^-a_c, and so are their computed values up to the
+// factor e^{da(a_c)} (a - da(a) grows with a): abs = 2.03 wr e^-a_c when
+// a_max > a_c, plus 2^-140 for subnormal rounding in the accumulation.
+// Returns rho, or +inf when no cut fits.
 template <int D>
 __device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const double *sq, int anc,
                                                   double inv_h, double klo, double wr,
-                                                  double &abs_err) {
+                                                  double rho_max, double &abs_err) {
     // an upper bound on a_max = -ln K_lo (MUFU lg2: <= 2^-21 relative plus the
     // FP32 rounding of K_lo, covered by the margins; +inf below FLT_MIN)
     const float kf = (float)klo;
     const double a_max = kf >= 1.17549435e-38f ? (double)(-__logf(kf)) * (1.0 + 0x1.0p-18) + 0x1.0p-18
                                                : CUDART_INF;
-    const double a_c = fmin(a_max, 80.0);
-    abs_err = (a_max > 80.0 ? 2.0 * wr * 1.8048513878454153e-35 : 0.0) + 0x1.0p-140;
     const double *abox = A.r_box + (int64_t)anc * 2 * D;
     const double *ac = A.r_c + (int64_t)anc * D;
     double M = 0.0;
@@ -331,9 +332,18 @@ __device__ __forceinline__ double fp32_item_bound(const TravArgs &A, const doubl
                          fmax(fabs(qlo - c), fabs(qhi - c))));
         M = fmax(M, fmax(fabs(c - cb), fmax(fabs(qlo - cb), fabs(qhi - cb))));
     }
-    const double da = 0x1.0p-21 * sqrt((double)D) * M * sqrt(a_c) * inv_h * 0.7071067811865476 +
-                      (4.0 + D) * 0x1.0p-24 * a_c;
-    return 2.0 * (da + 0x1.0p-17);
+    const double c1 = 0x1.0p-21 * sqrt((double)D) * M * inv_h * 0.7071067811865476;
+    const double c2 = (4.0 + D) * 0x1.0p-24;
+    const double room = 0.5 * rho_max - 0x1.0p-17;
+    abs_err = CUDART_INF;
+    if (!(room > 0.0)) return CUDART_INF;
+    // largest s = sqrt(a) with c2 s^2 + c1 s <= room
+    const double sfit = 2.0 * room / (c1 + sqrt(c1 * c1 + 4.0 * c2 * room));
+    const double a_c = fmin(fmin(a_max, 80.0), sfit * sfit * (1.0 - 0x1.0p-40));
+    abs_err = 0x1.0p-140;
+    if (a_max > a_c)
+        abs_err += 2.03 * wr * (double)ex2_approx((float)(-a_c * 1.4426950408889634)) * 1.0001;
+    return 2.0 * (c1 * sqrt(a_c) + c2 * a_c + 0x1.0p-17);
 }
 
 // packed FP32 pairs (sm_100 FADD2 / FFMA2 / FMUL2, round-to-nearest per lane)
@@ -680,7 +690,8 @@ traverse_kernel(const TravArgs A) {
                 bool use = false;
                 if ((small_mask >> lane) & 1u) {
                     anc = __ldg(A.r_anchor + ni.x);
-                    const double rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, abs32);
+                    const double rho =
+                        fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho, abs32);
                     use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
