@@ -257,6 +257,58 @@ __device__ __forceinline__ double base_case(const double (&x)[D],
     return s;
 }
 
+// Both query slots of a lane against one staged item in a single pass over
+// its points (two points x two queries = four independent exp chains).
+template <int D, bool CHECKED>
+__device__ __forceinline__ void base_case2(const double (&x)[kQPL][D],
+                                           const double *__restrict__ rp, int rc, double neg_inv,
+                                           const double *s_tab, double &out0, double &out1) {
+    constexpr int S = packed_stride(D);
+    const ExpK K = exp_consts(s_tab);
+    double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;  // a<query><point>
+    int j = 0;
+    for (; j + 1 < rc; j += 2) {
+        double y0[D], y1[D], w0, w1;
+        read_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        read_point_w<D>(rp + (int64_t)(j + 1) * S, y1, w1);
+        double d00, d01, d10, d11;
+        {
+            const double e00 = x[0][0] - y0[0], e01 = x[0][0] - y1[0];
+            const double e10 = x[1][0] - y0[0], e11 = x[1][0] - y1[0];
+            d00 = e00 * e00; d01 = e01 * e01; d10 = e10 * e10; d11 = e11 * e11;
+        }
+#pragma unroll
+        for (int d = 1; d < D; d++) {
+            const double f00 = x[0][d] - y0[d], f01 = x[0][d] - y1[d];
+            const double f10 = x[1][d] - y0[d], f11 = x[1][d] - y1[d];
+            d00 = fma(f00, f00, d00);
+            d01 = fma(f01, f01, d01);
+            d10 = fma(f10, f10, d10);
+            d11 = fma(f11, f11, d11);
+        }
+        a00 = fma(CHECKED ? fg_exp_kc(d00 * neg_inv, K) : fg_exp_k(d00 * neg_inv, K), w0, a00);
+        a01 = fma(CHECKED ? fg_exp_kc(d01 * neg_inv, K) : fg_exp_k(d01 * neg_inv, K), w1, a01);
+        a10 = fma(CHECKED ? fg_exp_kc(d10 * neg_inv, K) : fg_exp_k(d10 * neg_inv, K), w0, a10);
+        a11 = fma(CHECKED ? fg_exp_kc(d11 * neg_inv, K) : fg_exp_k(d11 * neg_inv, K), w1, a11);
+    }
+    if (j < rc) {
+        double y0[D], w0;
+        read_point_w<D>(rp + (int64_t)j * S, y0, w0);
+        const double e0 = x[0][0] - y0[0], e1 = x[1][0] - y0[0];
+        double d0 = e0 * e0, d1 = e1 * e1;
+#pragma unroll
+        for (int d = 1; d < D; d++) {
+            const double f0 = x[0][d] - y0[d], f1 = x[1][d] - y0[d];
+            d0 = fma(f0, f0, d0);
+            d1 = fma(f1, f1, d1);
+        }
+        a00 = fma(CHECKED ? fg_exp_kc(d0 * neg_inv, K) : fg_exp_k(d0 * neg_inv, K), w0, a00);
+        a10 = fma(CHECKED ? fg_exp_kc(d1 * neg_inv, K) : fg_exp_k(d1 * neg_inv, K), w0, a10);
+    }
+    out0 = a00 + a01;
+    out1 = a10 + a11;
+}
+
 // ---- FP32 base case --------------------------------------------------------
 // The reference tree keeps an FP32 copy of its points (fp32_pack,
 // fg_traverse.cu): coordinates relative to the centre c_a of the point's
@@ -621,7 +673,7 @@ traverse_kernel(const TravArgs A) {
                     }
                     if (possible <= maxerr)
                         select_method_gpu(base, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
-                                          A.ct, A.cross, A.kp, meth, p, bound);
+                                          A.ct, A.cross, A.kp, (double)nq, meth, p, bound);
                 }
                 const bool cand = meth != 0;
                 const double sreq = cand ? required_tokens(WR, bound, tok_scale)
@@ -797,13 +849,14 @@ traverse_kernel(const TravArgs A) {
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * kAnchorMax * S;
-#pragma unroll 1
-                    for (int qi = 0; qi < nq; qi++) {
-                        double xq[D];
-                        pick_query<D>(x, qi, xq);
-                        add_slot(contrib, qi,
-                                 kli >= 2.3e-308 ? base_case<D, false>(xq, bp, rc, H.neg_inv, s_tab)
-                                                 : base_case<D, true>(xq, bp, rc, H.neg_inv, s_tab));
+                    if (nq == 2) {
+                        if (kli >= 2.3e-308)
+                            base_case2<D, false>(x, bp, rc, H.neg_inv, s_tab, contrib[0], contrib[1]);
+                        else
+                            base_case2<D, true>(x, bp, rc, H.neg_inv, s_tab, contrib[0], contrib[1]);
+                    } else {
+                        contrib[0] = kli >= 2.3e-308 ? base_case<D, false>(x[0], bp, rc, H.neg_inv, s_tab)
+                                                     : base_case<D, true>(x[0], bp, rc, H.neg_inv, s_tab);
                     }
                     __syncwarp();
                     bi ^= 1;
