@@ -423,6 +423,11 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
+// acc += a * b in place (ties the accumulator register to the FFMA2 output)
+__device__ __forceinline__ void f2_fma_acc(unsigned long long &acc, unsigned long long a,
+                                           unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
 __device__ __forceinline__ unsigned long long f2_ex2(unsigned long long v) {
     return f2_pack(ex2_approx(f2_lo(v)), ex2_approx(f2_hi(v)));
 }
@@ -458,8 +463,8 @@ __device__ __forceinline__ void group_f32(const float (&xf)[D], const float *fst
         }
     }
     const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(fst + D * CAP + j);
-    acc_a = f2_fma(f2_ex2(f2_mul(da, s2)), w.x, acc_a);
-    acc_b = f2_fma(f2_ex2(f2_mul(db, s2)), w.y, acc_b);
+    f2_fma_acc(acc_a, f2_ex2(f2_mul(da, s2)), w.x);
+    f2_fma_acc(acc_b, f2_ex2(f2_mul(db, s2)), w.y);
 }
 
 template <int D>
@@ -468,6 +473,7 @@ __device__ __forceinline__ double batch_f32(const float (&xf)[D], const float *f
     const unsigned long long s2 = f2_pack(ex2s, ex2s);
     unsigned long long a0 = 0ull, b0 = 0ull, a1 = 0ull, b1 = 0ull;
     int j = 0;
+#pragma unroll 2
     for (; j + 8 <= total; j += 8) {
         group_f32<D>(xf, fst, gd, j, s2, a0, b0);
         group_f32<D>(xf, fst, gd, j + 4, s2, a1, b1);
