@@ -153,12 +153,13 @@ int fg_run_audit(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
 int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
                  int32_t plimit, int64_t block_begin, int64_t block_end, int64_t block_stride,
                  double *values, fg_counters *counters, double *seconds);
-/* engine knobs (0 keeps the current value): reference-side leaf size used by
- * the traversal, per-warp stack capacity; fp32_base (-1 keeps, 0 off, 1 on,
- * default on) lets the traversal evaluate a leaf pair in FP32 when the
- * rigorous error bound of that evaluation fits within the pair's own share of
- * the eps budget (it is charged through the token rule, so the eps guarantee
- * holds; eps = 0 always uses FP64).  Not part of the reference API. */
+/* engine knobs: ref_leaf = reference-side base-item size (> 0 fixes it, 0
+ * keeps the current setting, -1 restores the default choice by bandwidth);
+ * stack_cap = per-warp frontier capacity (0 keeps); fp32_base (-1 keeps, 0
+ * off, 1 on, default on) lets the traversal evaluate leaf pairs in FP32 when
+ * the rigorous error bound of that evaluation fits a reserved share of eps
+ * (eps = 0 always uses FP64).  Not part of the
+ * reference API. */
 int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap, int32_t fp32_base);
 
 /* ---- series algebra (series_expansion.py), batched over `batch` items ---

@@ -350,6 +350,7 @@ int fg_synchronize(void) {
 
 int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap, int32_t fp32_base) {
     if (ref_leaf > 0) g_ref_leaf = ref_leaf;
+    if (ref_leaf < 0) g_ref_leaf = 0;  // by bandwidth
     if (fp32_base >= 0) g_fp32_base = fp32_base ? 1 : 0;
     if (stack_cap > 0) {
         FG_REQUIRE(stack_cap >= 64, FG_EINVAL, "stack capacity must be >= 64");

@@ -156,6 +156,7 @@ struct TreeDev {
     DBuf pf;      // float n x fstride: coords about the anchor centre, then weight
     DBuf anchor;  // int n: the point's maximal node with <= 32 points (BFS id)
     int64_t nqb = 0;
+    double qb_rad_median = 0.0;  // median query-block inf-radius (base-item size rule)
     DBuf qb_range;  // int2 (start, count)
     DBuf qb_box;    // double nqb x 2*dim
     DBuf qb_c;      // double nqb x dim

@@ -46,7 +46,21 @@
 
 namespace fg {
 
-int g_ref_leaf = 48;  // measured best on C2 (32: +5%, 64: +8% kernel time)
+// reference-side base-item size: 0 = by bandwidth (ref_leaf_for), else fixed
+int g_ref_leaf = 0;
+
+// Base-item granularity by bandwidth relative to the query blocks' median
+// inf-radius r_b (measured on C2: 32-point items win below ~0.05 r_b, 48
+// below ~0.5 r_b, 64 above; the per-bandwidth choice is ~3 % faster than any
+// single size).
+static int ref_leaf_for(const TreeDev &q, double h) {
+    if (g_ref_leaf > 0) return g_ref_leaf;
+    const double rb = q.qb_rad_median;
+    if (!(rb > 0.0)) return 48;
+    if (h < 0.05 * rb) return 32;
+    if (h < 0.5 * rb) return 48;
+    return 64;
+}
 int g_stack_cap = 4096;
 int g_fp32_base = 1;
 static constexpr double kFp32Share = 0.05;
@@ -167,7 +181,14 @@ int query_blocks(TreeDev &t) {
     }
 #undef FG_QB
     FG_CUDA_TRY(cudaGetLastError());
-    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    {
+        std::vector<double> rad(nqb);
+        FG_CUDA_TRY(cudaMemcpyAsync(rad.data(), t.qb_rad.p, sizeof(double) * nqb,
+                                    cudaMemcpyDeviceToHost, stream()));
+        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+        std::nth_element(rad.begin(), rad.begin() + nqb / 2, rad.end());
+        t.qb_rad_median = nqb ? rad[nqb / 2] : 0.0;
+    }
     t.nqb = nqb;
     t.qb_valid = true;
     t.qb_order_valid = false;
@@ -367,7 +388,6 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     A.use_tokens = mode >= FG_DFDO;
     A.use_series = series;
     A.plimit = plimit;
-    A.ref_leaf = g_ref_leaf;
     A.stack_cap = g_stack_cap;
     {
         const char *env = getenv("FG_BFS_CAP");
@@ -433,6 +453,7 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         H.r_mom = series ? moms[j] : nullptr;
         H.out = outs[j];
         H.counters = dcnt + (size_t)kCounters * j;
+        H.ref_leaf = ref_leaf_for(q, h);
     }
     if (audit) {
         FG_REQUIRE(nh == 1, FG_EINVAL, "the audit ledger records single runs");

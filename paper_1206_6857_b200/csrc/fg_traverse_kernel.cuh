@@ -36,7 +36,7 @@ struct TravH {
     double *out;                  // values (original query order)
     unsigned long long *counters; // kCounters slots: the 8 fg_counters fields, cycles
     float ex2_scale;              // -log2(e) / (2 h^2)
-    int pad;
+    int ref_leaf;                 // reference nodes with <= ref_leaf points are base items
 };
 
 // One audit-ledger event (summation_engine.py:250, 350, 394-398): kind 0 base
@@ -67,7 +67,7 @@ struct TravArgs {
     long long nbl;  // blocks per bandwidth in [b0, b1) at this stride
     // scalars
     double total_w, floor_c;
-    int use_tokens, use_series, plimit, K, ref_leaf;
+    int use_tokens, use_series, plimit, K;
     double ct[kMaxOrder + 1], cross[kMaxOrder + 1];
     int kp[kMaxOrder + 1];  // coefficient count for order p
     const uint8_t *digits;
@@ -702,7 +702,7 @@ traverse_kernel(const TravArgs A) {
 
             // ---- descend or evaluate exactly (summation_engine.py:400-426)
             const bool rem = act && !fd && !((ser_mask >> lane) & 1u);
-            const bool leafy = ni.z < 0 || ni.y <= A.ref_leaf;
+            const bool leafy = ni.z < 0 || ni.y <= H.ref_leaf;
             unsigned split_mask = __ballot_sync(kFull, rem && !leafy);
             unsigned base_mask = __ballot_sync(kFull, rem && leafy);
             if (cnt + 2 * __popc(split_mask) > cap) {
