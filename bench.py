@@ -387,7 +387,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64+f32",
             "dtype_note": "FP64 traversal, bounds, series and results; leaf pairs in FP32 where "
-                          "their rigorous error bound fits a reserved 5% of eps (DESIGN.md)",
+                          "their rigorous error bound fits a reserved 10% of eps (DESIGN.md)",
             "data": "synthetic (seeded; SURVEY Appendix C)",
             "config": {"workload": describe(wl), "epsilon": wl.epsilon,
                        "bandwidths": len(wl.bandwidths), "parallelism": f"query-blocks x{world}",
