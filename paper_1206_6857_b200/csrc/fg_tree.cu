@@ -35,7 +35,10 @@ namespace fg {
 
 // A chunk is processed by one warp (8 points per lane): deep levels hold many
 // tiny nodes, and warp-level reductions need no block barriers.
-constexpr int kChunk = 256;
+#ifndef FG_BUILD_CHUNK
+#define FG_BUILD_CHUNK 256
+#endif
+constexpr int kChunk = FG_BUILD_CHUNK;
 constexpr int kBuildThreads = 256;
 constexpr int kPerThread = kChunk / kBuildThreads;  // 8
 constexpr int kMaxLevels = 1024;
