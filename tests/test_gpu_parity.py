@@ -494,3 +494,37 @@ def test_naive_mixed_range_tiles(fg, oracle, D):
         exact = oracle.naive_sum(q, ref, w, h, threads=0)
         assert np.all(np.isfinite(got))
         assert rel(got, exact) <= 1e-12, (D, h)
+
+
+def test_kde_entry_point_and_torch_ops(fg, oracle):
+    """kde(): one call for trees + every bandwidth (mono and bichromatic, NumPy
+    and CUDA tensors); torch.ops.fastgauss_b200 give the same values."""
+    import torch
+
+    rng = np.random.default_rng(61)
+    ref = rng.random((4000, 3))
+    w = rng.uniform(0.5, 1.5, 4000)
+    q = rng.random((700, 3))
+    hs = [0.01, 0.05, 0.3]
+    exact_mono = np.stack([oracle.naive_sum(ref, ref, w, h, threads=0) for h in hs])
+    exact_bi = np.stack([oracle.naive_sum(q, ref, w, h, threads=0) for h in hs])
+    for alg in ("dito", "dfd", "naive"):
+        got = fg.kde(None, ref, w, hs, epsilon=0.01, algorithm=alg)
+        assert got.shape == (3, 4000)
+        assert max(rel(got[j], exact_mono[j]) for j in range(3)) <= 0.01
+        got = fg.kde(q, ref, w, hs, epsilon=0.01, algorithm=alg)
+        assert max(rel(got[j], exact_bi[j]) for j in range(3)) <= 0.01
+    one = fg.kde(q, ref, w, 0.05)
+    assert one.shape == (700,) and rel(one, exact_bi[1]) <= 0.01
+    tr, tw = torch.from_numpy(ref).cuda(), torch.from_numpy(w).cuda()
+    dev = fg.kde(None, tr, tw, hs)
+    assert dev.is_cuda and dev.shape == (3, 4000)
+    host = fg.kde(None, ref, w, hs)
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
+    fg.register_torch_ops()
+    swept = torch.ops.fastgauss_b200.kde_sweep(tr, tw, hs, 0.01, 25)
+    np.testing.assert_array_equal(swept.cpu().numpy(), host)
+    nv = torch.ops.fastgauss_b200.naive_sum(tr, tr, tw, hs)
+    assert max(rel(nv[j].cpu().numpy(), exact_mono[j]) for j in range(3)) <= 1e-12
+    with pytest.raises(ValueError):
+        fg.kde(q, ref, w, [])
