@@ -161,6 +161,7 @@ struct TreeDev {
     DBuf qb_box;    // double nqb x 2*dim
     DBuf qb_c;      // double nqb x dim
     DBuf qb_rad;    // double nqb
+    DBuf qb_wmin;   // double nqb: smallest weight among the block's points
     // heaviest-first visiting order from the previous full run's block costs
     bool qb_order_valid = false;
     DBuf qb_cost;   // uint64 nqb: cycles per block in the last full run

@@ -62,6 +62,7 @@ struct TravArgs {
     const double *qb_box;
     const double *qb_c;
     const double *qb_rad;
+    const double *qb_wmin;  // monochromatic runs: per-block min weight (G floor), else null
     const int64_t *q_perm;
     long long b0, b1, stride;
     long long nbl;  // blocks per bandwidth in [b0, b1) at this stride
@@ -574,6 +575,9 @@ traverse_kernel(const TravArgs A) {
 #pragma unroll
         for (int qi = 0; qi < kQPL; qi++) pt_est[qi] = pt_mass[qi] = 0.0;
         double lane_est = 0.0;  // this lane's share of the node-level estimates
+        // lower bound on G for every query of the block known up front: in a
+        // monochromatic run each query's own term (w_q K(0) = w_q)
+        const double gfloor = A.qb_wmin ? A.qb_wmin[b] : 0.0;
         double tokens = 0.0;    // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
         int nh = 0, no = 0;  // deferred series items: Hermite from the front, others from the back
@@ -633,7 +637,7 @@ traverse_kernel(const TravArgs A) {
             c_vis += nb;
             const double pmin = warp_min(fmin(valid[0] ? pt_mass[0] : CUDART_INF,
                                               valid[1] ? pt_mass[1] : CUDART_INF));
-            const double gmin = (pmin + mass) * kMassSafety;
+            const double gmin = fmax((pmin + mass) * kMassSafety, gfloor);
 
             // ---- finite-difference prune (summation_engine.py:327-351)
             const double fd_err = 0.5 * WR * (khi - klo);
