@@ -162,6 +162,7 @@ struct TreeDev {
     DBuf qb_c;      // double nqb x dim
     DBuf qb_rad;    // double nqb
     DBuf qb_wmin;   // double nqb: smallest weight among the block's points
+    DBuf qb_wsum;   // double nqb: total weight of the block's points
     // heaviest-first visiting order from the previous full run's block costs
     bool qb_order_valid = false;
     DBuf qb_cost;   // uint64 nqb: cycles per block in the last full run

@@ -80,7 +80,7 @@ template <int D>
 __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
                                     const int2 *__restrict__ range, double *__restrict__ box,
                                     double *__restrict__ ctr, double *__restrict__ rad,
-                                    double *__restrict__ wmin) {
+                                    double *__restrict__ wmin, double *__restrict__ wsum) {
     constexpr int S = packed_stride(D);
     const int lane = threadIdx.x & 31;
     const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -88,7 +88,7 @@ __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
     const int2 rg = range[b];
     const int cnt = rg.y;
     bool v[kQPL];
-    double x[kQPL][D], wl = CUDART_INF;
+    double x[kQPL][D], wl = CUDART_INF, ws = 0.0;
 #pragma unroll
     for (int qi = 0; qi < kQPL; qi++) {
         v[qi] = lane + 32 * qi < cnt;
@@ -96,10 +96,15 @@ __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
             double w;
             load_point_w<D>(pw + ((int64_t)rg.x + lane + 32 * qi) * S, x[qi], w);
             wl = fmin(wl, w);
+            ws += w;
         }
     }
     wl = warp_min(wl);
-    if (lane == 0) wmin[b] = wl;
+    ws = warp_sum(ws);
+    if (lane == 0) {
+        wmin[b] = wl;
+        wsum[b] = ws;
+    }
     double c[D];
 #pragma unroll
     for (int d = 0; d < D; d++) {
@@ -173,6 +178,7 @@ int query_blocks(TreeDev &t) {
     FG_TRY(t.qb_c.reserve(sizeof(double) * nqb * D));
     FG_TRY(t.qb_rad.reserve(sizeof(double) * nqb));
     FG_TRY(t.qb_wmin.reserve(sizeof(double) * nqb));
+    FG_TRY(t.qb_wsum.reserve(sizeof(double) * nqb));
     FG_CUDA_TRY(cudaMemcpyAsync(t.qb_range.p, ranges.data(), sizeof(int2) * nqb,
                                 cudaMemcpyHostToDevice, stream()));
     const unsigned blocks = (unsigned)((nqb * 32 + 255) / 256);
@@ -181,7 +187,8 @@ int query_blocks(TreeDev &t) {
         count_launch();                                                                     \
         query_blocks_kernel<DD><<<blocks, 256, 0, stream()>>>(                              \
             nqb, t.pw.as<double>(), t.qb_range.as<int2>(), t.qb_box.as<double>(),           \
-            t.qb_c.as<double>(), t.qb_rad.as<double>(), t.qb_wmin.as<double>());            \
+            t.qb_c.as<double>(), t.qb_rad.as<double>(), t.qb_wmin.as<double>(),             \
+            t.qb_wsum.as<double>());                                                        \
         break;
     switch (D) {
         FG_QB(1) FG_QB(2) FG_QB(3) FG_QB(4) FG_QB(5) FG_QB(6) FG_QB(7) FG_QB(8)
@@ -390,6 +397,7 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     // monochromatic: every query is also a reference point, so G(x_q) >= w_q
     // (its own term, K(0) = 1) -- a lower bound available from the first step
     A.qb_wmin = &q == &r ? q.qb_wmin.as<double>() : nullptr;
+    A.qb_wsum = q.qb_wsum.as<double>();
     A.q_perm = q.perm.as<int64_t>();
     A.b0 = b0;
     A.b1 = b1;

@@ -63,6 +63,7 @@ struct TravArgs {
     const double *qb_c;
     const double *qb_rad;
     const double *qb_wmin;  // monochromatic runs: per-block min weight (G floor), else null
+    const double *qb_wsum;  // per-block total weight
     const int64_t *q_perm;
     long long b0, b1, stride;
     long long nbl;  // blocks per bandwidth in [b0, b1) at this stride
@@ -577,7 +578,18 @@ traverse_kernel(const TravArgs A) {
         double lane_est = 0.0;  // this lane's share of the node-level estimates
         // lower bound on G for every query of the block known up front: in a
         // monochromatic run each query's own term (w_q K(0) = w_q)
-        const double gfloor = A.qb_wmin ? A.qb_wmin[b] : 0.0;
+        // and the block's own points: G(x_q) >= W_block exp(-diam^2 / 2h^2)
+        double gfloor = 0.0;
+        if (A.qb_wmin) {
+            double dsq = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const double e = sq[D + d] - sq[d];
+                dsq += e * e;
+            }
+            gfloor = fmax(A.qb_wmin[b],
+                          A.qb_wsum[b] * fg_exp_fast(dsq * H.neg_inv, s_tab) * (1.0 - 1e-12));
+        }
         double tokens = 0.0;    // per block (uniform)
         unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
         int nh = 0, no = 0;  // deferred series items: Hermite from the front, others from the back
