@@ -319,7 +319,8 @@ __device__ __forceinline__ void feasible_orders(double base, double r_ref, doubl
 // best_method, with costs in warp-instruction units of THIS engine instead of
 // the reference's sequential-CPU costs (error_bounds.py:217-221).  A warp owns
 // a block of <= 32 nq queries, nq per lane, so
-//   exhaustive ~ nq N_R (2D + 20)        (lanes evaluate 32 pairs per step)
+//   exhaustive ~ nq N_R c_pair            (lanes evaluate 32 pairs per step;
+//                c_pair = 2D + 20 in FP64, (3D + 8) / 6 with FP32 leaves: tuned)
 //   Hermite    ~ nq (32 D + K_p (D + 1)) (per-query ladders + one K_p product sum)
 //   local      ~ N_R (32 D + ceil(K_p/32)(D + 1))
 //   H2L        ~ 32 D + ceil(K_p/32) K_p (D + 1)
@@ -330,7 +331,8 @@ __device__ __forceinline__ void select_method_gpu(double base, double r_ref, dou
                                                   double n_ref, int dim, double maxerr,
                                                   int plimit, const double *ct,
                                                   const double *cross, const int *kp, double nq,
-                                                  int &method, int &order, double &bound) {
+                                                  double pair_cost, int &method, int &order,
+                                                  double &bound) {
     int p_h, p_l, p_t;
     double e_h, e_l, e_t;
     feasible_orders(base, r_ref, r_query, maxerr, plimit, ct, cross, p_h, p_l, p_t, e_h, e_l,
@@ -340,7 +342,7 @@ __device__ __forceinline__ void select_method_gpu(double base, double r_ref, dou
     if (p_h) c_h = nq * (32.0 * d + kp[p_h] * (d + 1.0));
     if (p_l) c_l = n_ref * (32.0 * d + ((kp[p_l] + 31) / 32) * (d + 1.0));
     if (p_t) c_t = 32.0 * d + ((kp[p_t] + 31) / 32) * (double)kp[p_t] * (d + 1.0);
-    const double c_x = nq * n_ref * (2.0 * d + 20.0);
+    const double c_x = nq * n_ref * pair_cost;
     const double c = fmin(fmin(c_h, c_l), fmin(c_t, c_x));
     if (c == c_h) { method = 2; order = p_h; bound = e_h; return; }
     if (c == c_l) { method = 3; order = p_l; bound = e_l; return; }

@@ -475,6 +475,14 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         H.out = outs[j];
         H.counters = dcnt + (size_t)kCounters * j;
         H.ref_leaf = ref_leaf_for(q, h);
+        {
+            // leaves mostly run as packed FP32 when that path is on: the measured
+            // best exhaustive-vs-series balance is ~(3D + 8) / 6 per pair column
+            // (C5: 2.5-3.5 beat 5 by 10-18 %, 8.5 by 25 %), against 2D + 20 in FP64
+            double c = fp32 ? (3.0 * D + 8.0) / 6.0 : 2.0 * D + 20.0;
+            if (const char *env = getenv("FG_PAIR_COST")) c = atof(env);  // experiment knob
+            H.pair_cost = c;
+        }
     }
     if (audit) {
         FG_REQUIRE(nh == 1, FG_EINVAL, "the audit ledger records single runs");

@@ -37,6 +37,7 @@ struct TravH {
     unsigned long long *counters; // kCounters slots: the 8 fg_counters fields, cycles
     float ex2_scale;              // -log2(e) / (2 h^2)
     int ref_leaf;                 // reference nodes with <= ref_leaf points are base items
+    double pair_cost;             // selector's exhaustive cost per pair (FP32 or FP64 leaves)
 };
 
 // One audit-ledger event (summation_engine.py:250, 350, 394-398): kind 0 base
@@ -695,7 +696,8 @@ traverse_kernel(const TravArgs A) {
                     }
                     if (possible <= maxerr)
                         select_method_gpu(base, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
-                                          A.ct, A.cross, A.kp, (double)nq, meth, p, bound);
+                                          A.ct, A.cross, A.kp, (double)nq, H.pair_cost, meth, p,
+                                          bound);
                 }
                 const bool cand = meth != 0;
                 const double sreq = cand ? required_tokens(WR, bound, tok_scale)
