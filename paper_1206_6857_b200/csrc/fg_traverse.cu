@@ -309,9 +309,9 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     int dev = 0;
     FG_CUDA_TRY(cudaGetDevice(&dev));
     if (c_kern != (const void *)kern || c_smem != smem || c_dev != dev) {
-        if (smem > 48 * 1024)
-            FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem));
+        // (static + dynamic shared memory above 48 KB needs the opt-in)
+        FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
         int sms = 0, occ = 0;
         FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         FG_CUDA_TRY(

@@ -340,9 +340,10 @@ template <int D>
 constexpr int f32_cap() { return D <= 4 ? 256 : 128; }
 template <int D>
 constexpr int f32_fd() { return (D + 3) & ~3; }
-// per-warp shared memory of the batch, in doubles
+// per-warp shared memory of the batch, in doubles: CAP AoS records of
+// fstride floats, then the item table (32 x {offset, count, offset vector})
 template <int D>
-constexpr int f32_smem_doubles() { return (f32_cap<D>() * (D + 1) + f32_cap<D>() / 4 * f32_fd<D>()) / 2; }
+constexpr int f32_smem_doubles() { return (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2; }
 
 __device__ __forceinline__ float ex2_approx(float v) {
     float r;
@@ -359,7 +360,7 @@ __device__ __forceinline__ float ex2_approx(float v) {
 //   da(a) = C1 sqrt(a) + C2 a,  C1 = 2^-21 sqrt(D) M / (sqrt2 h),  C2 = (4+D) u
 // (the FP32 difference, squared distance and scaling), plus 2^-17 for
 // ex2.approx (measured <= 2^-22.7 by tools/ex2_accuracy.cu), weight rounding
-// and <= 63 additions per FP32 accumulator (eight of them); rho doubles that
+// and <= 63 additions per FP32 accumulator (four per query slot); rho doubles that
 // for safety.  The relative part is only claimed up to a cut a_c: the largest
 // exponent with rho(a_c) <= rho_max, capped at 80 and at a_max = -ln K_lo,
 // the item's largest pair exponent.  Terms beyond a_c (ex2 may flush them)
@@ -435,55 +436,70 @@ __device__ __forceinline__ unsigned long long f2_ex2(unsigned long long v) {
     return f2_pack(ex2_approx(f2_lo(v)), ex2_approx(f2_hi(v)));
 }
 
-// Stream one staged batch of `total` points (a multiple of 4): component c of
-// point j at fst[c * CAP + j], group g's offset record at gd[g * FD].  Groups
-// of 4 points go through as two packed pairs, two groups per iteration.
+// Stream one staged batch: nitems items, item t with `cnt` AoS records
+// (fstride floats: coordinates about its anchor, weight) at record offset
+// `off`, and its offset vector dl = fl(c_a - c_b).  The two query slots of the
+// lane form the packed FP32 pair, so every record is loaded once for both
+// (the reference coordinate and weight enter as broadcast operands); four
+// records per iteration, each with its own accumulator pair.
 template <int D>
-__device__ __forceinline__ void group_f32(const float (&xf)[D], const float *fst, const float *gd,
-                                          int j, unsigned long long s2, unsigned long long &acc_a,
-                                          unsigned long long &acc_b) {
-    constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>();
-    float dl[FD];
+__device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], const float *fst,
+                                          const int *ioff, const int *icnt, const float *idl,
+                                          int nitems, float ex2s, double &sum0, double &sum1) {
+    constexpr int F = fstride<D>(), FD = f32_fd<D>();
+    const unsigned long long s2 = f2_pack(ex2s, ex2s);
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 1
+    for (int it = 0; it < nitems; it++) {
+        const int off = ioff[it], cnt = icnt[it];
+        unsigned long long q2[D];
 #pragma unroll
-    for (int k = 0; k < FD; k += 4) {
-        const float4 v = *reinterpret_cast<const float4 *>(gd + (j >> 2) * FD + k);
-        dl[k] = v.x; dl[k + 1] = v.y; dl[k + 2] = v.z; dl[k + 3] = v.w;
-    }
-    unsigned long long da, db;
+        for (int d = 0; d < D; d++) {
+            const float dv = idl[it * FD + d];
+            q2[d] = f2_sub(xf2[d], f2_pack(dv, dv));
+        }
+        const float *rec = fst + off * F;
+        int j = 0;
+        for (; j + 4 <= cnt; j += 4) {
 #pragma unroll
-    for (int d = 0; d < D; d++) {
-        const float q = xf[d] - dl[d];
-        const unsigned long long q2 = f2_pack(q, q);
-        const ulonglong2 c = *reinterpret_cast<const ulonglong2 *>(fst + d * CAP + j);
-        const unsigned long long fa = f2_sub(q2, c.x);
-        const unsigned long long fb = f2_sub(q2, c.y);
-        if (d == 0) {
-            da = f2_mul(fa, fa);
-            db = f2_mul(fb, fb);
-        } else {
-            da = f2_fma(fa, fa, da);
-            db = f2_fma(fb, fb, db);
+            for (int u = 0; u < 4; u++) {
+                const float *r = rec + (j + u) * F;
+                float y[F];
+#pragma unroll
+                for (int k = 0; k < F; k += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(r + k);
+                    y[k] = v.x; y[k + 1] = v.y; y[k + 2] = v.z; y[k + 3] = v.w;
+                }
+                unsigned long long dd = 0ull;
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const unsigned long long f = f2_sub(q2[d], f2_pack(y[d], y[d]));
+                    dd = d == 0 ? f2_mul(f, f) : f2_fma(f, f, dd);
+                }
+                f2_fma_acc(acc[u], f2_ex2(f2_mul(dd, s2)), f2_pack(y[D], y[D]));
+            }
+        }
+        for (; j < cnt; j++) {
+            const float *r = rec + j * F;
+            float y[F];
+#pragma unroll
+            for (int k = 0; k < F; k += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(r + k);
+                y[k] = v.x; y[k + 1] = v.y; y[k + 2] = v.z; y[k + 3] = v.w;
+            }
+            unsigned long long dd = 0ull;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const unsigned long long f = f2_sub(q2[d], f2_pack(y[d], y[d]));
+                dd = d == 0 ? f2_mul(f, f) : f2_fma(f, f, dd);
+            }
+            f2_fma_acc(acc[j & 3], f2_ex2(f2_mul(dd, s2)), f2_pack(y[D], y[D]));
         }
     }
-    const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(fst + D * CAP + j);
-    f2_fma_acc(acc_a, f2_ex2(f2_mul(da, s2)), w.x);
-    f2_fma_acc(acc_b, f2_ex2(f2_mul(db, s2)), w.y);
-}
-
-template <int D>
-__device__ __forceinline__ double batch_f32(const float (&xf)[D], const float *fst,
-                                            const float *gd, int total, float ex2s) {
-    const unsigned long long s2 = f2_pack(ex2s, ex2s);
-    unsigned long long a0 = 0ull, b0 = 0ull, a1 = 0ull, b1 = 0ull;
-    int j = 0;
-#pragma unroll 2
-    for (; j + 8 <= total; j += 8) {
-        group_f32<D>(xf, fst, gd, j, s2, a0, b0);
-        group_f32<D>(xf, fst, gd, j + 4, s2, a1, b1);
-    }
-    if (j < total) group_f32<D>(xf, fst, gd, j, s2, a0, b0);
-    return (((double)f2_lo(a0) + (double)f2_hi(a0)) + ((double)f2_lo(b0) + (double)f2_hi(b0))) +
-           (((double)f2_lo(a1) + (double)f2_hi(a1)) + ((double)f2_lo(b1) + (double)f2_hi(b1)));
+    sum0 = ((double)f2_lo(acc[0]) + (double)f2_lo(acc[1])) +
+           ((double)f2_lo(acc[2]) + (double)f2_lo(acc[3]));
+    sum1 = ((double)f2_hi(acc[0]) + (double)f2_hi(acc[1])) +
+           ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
 }
 
 // query slot qi of a lane without dynamic register indexing (keeps the
@@ -529,7 +545,8 @@ traverse_kernel(const TravArgs A) {
     double *loc = sq + 3 * D;
     double *sbuf = sq + head;
     float *fst = reinterpret_cast<float *>(sbuf + 2 * kAnchorMax * S);
-    float *gdl = fst + f32_cap<D>() * (D + 1);
+    int *itab = reinterpret_cast<int *>(fst + f32_cap<D>() * fstride<D>());  // offsets, counts
+    float *idl = reinterpret_cast<float *>(itab + 64);                       // 32 x FD
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;
@@ -781,8 +798,8 @@ traverse_kernel(const TravArgs A) {
             if (f32_mask) {
                 constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>(), F = fstride<D>();
                 const bool mine = (f32_mask >> lane) & 1u;
-                const int rc4 = mine ? ((ni.y + 3) & ~3) : 0;
-                const int off = warp_excl_scan(rc4);
+                const int rcm = mine ? ni.y : 0;
+                const int off = warp_excl_scan(rcm);
                 float dl[D];
                 if (mine) {
 #pragma unroll
@@ -791,54 +808,47 @@ traverse_kernel(const TravArgs A) {
                 }
                 if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
                 const double abs_sum = warp_sum(mine ? abs32 : 0.0);
-                c_f32 += (unsigned)qn * (unsigned)warp_sum(mine ? ni.y : 0);
+                c_f32 += (unsigned)qn * (unsigned)warp_sum(rcm);
                 c_base += __popc(f32_mask);
+                // both query slots about the block centroid, packed (slot 0, slot 1)
+                unsigned long long xf2[D];
+#pragma unroll
+                for (int d = 0; d < D; d++)
+                    xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
                 double sum32[kQPL] = {0.0, 0.0};
-                static_assert(kQPL == 2, "pick_query/add_slot assume two query slots");
                 unsigned todo = f32_mask;
                 while (todo) {
                     // the next run of whole items that fits the staging area
                     const int base = __shfl_sync(kFull, off, __ffs(todo) - 1);
                     const unsigned batch =
-                        __ballot_sync(kFull, ((todo >> lane) & 1u) && off - base + rc4 <= CAP);
+                        __ballot_sync(kFull, ((todo >> lane) & 1u) && off - base + rcm <= CAP);
                     todo &= ~batch;
                     if ((batch >> lane) & 1u) {
-                        for (int g = (off - base) >> 2; g < (off - base + rc4) >> 2; g++) {
+                        const int t = __popc(batch & lt_mask);
+                        itab[t] = off - base;
+                        itab[32 + t] = rcm;
 #pragma unroll
-                            for (int d = 0; d < D; d++) gdl[g * FD + d] = dl[d];
-                        }
+                        for (int d = 0; d < D; d++) idl[t * FD + d] = dl[d];
                     }
-                    int total = 0;
                     for (unsigned m = batch; m; m &= m - 1) {
                         const int i = __ffs(m) - 1;
                         const int rs = __shfl_sync(kFull, ni.x, i);
                         const int rc = __shfl_sync(kFull, ni.y, i);
                         const int o = __shfl_sync(kFull, off, i) - base;
-                        for (int l = lane; l < ((rc + 3) & ~3); l += 32) {
-                            if (l < rc) {
-                                const float *src = A.r_pf + (int64_t)(rs + l) * F;
+                        for (int l = lane; l < rc; l += 32) {
+                            const float *src = A.r_pf + (int64_t)(rs + l) * F;
+                            float *dst = fst + (o + l) * F;
 #pragma unroll
-                                for (int c = 0; c <= D; c++)
-                                    __pipeline_memcpy_async(fst + c * CAP + o + l, src + c, 4);
-                            } else {
-#pragma unroll
-                                for (int c = 0; c <= D; c++) fst[c * CAP + o + l] = 0.f;
-                            }
+                            for (int k = 0; k < F; k += 4) __pipeline_memcpy_async(dst + k, src + k, 16);
                         }
-                        total = o + ((rc + 3) & ~3);
                     }
                     __pipeline_commit();
                     __pipeline_wait_prior(0);
                     __syncwarp();
-#pragma unroll 1
-                    for (int qi = 0; qi < nq; qi++) {
-                        double xq[D];
-                        pick_query<D>(x, qi, xq);
-                        float xf[D];
-#pragma unroll
-                        for (int d = 0; d < D; d++) xf[d] = (float)(xq[d] - sqc[d]);
-                        add_slot(sum32, qi, batch_f32<D>(xf, fst, gdl, total, H.ex2_scale));
-                    }
+                    double s0, s1;
+                    batch_f32<D>(xf2, fst, itab, itab + 32, idl, __popc(batch), H.ex2_scale, s0, s1);
+                    sum32[0] += s0;
+                    sum32[1] += s1;
                     __syncwarp();
                 }
 #pragma unroll
