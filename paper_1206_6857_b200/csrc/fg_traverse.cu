@@ -62,6 +62,9 @@ static int ref_leaf_for(const TreeDev &q, double h) {
     return 64;
 }
 int g_stack_cap = 4096;
+// h / (median query-block radius) at which a bandwidth's tasks cost most
+// (C2 sweep per-block cycles: the heaviest groups sit at h / r_b ~ 1.5-20)
+static constexpr double kHeavyRatio = 5.0;
 int g_fp32_base = 1;
 static constexpr double kFp32Share = 0.1;  // measured: C5 0.02: +97%, 0.05: +5%, 0.2: +4%
 #ifndef FG_TRAV_MINB
@@ -484,6 +487,22 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
             H.pair_cost = c;
         }
     }
+    // Bandwidth groups run heaviest-first: a (bandwidth, block) task costs most
+    // when h is a few times the query block's radius (the block can neither be
+    // pruned whole nor use a cheap series, and the exact region is wide).
+    // Starting those groups first leaves the cheap ones to fill the launch's
+    // tail (C2 sweep: tasks' summed cycles / launch time 0.67 -> see DESIGN.md
+    // "Task order").  Order only: every task's result is unchanged.
+    {
+        const double rb = q.qb_rad_median > 0.0 ? q.qb_rad_median : 1.0;
+        double key[kMaxSweep];
+        for (int j = 0; j < nh; j++) {
+            key[j] = fabs(log(hs[j] / rb) - log(kHeavyRatio));
+            A.jord[j] = j;
+        }
+        if (getenv("FG_SWEEP_NATURAL") == nullptr)
+            std::stable_sort(A.jord, A.jord + nh, [&](int a, int b) { return key[a] < key[b]; });
+    }
     if (audit) {
         FG_REQUIRE(nh == 1, FG_EINVAL, "the audit ledger records single runs");
         A.audit = reinterpret_cast<AuditEvent *>(audit->events);
@@ -639,6 +658,9 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
         // per-block cycles
         double cyc = 0.0;
         for (int j = 0; j < nj; j++) cyc += (double)hc[(size_t)kCounters * (j0 + j) + 8];
+        if (getenv("FG_DEBUG_SWEEP"))
+            fprintf(stderr, "sweep chunk %d: %.3f ms, task cycles %.4e (= %.3f ms over %d warps at 1.965 GHz)\n",
+                    c, ms, cyc, cyc / (1.965e6 * 148 * 16), 148 * 16);
         for (int j = 0; j < nj; j++) {
             const double share = cyc > 0.0 ? hc[(size_t)kCounters * (j0 + j) + 8] / cyc : 1.0 / nj;
             if (seconds) seconds[j0 + j] = ms * 1e-3 * share;

@@ -83,7 +83,7 @@ struct TravArgs {
     int stack_cap;
     int bfs_cap;  // breadth-first while the frontier holds <= bfs_cap entries
     unsigned long long *work;
-    unsigned long long *dbg;       // optional per-block (cycles, steps, visits, pairs)
+    unsigned long long *dbg;       // optional per-block (cycles, steps, visits, radius bits)
     const int *order;              // block visiting order (single full runs) or null
     unsigned long long *cost;      // per-block cycles of this run (or null)
     const float *r_pf;             // FP32 records about each point's anchor (fp32_pack)
@@ -92,6 +92,7 @@ struct TravArgs {
     unsigned long long *audit_count;
     long long audit_cap;
     int nh;                        // bandwidths in this launch
+    int jord[kMaxSweep];           // task group k runs bandwidth jord[k] (heaviest first)
     TravH hp[kMaxSweep];
 };
 
@@ -461,23 +462,29 @@ __device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], co
         const float *rec = fst + off * F;
         int j = 0;
         for (; j + 4 <= cnt; j += 4) {
+            // four records, dimension-major: four independent FFMA2 chains
+            // interleaved, so a lone warp (the launch's tail) still issues
+            // back to back instead of waiting on each chain's latency
+            float y[4][F];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const float *r = rec + (j + u) * F;
-                float y[F];
+            for (int u = 0; u < 4; u++)
 #pragma unroll
                 for (int k = 0; k < F; k += 4) {
-                    const float4 v = *reinterpret_cast<const float4 *>(r + k);
-                    y[k] = v.x; y[k + 1] = v.y; y[k + 2] = v.z; y[k + 3] = v.w;
+                    const float4 v = *reinterpret_cast<const float4 *>(rec + (j + u) * F + k);
+                    y[u][k] = v.x; y[u][k + 1] = v.y; y[u][k + 2] = v.z; y[u][k + 3] = v.w;
                 }
-                unsigned long long dd = 0ull;
+            unsigned long long dd[4];
 #pragma unroll
-                for (int d = 0; d < D; d++) {
-                    const unsigned long long f = f2_sub(q2[d], f2_pack(y[d], y[d]));
-                    dd = d == 0 ? f2_mul(f, f) : f2_fma(f, f, dd);
+            for (int d = 0; d < D; d++)
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const unsigned long long f = f2_sub(q2[d], f2_pack(y[u][d], y[u][d]));
+                    dd[u] = d == 0 ? f2_mul(f, f) : f2_fma(f, f, dd[u]);
                 }
-                f2_fma_acc(acc[u], f2_ex2(f2_mul(dd, s2)), f2_pack(y[D], y[D]));
-            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) dd[u] = f2_ex2(f2_mul(dd[u], s2));
+#pragma unroll
+            for (int u = 0; u < 4; u++) f2_fma_acc(acc[u], dd[u], f2_pack(y[u][D], y[u][D]));
         }
         for (; j < cnt; j++) {
             const float *r = rec + j * F;
@@ -562,8 +569,9 @@ traverse_kernel(const TravArgs A) {
         if (lane == 0) t = (long long)atomicAdd(A.work, 1ULL);
         t = __shfl_sync(kFull, t, 0);
         if (t >= A.nbl * A.nh) break;
-        const int j = (int)(t / A.nbl);
-        long long b = (t - (long long)j * A.nbl) * A.stride + A.b0;
+        const int g = (int)(t / A.nbl);
+        const int j = A.jord[g];
+        long long b = (t - (long long)g * A.nbl) * A.stride + A.b0;
         // single full runs visit blocks in the given order (heaviest first,
         // from the previous run's measured costs): shortens the tail
         if (A.order) b = __ldg(A.order + b);
@@ -1015,7 +1023,7 @@ traverse_kernel(const TravArgs A) {
             A.dbg[4 * b + 0] = cyc;
             A.dbg[4 * b + 1] = steps;
             A.dbg[4 * b + 2] = c_vis;
-            A.dbg[4 * b + 3] = c_pairs;
+            A.dbg[4 * b + 3] = (unsigned long long)__double_as_longlong(A.qb_rad[b]);
         }
         if (lane == 0) {
             unsigned long long *cn = H.counters;
