@@ -455,7 +455,7 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     if (!q.fp32_ok || !r.fp32_ok || !(eps > 0.0)) fp32 = 0;
     for (int j = 0; j < nh; j++)
         if (!(fabs(-1.4426950408889634 / (2.0 * hs[j] * hs[j])) < 1e30)) fp32 = 0;
-    if (fp32) {
+    if (fp32 && D < 5) {  // anchored FP32 records (the direct stream at D >= 5 needs none)
         FG_TRY(fp32_pack(r));
         A.r_pf = r.pf.as<float>();
         A.r_anchor = r.anchor.as<int>();

@@ -343,8 +343,16 @@ template <int D>
 constexpr int f32_fd() { return (D + 3) & ~3; }
 // per-warp shared memory of the batch, in doubles: CAP AoS records of
 // fstride floats, then the item table (32 x {offset, count, offset vector})
+// D >= 5 streams FP32 records converted from the FP64 points instead (see
+// "Direct FP32 stream" below): one window of kF32Win converted records
 template <int D>
-constexpr int f32_smem_doubles() { return (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2; }
+constexpr bool f32_direct() { return D >= 5; }
+constexpr int kF32Win = kAnchorMax;
+template <int D>
+constexpr int f32_smem_doubles() {
+    return f32_direct<D>() ? kF32Win * fstride<D>() / 2
+                           : (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2;
+}
 
 __device__ __forceinline__ float ex2_approx(float v) {
     float r;
@@ -507,6 +515,141 @@ __device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], co
            ((double)f2_lo(acc[2]) + (double)f2_lo(acc[3]));
     sum1 = ((double)f2_hi(acc[0]) + (double)f2_hi(acc[1])) +
            ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
+}
+
+// ---- Direct FP32 stream (D >= 5) ------------------------------------------
+// At D >= 5 the per-item loop of batch_f32 (each item re-centres the query,
+// then a short record loop with a ragged tail) costs more than converting the
+// records: the items' FP64 points are copied (cp.async) window by window into
+// the FP64 staging buffer -- the next window's copy in flight while the
+// current one computes -- converted by the lanes to FP32 records about the
+// query block's centroid, y' = fl(y - c_b) with fl(w), and streamed in one
+// flat loop.  Records are item-independent, so windows cut items anywhere and
+// items may exceed an anchor (measured: C3 -11 %, C4 -9 % vs anchored batches;
+// at D = 3 the conversion costs more than it saves, +3 %).
+//
+// Error bound of an item (query block box `sq` with centroid c_b, node
+// `node`): with M bounding |x - c_b| over the query box and |y - c_b| over the
+// node's box per coordinate, each coordinate difference fl(xf - y') carries at
+// most 2 u M of rounding (xf and y' one rounding each) before its own
+// rounding, so C1 = 2^-22 sqrt(D) M / (sqrt2 h) in fp32_item_bound's model;
+// everything else is as there (<= 16 additions per accumulator per window).
+template <int D>
+__device__ __forceinline__ double fp32_node_bound(const TravArgs &A, const double *sq, int node,
+                                                  double inv_h, double klo, double wr,
+                                                  double rho_max, double &abs_err) {
+    const float kf = (float)klo;
+    const double a_max = kf >= 1.17549435e-38f ? (double)(-__logf(kf)) * (1.0 + 0x1.0p-18) + 0x1.0p-18
+                                               : CUDART_INF;
+    const double *rbox = A.r_box + (int64_t)node * 2 * D;
+    double M = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double cb = sq[2 * D + d];
+        M = fmax(M, fmax(fmax(fabs(__ldg(rbox + d) - cb), fabs(__ldg(rbox + D + d) - cb)),
+                         fmax(fabs(sq[d] - cb), fabs(sq[D + d] - cb))));
+    }
+    // 2^-22 (1 + 2^-4): the FP64 differences x - c_b, y - c_b before their
+    // FP32 rounding carry 2^-53 relative, covered by the margin
+    const double c1 = 0x1.1p-22 * sqrt((double)D) * M * inv_h * 0.7071067811865476;
+    const double c2 = (4.0 + D) * 0x1.0p-24;
+    const double room = 0.5 * rho_max - 0x1.0p-17;
+    abs_err = CUDART_INF;
+    if (!(room > 0.0)) return CUDART_INF;
+    const double sfit = 2.0 * room / (c1 + sqrt(c1 * c1 + 4.0 * c2 * room));
+    const double a_c = fmin(fmin(a_max, 80.0), sfit * sfit * (1.0 - 0x1.0p-40));
+    abs_err = 0x1.0p-140;
+    if (a_max > a_c)
+        abs_err += 2.03 * wr * (double)ex2_approx((float)(-a_c * 1.4426950408889634)) * 1.0001;
+    return 2.0 * (c1 * sqrt(a_c) + c2 * a_c + 0x1.0p-17);
+}
+
+// Stream one converted window of n records (n a multiple of 4): the lane's two
+// query slots form the packed pair, four records per iteration.
+template <int D>
+__device__ __forceinline__ void window_f32(const unsigned long long (&xf2)[D], const float *fst,
+                                           int n, unsigned long long s2, double &sum0,
+                                           double &sum1) {
+    constexpr int F = fstride<D>();
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 1
+    for (int j = 0; j < n; j += 4) {
+        float y[4][F];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int k = 0; k < F; k += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(fst + (j + u) * F + k);
+                y[u][k] = v.x; y[u][k + 1] = v.y; y[u][k + 2] = v.z; y[u][k + 3] = v.w;
+            }
+        unsigned long long dd[4];
+#pragma unroll
+        for (int d = 0; d < D; d++)
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const unsigned long long f = f2_sub(xf2[d], f2_pack(y[u][d], y[u][d]));
+                dd[u] = d == 0 ? f2_mul(f, f) : f2_fma(f, f, dd[u]);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; u++) dd[u] = f2_ex2(f2_mul(dd[u], s2));
+#pragma unroll
+        for (int u = 0; u < 4; u++) f2_fma_acc(acc[u], dd[u], f2_pack(y[u][D], y[u][D]));
+    }
+    sum0 = ((double)f2_lo(acc[0]) + (double)f2_lo(acc[1])) +
+           ((double)f2_lo(acc[2]) + (double)f2_lo(acc[3]));
+    sum1 = ((double)f2_hi(acc[0]) + (double)f2_hi(acc[1])) +
+           ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
+}
+
+// cp.async the FP64 points of stream window [w0, w0 + kF32Win) into `dst`:
+// item t of the stream (lanes of `items`, in lane order) covers stream
+// positions [off, off + cnt) and tree positions [start, start + cnt).
+template <int D>
+__device__ __forceinline__ void stage_window(const double *__restrict__ pw, unsigned items, int off,
+                                             int cnt, int start, int w0, double *dst) {
+    constexpr int S = packed_stride(D);
+    const int lane = threadIdx.x & 31;
+    const unsigned ov = __ballot_sync(kFull, ((items >> lane) & 1u) && off < w0 + kF32Win &&
+                                                 off + cnt > w0);
+    for (unsigned m = ov; m; m &= m - 1) {
+        const int i = __ffs(m) - 1;
+        const int o = __shfl_sync(kFull, off, i);
+        const int c = __shfl_sync(kFull, cnt, i);
+        const int st = __shfl_sync(kFull, start, i);
+        const int p0 = max(o, w0), p1 = min(o + c, w0 + kF32Win);
+        for (int p = p0 + lane; p < p1; p += 32) {
+            const double *src = pw + (int64_t)(st + p - o) * S;
+            double *d = dst + (p - w0) * S;
+#pragma unroll
+            for (int q = 0; q < S / 2; q++) __pipeline_memcpy_async(d + 2 * q, src + 2 * q, 16);
+        }
+    }
+    __pipeline_commit();
+}
+
+// FP64 window records -> FP32 records about c_b (y' = fl(y - c_b), fl(w)),
+// one record per lane per pass; records [n, n4) become zero-weight padding.
+template <int D>
+__device__ __forceinline__ void convert_window(const double *raw, int n, int n4, const double *sqc,
+                                               float *fst) {
+    constexpr int S = packed_stride(D), F = fstride<D>();
+    const int lane = threadIdx.x & 31;
+    for (int r = lane; r < n4; r += 32) {
+        float rec[F];
+#pragma unroll
+        for (int k = 0; k < F; k++) rec[k] = 0.f;
+        if (r < n) {
+            double y[D], w;
+            read_point_w<D>(raw + r * S, y, w);
+#pragma unroll
+            for (int d = 0; d < D; d++) rec[d] = (float)(y[d] - sqc[d]);
+            rec[D] = (float)w;
+        }
+#pragma unroll
+        for (int k = 0; k < F; k += 4)
+            *reinterpret_cast<float4 *>(fst + r * F + k) =
+                make_float4(rec[k], rec[k + 1], rec[k + 2], rec[k + 3]);
+    }
 }
 
 // query slot qi of a lane without dynamic register indexing (keeps the
@@ -783,16 +926,22 @@ traverse_kernel(const TravArgs A) {
             // as one FP32 batch; the rest (FP64) are staged one by one into shared
             // memory with cp.async, double-buffered so the next item's points load
             // while this one computes (leaves of > 64 points read global memory).
-            const unsigned small_mask = __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask;
+            // anchored batches take items inside one anchor; the direct stream any item
+            const unsigned small_mask =
+                f32_direct<D>() ? base_mask : __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask;
             unsigned f32_mask = 0;
             int anc = 0;
             double abs32 = 0.0;
             if (H.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
                 bool use = false;
                 if ((small_mask >> lane) & 1u) {
-                    anc = __ldg(A.r_anchor + ni.x);
-                    const double rho =
-                        fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho, abs32);
+                    double rho;
+                    if constexpr (f32_direct<D>()) {
+                        rho = fp32_node_bound<D>(A, sq, node, H.inv_h, klo, WR, H.fp32_rho, abs32);
+                    } else {
+                        anc = __ldg(A.r_anchor + ni.x);
+                        rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho, abs32);
+                    }
                     use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
@@ -803,7 +952,51 @@ traverse_kernel(const TravArgs A) {
                              abs32 * tok_scale - WR);
                 audit_append(A, base_mask & ~f32_mask, 0, (int)b, (int)steps, WR, 0.0, gmin, -WR);
             }
-            if (f32_mask) {
+            if (f32_direct<D>() && f32_mask) {
+                const bool mine = (f32_mask >> lane) & 1u;
+                const int rcm = mine ? ni.y : 0;
+                const int off = warp_excl_scan(rcm);
+                const int total = __shfl_sync(kFull, off + rcm, 31);
+                // the first window's copy is in flight during the bookkeeping
+                stage_window<D>(A.r_pw, f32_mask, off, rcm, ni.x, 0, sbuf);
+                if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
+                const double abs_sum = warp_sum(mine ? abs32 : 0.0);
+                c_f32 += (unsigned)qn * (unsigned)total;
+                c_base += __popc(f32_mask);
+                // both query slots about the block centroid, packed (slot 0, slot 1)
+                unsigned long long xf2[D];
+#pragma unroll
+                for (int d = 0; d < D; d++)
+                    xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
+                const unsigned long long s2 = f2_pack(H.ex2_scale, H.ex2_scale);
+                double sum32[kQPL] = {0.0, 0.0};
+                int wb = 0;
+                for (int w0 = 0; w0 < total; w0 += kF32Win) {
+                    // the next window's copy overlaps this window's conversion + math
+                    if (w0 + kF32Win < total)
+                        stage_window<D>(A.r_pw, f32_mask, off, rcm, ni.x, w0 + kF32Win,
+                                        sbuf + (wb ^ 1) * kF32Win * S);
+                    else
+                        __pipeline_commit();
+                    __pipeline_wait_prior(1);
+                    __syncwarp();
+                    const int n = min(kF32Win, total - w0), n4 = (n + 3) & ~3;
+                    convert_window<D>(sbuf + wb * kF32Win * S, n, n4, sqc, fst);
+                    __syncwarp();
+                    double s0, s1;
+                    window_f32<D>(xf2, fst, n4, s2, s0, s1);
+                    sum32[0] += s0;
+                    sum32[1] += s1;
+                    __syncwarp();
+                    wb ^= 1;
+                }
+#pragma unroll
+                for (int qi = 0; qi < kQPL; qi++) {
+                    pt_est[qi] += sum32[qi];
+                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                }
+            }
+            if (!f32_direct<D>() && f32_mask) {
                 constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>(), F = fstride<D>();
                 const bool mine = (f32_mask >> lane) & 1u;
                 const int rcm = mine ? ni.y : 0;

@@ -18,10 +18,14 @@ def main():
     ap.add_argument("--algo", default="dito")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--naive", action="store_true")
+    ap.add_argument("--ref-leaf", type=int, default=0)
     args = ap.parse_args()
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200.configs import config
 
+    if args.ref_leaf:
+        from paper_1206_6857_b200 import _lib
+        _lib.call("fg_set_engine_params", args.ref_leaf, 0, -1)
     wl = config(args.config, scale=args.scale)
     h = wl.bandwidths[args.bw]
     if args.naive:
