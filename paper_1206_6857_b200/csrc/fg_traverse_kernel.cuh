@@ -348,9 +348,16 @@ constexpr int f32_fd() { return (D + 3) & ~3; }
 template <int D>
 constexpr bool f32_direct() { return D >= 5; }
 constexpr int kF32Win = kAnchorMax;
+#ifndef FG_DOT_FORM
+#define FG_DOT_FORM 1
+#endif
+constexpr bool g_dot_form = FG_DOT_FORM;
+// dot-form records of the direct stream: 2s(y - c_b), -s |y - c_b|^2, w
+template <int D>
+constexpr int dstride() { return (D + 2 + 3) & ~3; }
 template <int D>
 constexpr int f32_smem_doubles() {
-    return f32_direct<D>() ? kF32Win * fstride<D>() / 2
+    return f32_direct<D>() ? kF32Win * dstride<D>() / 2
                            : (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2;
 }
 
@@ -534,28 +541,60 @@ __device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], co
 // most 2 u M of rounding (xf and y' one rounding each) before its own
 // rounding, so C1 = 2^-22 sqrt(D) M / (sqrt2 h) in fp32_item_bound's model;
 // everything else is as there (<= 16 additions per accumulator per window).
+//
+// Dot form.  The stream may instead expand the exponent (log2 units,
+// s = log2(e) / 2h^2) as  t = (A_q + B_r) + sum_d X_d C_d  with per-query
+// A_q = fl(-s |X|^2) (X = the FP32 query offsets), per-record
+// B_r = fl(-s |Y|^2), C_d = fl(2 s Y_d) (Y = y - c_b in FP64): one FFMA2 per
+// coordinate instead of FADD2 + FFMA2.  Every rounding is absolute in t:
+// u (|A| + |B| + sum |X_d C_d|) for the stored values and u |t_k| for the
+// D + 1 chain steps, each <= u s (|X| + |Y|)^2, so in natural-log units
+// E = (D + 2) u (R_q + R_r)^2 / 2h^2 with R_q, R_r the largest 2-norm
+// offsets of the query box and the node box from c_b; the query rounding
+// adds C1 / 2 sqrt(a) as above (the record side is exact before its own
+// rounding).  rho_dot = 2 (C1 / 2 sqrt(a) + E + 2^-17), cut as above.
 template <int D>
 __device__ __forceinline__ double fp32_node_bound(const TravArgs &A, const double *sq, int node,
                                                   double inv_h, double klo, double wr,
-                                                  double rho_max, double &abs_err) {
+                                                  double rho_max, double &abs_err,
+                                                  double &rho_dot, double &abs_dot) {
     const float kf = (float)klo;
     const double a_max = kf >= 1.17549435e-38f ? (double)(-__logf(kf)) * (1.0 + 0x1.0p-18) + 0x1.0p-18
                                                : CUDART_INF;
     const double *rbox = A.r_box + (int64_t)node * 2 * D;
-    double M = 0.0;
+    double M = 0.0, Mq = 0.0, rq2 = 0.0, rr2 = 0.0;
 #pragma unroll
     for (int d = 0; d < D; d++) {
         const double cb = sq[2 * D + d];
-        M = fmax(M, fmax(fmax(fabs(__ldg(rbox + d) - cb), fabs(__ldg(rbox + D + d) - cb)),
-                         fmax(fabs(sq[d] - cb), fabs(sq[D + d] - cb))));
+        const double mr = fmax(fabs(__ldg(rbox + d) - cb), fabs(__ldg(rbox + D + d) - cb));
+        const double mq = fmax(fabs(sq[d] - cb), fabs(sq[D + d] - cb));
+        M = fmax(M, fmax(mr, mq));
+        Mq = fmax(Mq, mq);
+        rq2 += mq * mq;
+        rr2 += mr * mr;
     }
     // 2^-22 (1 + 2^-4): the FP64 differences x - c_b, y - c_b before their
     // FP32 rounding carry 2^-53 relative, covered by the margin
     const double c1 = 0x1.1p-22 * sqrt((double)D) * M * inv_h * 0.7071067811865476;
     const double c2 = (4.0 + D) * 0x1.0p-24;
     const double room = 0.5 * rho_max - 0x1.0p-17;
-    abs_err = CUDART_INF;
+    abs_err = abs_dot = CUDART_INF;
+    rho_dot = CUDART_INF;
     if (!(room > 0.0)) return CUDART_INF;
+    {
+        const double c1q = 0x1.1p-23 * sqrt((double)D) * Mq * inv_h * 0.7071067811865476;
+        const double rs = (sqrt(rq2) + sqrt(rr2)) * inv_h;
+        const double e = (D + 2.0) * 0x1.0p-24 * 0.5 * rs * rs * 1.01;
+        const double rm = room - e;
+        if (rm > 0.0) {
+            const double sf = c1q > 0.0 ? rm / c1q : CUDART_INF;
+            const double ac = fmin(fmin(a_max, 80.0), sf * sf * (1.0 - 0x1.0p-40));
+            abs_dot = 0x1.0p-140;
+            if (a_max > ac)
+                abs_dot += 2.03 * wr * (double)ex2_approx((float)(-ac * 1.4426950408889634)) * 1.0001;
+            rho_dot = 2.0 * (c1q * sqrt(ac) + e + 0x1.0p-17);
+        }
+    }
     const double sfit = 2.0 * room / (c1 + sqrt(c1 * c1 + 4.0 * c2 * room));
     const double a_c = fmin(fmin(a_max, 80.0), sfit * sfit * (1.0 - 0x1.0p-40));
     abs_err = 0x1.0p-140;
@@ -644,6 +683,74 @@ __device__ __forceinline__ void convert_window(const double *raw, int n, int n4,
 #pragma unroll
             for (int d = 0; d < D; d++) rec[d] = (float)(y[d] - sqc[d]);
             rec[D] = (float)w;
+        }
+#pragma unroll
+        for (int k = 0; k < F; k += 4)
+            *reinterpret_cast<float4 *>(fst + r * F + k) =
+                make_float4(rec[k], rec[k + 1], rec[k + 2], rec[k + 3]);
+    }
+}
+
+// Dot-form window: records {C_0..C_{D-1}, B, w} (dstride floats), lane
+// query X (packed, both slots) and A_q (packed): t = (A_q + B) + sum X_d C_d.
+template <int D>
+__device__ __forceinline__ void window_dot(const unsigned long long (&xf2)[D],
+                                           unsigned long long aq2, const float *fst, int n,
+                                           double &sum0, double &sum1) {
+    constexpr int F = dstride<D>();
+    unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll 1
+    for (int j = 0; j < n; j += 4) {
+        float y[4][F];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int k = 0; k < F; k += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(fst + (j + u) * F + k);
+                y[u][k] = v.x; y[u][k + 1] = v.y; y[u][k + 2] = v.z; y[u][k + 3] = v.w;
+            }
+        unsigned long long t[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            unsigned long long b2 = f2_pack(y[u][D], y[u][D]);
+            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(t[u]) : "l"(aq2), "l"(b2));
+        }
+#pragma unroll
+        for (int d = 0; d < D; d++)
+#pragma unroll
+            for (int u = 0; u < 4; u++) f2_fma_acc(t[u], xf2[d], f2_pack(y[u][d], y[u][d]));
+#pragma unroll
+        for (int u = 0; u < 4; u++) t[u] = f2_ex2(t[u]);
+#pragma unroll
+        for (int u = 0; u < 4; u++) f2_fma_acc(acc[u], t[u], f2_pack(y[u][D + 1], y[u][D + 1]));
+    }
+    sum0 = ((double)f2_lo(acc[0]) + (double)f2_lo(acc[1])) +
+           ((double)f2_lo(acc[2]) + (double)f2_lo(acc[3]));
+    sum1 = ((double)f2_hi(acc[0]) + (double)f2_hi(acc[1])) +
+           ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
+}
+
+// FP64 window records -> dot-form records about c_b (s = log2(e) / 2h^2).
+template <int D>
+__device__ __forceinline__ void convert_window_dot(const double *raw, int n, int n4,
+                                                   const double *sqc, double s, float *fst) {
+    constexpr int S = packed_stride(D), F = dstride<D>();
+    const int lane = threadIdx.x & 31;
+    for (int r = lane; r < n4; r += 32) {
+        float rec[F];
+#pragma unroll
+        for (int k = 0; k < F; k++) rec[k] = 0.f;
+        if (r < n) {
+            double y[D], w, q = 0.0;
+            read_point_w<D>(raw + r * S, y, w);
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const double e = y[d] - sqc[d];
+                q = fma(e, e, q);
+                rec[d] = (float)(2.0 * s * e);
+            }
+            rec[D] = (float)(-s * q);
+            rec[D + 1] = (float)w;
         }
 #pragma unroll
         for (int k = 0; k < F; k += 4)
@@ -932,12 +1039,19 @@ traverse_kernel(const TravArgs A) {
             unsigned f32_mask = 0;
             int anc = 0;
             double abs32 = 0.0;
+            bool dot_step = false;
             if (H.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
-                bool use = false;
+                bool use = false, use_dot = false;
+                double abs_dot_l = 0.0;
                 if ((small_mask >> lane) & 1u) {
                     double rho;
                     if constexpr (f32_direct<D>()) {
-                        rho = fp32_node_bound<D>(A, sq, node, H.inv_h, klo, WR, H.fp32_rho, abs32);
+                        double rho_dot, abs_dot;
+                        rho = fp32_node_bound<D>(A, sq, node, H.inv_h, klo, WR, H.fp32_rho, abs32,
+                                                 rho_dot, abs_dot);
+                        use_dot = rho_dot <= H.fp32_rho && abs_dot * tok_scale <= WR &&
+                                  g_dot_form;
+                        if (use_dot) abs_dot_l = abs_dot;
                     } else {
                         anc = __ldg(A.r_anchor + ni.x);
                         rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho, abs32);
@@ -945,6 +1059,15 @@ traverse_kernel(const TravArgs A) {
                     use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
                 f32_mask = __ballot_sync(kFull, use);
+                if constexpr (f32_direct<D>()) {
+                    // the dot form when every eligible item admits it
+                    const unsigned dm = __ballot_sync(kFull, use_dot);
+                    dot_step = dm != 0u && (dm | f32_mask) == dm;
+                    if (dot_step) {
+                        f32_mask = dm;
+                        abs32 = abs_dot_l;
+                    }
+                }
             }
             if constexpr (AUDIT) {
                 // FP32 items charge their absolute error part to the tokens
@@ -969,6 +1092,19 @@ traverse_kernel(const TravArgs A) {
                 for (int d = 0; d < D; d++)
                     xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
                 const unsigned long long s2 = f2_pack(H.ex2_scale, H.ex2_scale);
+                // dot form: per-slot A_q = fl(-s |X|^2) from the FP32 offsets X
+                const double sdot = -H.neg_inv * 1.4426950408889634;
+                unsigned long long aq2 = 0ull;
+                if (dot_step) {
+                    double q0 = 0.0, q1 = 0.0;
+#pragma unroll
+                    for (int d = 0; d < D; d++) {
+                        const double e0 = f2_lo(xf2[d]), e1 = f2_hi(xf2[d]);
+                        q0 = fma(e0, e0, q0);
+                        q1 = fma(e1, e1, q1);
+                    }
+                    aq2 = f2_pack((float)(-sdot * q0), (float)(-sdot * q1));
+                }
                 double sum32[kQPL] = {0.0, 0.0};
                 int wb = 0;
                 for (int w0 = 0; w0 < total; w0 += kF32Win) {
@@ -981,10 +1117,16 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_wait_prior(1);
                     __syncwarp();
                     const int n = min(kF32Win, total - w0), n4 = (n + 3) & ~3;
-                    convert_window<D>(sbuf + wb * kF32Win * S, n, n4, sqc, fst);
-                    __syncwarp();
                     double s0, s1;
-                    window_f32<D>(xf2, fst, n4, s2, s0, s1);
+                    if (dot_step) {
+                        convert_window_dot<D>(sbuf + wb * kF32Win * S, n, n4, sqc, sdot, fst);
+                        __syncwarp();
+                        window_dot<D>(xf2, aq2, fst, n4, s0, s1);
+                    } else {
+                        convert_window<D>(sbuf + wb * kF32Win * S, n, n4, sqc, fst);
+                        __syncwarp();
+                        window_f32<D>(xf2, fst, n4, s2, s0, s1);
+                    }
                     sum32[0] += s0;
                     sum32[1] += s1;
                     __syncwarp();
