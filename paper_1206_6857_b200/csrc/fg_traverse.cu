@@ -53,11 +53,20 @@ int g_ref_leaf = 0;
 // inf-radius r_b (measured on C2: 32-point items win below ~0.05 r_b, 48
 // below ~0.5 r_b, 64 above; the per-bandwidth choice is ~3 % faster than any
 // single size).
+// At D >= 5 the direct FP32 stream takes items of any size: at h >~ 0.4 r_b,
+// where nearly every pair is exact, bigger items save traversal steps (C4
+// single runs: 128 points -2 % at 0.44 r_b, 256 points -8..-14 % from 0.6 r_b;
+// C3 -6..-14 % at 1-11 r_b).
 static int ref_leaf_for(const TreeDev &q, double h) {
     if (g_ref_leaf > 0) return g_ref_leaf;
     const double rb = q.qb_rad_median;
     if (!(rb > 0.0)) return 48;
     if (h < 0.05 * rb) return 32;
+    if (q.dim >= 5) {
+        if (h < 0.4 * rb) return 48;
+        if (h < 0.8 * rb) return 128;
+        return 256;
+    }
     if (h < 0.5 * rb) return 48;
     return 64;
 }
