@@ -446,13 +446,12 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     // points, the FP32 batch
     size_t smem;
     {
-        static const int f32d[9] = {0,
-                                    f32_smem_doubles<1>(), f32_smem_doubles<2>(),
-                                    f32_smem_doubles<3>(), f32_smem_doubles<4>(),
-                                    f32_smem_doubles<5>(), f32_smem_doubles<6>(),
-                                    f32_smem_doubles<7>(), f32_smem_doubles<8>()};
-        smem = sizeof(double) * (((3 * D + A.K + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32d[D]) *
-               kTravWarps;
+        static const int fixd[9] = {0,
+                                    warp_fixed_doubles<1>(), warp_fixed_doubles<2>(),
+                                    warp_fixed_doubles<3>(), warp_fixed_doubles<4>(),
+                                    warp_fixed_doubles<5>(), warp_fixed_doubles<6>(),
+                                    warp_fixed_doubles<7>(), warp_fixed_doubles<8>()};
+        smem = sizeof(double) * (fixd[D] + ((A.K + 1) & ~1)) *kTravWarps;
     }
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
     A.work = g_scr.work.as<unsigned long long>();

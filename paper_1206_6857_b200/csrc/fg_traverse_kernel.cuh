@@ -361,6 +361,13 @@ constexpr int f32_smem_doubles() {
                            : (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2;
 }
 
+// per-warp shared memory before the local coefficients (K doubles): query
+// box and centroid, the FP64 staging buffer, the FP32 batch / window
+template <int D>
+constexpr int warp_fixed_doubles() {
+    return ((3 * D + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32_smem_doubles<D>();
+}
+
 __device__ __forceinline__ float ex2_approx(float v) {
     float r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
@@ -796,14 +803,15 @@ traverse_kernel(const TravArgs A) {
     // per-warp shared memory: query box (lo, hi), centroid, local coefficients,
     // a double buffer of 2 x 32 staged FP64 reference points, then the FP32
     // batch (transposed records and per-group offsets)
-    const int head = (3 * D + A.K + 1) & ~1;
-    double *sq = smem + wib * (head + 2 * kAnchorMax * S + f32_smem_doubles<D>());
+    // (fixed-size parts first: every pointer below is sq + a compile-time
+    // offset, so the kernel keeps one shared-memory base register)
+    double *sq = smem + wib * (warp_fixed_doubles<D>() + ((A.K + 1) & ~1));
     double *sqc = sq + 2 * D;
-    double *loc = sq + 3 * D;
-    double *sbuf = sq + head;
+    double *sbuf = sq + ((3 * D + 1) & ~1);
     float *fst = reinterpret_cast<float *>(sbuf + 2 * kAnchorMax * S);
     int *itab = reinterpret_cast<int *>(fst + f32_cap<D>() * fstride<D>());  // offsets, counts
     float *idl = reinterpret_cast<float *>(itab + 64);                       // 32 x FD
+    double *loc = sq + warp_fixed_doubles<D>();
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;

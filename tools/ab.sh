@@ -6,7 +6,7 @@ for rep in 1 2; do
   for c in $cfgs; do
     for v in "$@"; do
       if [ "$v" = cur ]; then lib=""; else lib="variants/$v.so"; fi
-      ms=$(FG_LIB=$lib python tools/one_sweep.py --config $c --reps 3 2>/dev/null | awk '{print $4}')
+      ms=$(FG_LIB=$lib python tools/one_sweep.py --config $c --reps $([ $c -le 2 ] && echo 8 || echo 3) 2>/dev/null | awk '{print $4}')
       echo "C$c $v $ms"
     done
   done

@@ -21,9 +21,13 @@ def main():
     rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
     qt = rt if wl.monochromatic else fg.build_tree(fg.PointStore(wl.queries), 25)
     cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon)
-    for _ in range(args.reps):
+    best = None
+    for i in range(args.reps):
         res = fg.sweep_run(cfg, qt, rt, wl.bandwidths)
-    print("sweep kernel ms", sum(r.seconds for r in res) * 1e3)
+        ms = sum(r.seconds for r in res) * 1e3
+        if i > 0 or args.reps == 1:
+            best = ms if best is None else min(best, ms)
+    print("sweep kernel ms", best, "(min over reps after the first)")
 
 
 if __name__ == "__main__":
