@@ -363,9 +363,17 @@ constexpr int f32_smem_doubles() {
 
 // per-warp shared memory before the local coefficients (K doubles): query
 // box and centroid, the FP64 staging buffer, the FP32 batch / window
+// At D <= 4 the block's query coordinates live in shared memory (xs_doubles)
+// rather than in registers: the traversal kernel is register-bound, and the
+// FP32 batch loop is scheduled tighter with the 4D registers back.
+template <int D>
+constexpr bool xs_smem() { return D <= 4; }
+template <int D>
+constexpr int xs_doubles() { return xs_smem<D>() ? kQBlock * D : 0; }
 template <int D>
 constexpr int warp_fixed_doubles() {
-    return ((3 * D + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32_smem_doubles<D>();
+    return ((3 * D + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32_smem_doubles<D>() +
+           xs_doubles<D>();
 }
 
 __device__ __forceinline__ float ex2_approx(float v) {
@@ -812,6 +820,8 @@ traverse_kernel(const TravArgs A) {
     int *itab = reinterpret_cast<int *>(fst + f32_cap<D>() * fstride<D>());  // offsets, counts
     float *idl = reinterpret_cast<float *>(itab + 64);                       // 32 x FD
     double *loc = sq + warp_fixed_doubles<D>();
+    // query coordinates (D <= 4): sx[(d * kQPL + qi) * 32 + lane]
+    double *sx = loc - xs_doubles<D>();
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;
@@ -846,16 +856,32 @@ traverse_kernel(const TravArgs A) {
         if (A.use_series)
             for (int k = lane; k < A.K; k += 32) loc[k] = 0.0;
         __syncwarp();
-        double x[kQPL][D];
+        double xr[xs_smem<D>() ? 1 : kQPL][D];  // query coordinates in registers (D >= 5)
 #pragma unroll
         for (int qi = 0; qi < kQPL; qi++) {
             valid[qi] = lane + 32 * qi < qn;
-            if (valid[qi]) load_point<D>(A.q_pw + (int64_t)(qs + lane + 32 * qi) * S, x[qi]);
+            double xq[D];
+            if (valid[qi]) load_point<D>(A.q_pw + (int64_t)(qs + lane + 32 * qi) * S, xq);
             else {
 #pragma unroll
-                for (int d = 0; d < D; d++) x[qi][d] = sqc[d];
+                for (int d = 0; d < D; d++) xq[d] = sqc[d];
+            }
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                if constexpr (xs_smem<D>()) sx[(d * kQPL + qi) * 32 + lane] = xq[d];
+                else xr[qi][d] = xq[d];
             }
         }
+        // the lane's query coordinates, wherever they live
+        auto get_x = [&](double (&xx)[kQPL][D]) {
+#pragma unroll
+            for (int qi = 0; qi < kQPL; qi++)
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    if constexpr (xs_smem<D>()) xx[qi][d] = sx[(d * kQPL + qi) * 32 + lane];
+                    else xx[qi][d] = xr[xs_smem<D>() ? 0 : qi][d];
+                }
+        };
         double pt_est[kQPL], pt_mass[kQPL];  // per point
 #pragma unroll
         for (int qi = 0; qi < kQPL; qi++) pt_est[qi] = pt_mass[qi] = 0.0;
@@ -1096,9 +1122,13 @@ traverse_kernel(const TravArgs A) {
                 c_base += __popc(f32_mask);
                 // both query slots about the block centroid, packed (slot 0, slot 1)
                 unsigned long long xf2[D];
+                {
+                    double x[kQPL][D];
+                    get_x(x);
 #pragma unroll
-                for (int d = 0; d < D; d++)
-                    xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
+                    for (int d = 0; d < D; d++)
+                        xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
+                }
                 const unsigned long long s2 = f2_pack(H.ex2_scale, H.ex2_scale);
                 // dot form: per-slot A_q = fl(-s |X|^2) from the FP32 offsets X
                 const double sdot = -H.neg_inv * 1.4426950408889634;
@@ -1163,9 +1193,13 @@ traverse_kernel(const TravArgs A) {
                 c_base += __popc(f32_mask);
                 // both query slots about the block centroid, packed (slot 0, slot 1)
                 unsigned long long xf2[D];
+                {
+                    double x[kQPL][D];
+                    get_x(x);
 #pragma unroll
-                for (int d = 0; d < D; d++)
-                    xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
+                    for (int d = 0; d < D; d++)
+                        xf2[d] = f2_pack((float)(x[0][d] - sqc[d]), (float)(x[1][d] - sqc[d]));
+                }
                 double sum32[kQPL] = {0.0, 0.0};
                 unsigned todo = f32_mask;
                 while (todo) {
@@ -1234,6 +1268,8 @@ traverse_kernel(const TravArgs A) {
                     }
                     __syncwarp();
                     const double *bp = sbuf + bi * kAnchorMax * S;
+                    double x[kQPL][D];
+                    get_x(x);
                     if (nq == 2) {
                         if (kli >= 2.3e-308)
                             base_case2<D, false>(x, bp, rc, H.neg_inv, s_tab, contrib[0], contrib[1]);
@@ -1247,6 +1283,8 @@ traverse_kernel(const TravArgs A) {
                     bi ^= 1;
                 } else {
                     const double *rp = A.r_pw + (int64_t)rs * S;
+                    double x[kQPL][D];
+                    get_x(x);
 #pragma unroll 1
                     for (int qi = 0; qi < nq; qi++) {
                         double xq[D];
@@ -1269,6 +1307,8 @@ traverse_kernel(const TravArgs A) {
         unsigned c_dh = 0, c_dl = 0, c_h2l = 0;
         bool local_used = false;
         if (nh + no > 0) {
+            double x[kQPL][D];
+            get_x(x);
             double qc[D];
 #pragma unroll
             for (int d = 0; d < D; d++) qc[d] = sqc[d];
