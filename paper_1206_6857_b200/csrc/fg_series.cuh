@@ -106,19 +106,23 @@ struct GLex {
 
 // EVALM with a compile-time index set: the ladders live in registers and every
 // product indexes them with constants.  Evaluates the order-p prefix (p <= P).
-template <int D, int P>
+// The Hermite functions factor as h_n(t) = H_n(t) e^{-t^2} (kernel_math.py:42-65
+// builds them by the same recurrence from h_0 = e^{-t^2}), so the ladders carry
+// the Hermite polynomials and the product over dimensions takes ONE
+// exponential, e^{-|t|^2}, applied to the sum (instead of one per dimension).
+template <int D, int P, class ExpF>
 __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
                                                  const double *__restrict__ c,
                                                  const double *__restrict__ A, int p,
-                                                 double inv_sc) {
+                                                 double inv_sc, ExpF expf) {
     constexpr GLex<D, P> G;
-    double lad[D][P];
+    double lad[D][P], tt = 0.0;
 #pragma unroll
     for (int d = 0; d < D; d++) {
         const double t = (x[d] - c[d]) * inv_sc;
-        const double g = exp(-t * t);
-        lad[d][0] = g;
-        if (P > 1) lad[d][1] = 2.0 * t * g;
+        tt = fma(t, t, tt);
+        lad[d][0] = 1.0;
+        if (P > 1) lad[d][1] = 2.0 * t;
 #pragma unroll
         for (int n = 1; n + 1 < P; n++) lad[d][n + 1] = 2.0 * t * lad[d][n] - 2.0 * n * lad[d][n - 1];
     }
@@ -136,7 +140,8 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
             acc = fma(v, A[k], acc);
         }
     }
-    return acc;
+    const double g = expf(-tt);
+    return g == 0.0 ? 0.0 : acc * g;  // (no inf * 0 for absurdly distant centres)
 }
 
 // Graded-lex position of a 3-digit index (for the factorised D = 3 EVALM).
@@ -161,13 +166,13 @@ __device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
                                                   const double *__restrict__ A, int p,
                                                   double inv_sc, ExpF expf) {
     constexpr GLexIndex3<P> I{};
-    double lad[3][P];
+    double lad[3][P], tt = 0.0;  // Hermite polynomials; e^{-|t|^2} applied once
 #pragma unroll
     for (int d = 0; d < 3; d++) {
         const double t = (x[d] - c[d]) * inv_sc;
-        const double g = expf(-t * t);
-        lad[d][0] = g;
-        if (P > 1) lad[d][1] = 2.0 * t * g;
+        tt = fma(t, t, tt);
+        lad[d][0] = 1.0;
+        if (P > 1) lad[d][1] = 2.0 * t;
 #pragma unroll
         for (int n = 1; n + 1 < P; n++) lad[d][n + 1] = 2.0 * t * lad[d][n] - 2.0 * n * lad[d][n - 1];
     }
@@ -187,7 +192,8 @@ __device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
         }
         acc = fma(t1, lad[0][a], acc);
     }
-    return acc;
+    const double g = expf(-tt);
+    return g == 0.0 ? 0.0 : acc * g;  // (no inf * 0 for absurdly distant centres)
 }
 
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)

@@ -519,8 +519,8 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         FG_CUDA_TRY(cudaMemsetAsync(audit->count, 0, sizeof(unsigned long long), stream()));
     }
     if (getenv("FG_DEBUG_BLOCKS") && nh == 1) {
-        FG_TRY(g_scr.dbg.reserve(sizeof(unsigned long long) * 4 * q.nqb));
-        FG_CUDA_TRY(cudaMemsetAsync(g_scr.dbg.p, 0, sizeof(unsigned long long) * 4 * q.nqb, stream()));
+        FG_TRY(g_scr.dbg.reserve(sizeof(unsigned long long) * kDbgFields * q.nqb));
+        FG_CUDA_TRY(cudaMemsetAsync(g_scr.dbg.p, 0, sizeof(unsigned long long) * kDbgFields * q.nqb, stream()));
         A.dbg = g_scr.dbg.as<unsigned long long>();
     }
     const bool full = b0 == 0 && b1 == q.nqb && A.stride == 1 && nh == 1 && lpt;
@@ -606,8 +606,8 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         *seconds = ms * 1e-3;
     }
     if (const char *dbg_path = getenv("FG_DEBUG_BLOCKS")) {
-        std::vector<unsigned long long> hd(4 * q.nqb);
-        cudaMemcpy(hd.data(), g_scr.dbg.p, sizeof(unsigned long long) * 4 * q.nqb,
+        std::vector<unsigned long long> hd(kDbgFields * q.nqb);
+        cudaMemcpy(hd.data(), g_scr.dbg.p, sizeof(unsigned long long) * kDbgFields * q.nqb,
                    cudaMemcpyDeviceToHost);
         if (FILE *f = fopen(dbg_path, "ab")) {
             fwrite(hd.data(), sizeof(unsigned long long), hd.size(), f);

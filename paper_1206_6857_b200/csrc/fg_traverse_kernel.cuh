@@ -28,6 +28,10 @@ constexpr double kMassSafety = 1.0 - 1e-10;
 // Per-bandwidth parameters of one launch (a launch serves up to kMaxSweep
 // bandwidths of a sweep; its tasks are (bandwidth, query block) pairs).
 constexpr int kMaxSweep = 24;
+constexpr int kDbgFields = 16;  // per-block debug record (FG_DEBUG_BLOCKS)
+#ifndef FG_PHASE_PROF
+#define FG_PHASE_PROF 0  // per-block phase cycle counters in the debug record
+#endif
 constexpr int kCounters = 16;  // per-bandwidth device counter slots (9 used)
 struct TravH {
     double h, neg_inv, inv_h, sc, inv_sc, eps;
@@ -83,7 +87,8 @@ struct TravArgs {
     int stack_cap;
     int bfs_cap;  // breadth-first while the frontier holds <= bfs_cap entries
     unsigned long long *work;
-    unsigned long long *dbg;       // optional per-block (cycles, steps, visits, radius bits)
+    unsigned long long *dbg;       // optional per-block kDbgFields: cycles, steps, visits,
+                                   // radius bits, FP32 pairs, -, -, -, phase cycles x 8
     const int *order;              // block visiting order (single full runs) or null
     unsigned long long *cost;      // per-block cycles of this run (or null)
     const float *r_pf;             // FP32 records about each point's anchor (fp32_pack)
@@ -846,6 +851,20 @@ traverse_kernel(const TravArgs A) {
         const TravH &H = A.hp[j];
 
         const long long t_start = clock64();
+#if FG_PHASE_PROF
+        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long ph_t = t_start;
+#define PH_MARK(k)                           \
+    do {                                     \
+        const long long ph_n = clock64();    \
+        ph[k] += (unsigned long long)(ph_n - ph_t); \
+        ph_t = ph_n;                         \
+    } while (0)
+#else
+#define PH_MARK(k) \
+    do {           \
+    } while (0)
+#endif
         unsigned steps = 0;
         const int2 rg = A.qb_range[b];
         const int qs = rg.x, qn = rg.y;
@@ -927,6 +946,7 @@ traverse_kernel(const TravArgs A) {
         }
         __syncwarp();
 
+        PH_MARK(7);
         while (cnt > 0) {
             const int nb = min(cnt, 32);
             steps++;
@@ -982,6 +1002,7 @@ traverse_kernel(const TravArgs A) {
                 est_add = 0.5 * (dl + du + WR);
             }
 
+            PH_MARK(0);
             // ---- series prunes (summation_engine.py:352-399); the evaluation
             // itself is deferred to the end of the block (it never feeds a bound)
             unsigned ser_mask = 0;
@@ -1027,6 +1048,7 @@ traverse_kernel(const TravArgs A) {
             }
             lane_est += est_add;
 
+            PH_MARK(1);
             // ---- descend or evaluate exactly (summation_engine.py:400-426)
             const bool rem = act && !fd && !((ser_mask >> lane) & 1u);
             const bool leafy = ni.z < 0 || ni.y <= H.ref_leaf;
@@ -1062,6 +1084,7 @@ traverse_kernel(const TravArgs A) {
             mass += warp_sum(settled + child_sum - (act ? WR * klo : 0.0));
             if (mass < 0.0) mass = 0.0;
 
+            PH_MARK(2);
             // ---- exhaustive base cases, eager (dito_base, :221-250).  Items whose
             // FP32 error bound fits (decided lane-parallel, one item per lane) run
             // as one FP32 batch; the rest (FP64) are staged one by one into shared
@@ -1109,6 +1132,7 @@ traverse_kernel(const TravArgs A) {
                              abs32 * tok_scale - WR);
                 audit_append(A, base_mask & ~f32_mask, 0, (int)b, (int)steps, WR, 0.0, gmin, -WR);
             }
+            PH_MARK(3);
             if (f32_direct<D>() && f32_mask) {
                 const bool mine = (f32_mask >> lane) & 1u;
                 const int rcm = mine ? ni.y : 0;
@@ -1244,6 +1268,7 @@ traverse_kernel(const TravArgs A) {
                     pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
+            PH_MARK(4);
             const unsigned base64 = base_mask & ~f32_mask;
             const unsigned small64 = __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask & ~f32_mask;
             int bi = 0;
@@ -1301,6 +1326,7 @@ traverse_kernel(const TravArgs A) {
                 c_base++;
                 c_pairs += (unsigned)(qn * rc);
             }
+            PH_MARK(5);
         }
 
         // ---- deferred series contributions, then the post pass (dito_post, :253-281)
@@ -1351,7 +1377,8 @@ traverse_kernel(const TravArgs A) {
                                                          [&](double v) { return fg_exp_fast(v, s_tab); }));
                         } else {
                             add_slot(pt_est, qi,
-                                     eval_far_fixed<D, PF>(xq, buf + A.K, buf, p, H.inv_sc));
+                                     eval_far_fixed<D, PF>(xq, buf + A.K, buf, p, H.inv_sc,
+                                                           [&](double v) { return fg_exp_fast(v, s_tab); }));
                         }
                     }
                     __syncwarp();
@@ -1396,6 +1423,7 @@ traverse_kernel(const TravArgs A) {
                 }
             }
         }
+        PH_MARK(6);
         const double node_est = warp_sum(lane_est);
 #pragma unroll
         for (int qi = 0; qi < kQPL; qi++)
@@ -1403,10 +1431,14 @@ traverse_kernel(const TravArgs A) {
         const unsigned long long cyc = (unsigned long long)(clock64() - t_start);
         if (lane == 0 && A.cost) A.cost[b] = cyc;
         if (lane == 0 && A.dbg) {
-            A.dbg[4 * b + 0] = cyc;
-            A.dbg[4 * b + 1] = steps;
-            A.dbg[4 * b + 2] = c_vis;
-            A.dbg[4 * b + 3] = (unsigned long long)__double_as_longlong(A.qb_rad[b]);
+            A.dbg[kDbgFields * b + 0] = cyc;
+            A.dbg[kDbgFields * b + 1] = steps;
+            A.dbg[kDbgFields * b + 2] = c_vis;
+            A.dbg[kDbgFields * b + 3] = (unsigned long long)__double_as_longlong(A.qb_rad[b]);
+            A.dbg[kDbgFields * b + 4] = c_f32;
+#if FG_PHASE_PROF
+            for (int k = 0; k < 8; k++) A.dbg[kDbgFields * b + 8 + k] = ph[k];
+#endif
         }
         if (lane == 0) {
             unsigned long long *cn = H.counters;

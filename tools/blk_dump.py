@@ -13,9 +13,11 @@ for j, h in enumerate(wl.bandwidths):
     os.environ["FG_DEBUG_BLOCKS"] = path
     res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon), rt, rt)
     del os.environ["FG_DEBUG_BLOCKS"]
-    a = np.fromfile(path, dtype=np.uint64).reshape(-1, 4)
+    a = np.fromfile(path, dtype=np.uint64).reshape(-1, 16)
     out[f"cyc{j}"] = a[:, 0].astype(float); out[f"vis{j}"] = a[:, 2].astype(float)
     out["rad"] = a[:, 3].view(np.float64)
+    out[f"f32_{j}"] = a[:, 4].astype(float)
+    out[f"ph{j}"] = a[:, 8:16].astype(float)
     os.remove(path)
     print(j, h, res.seconds)
 np.savez(f"gpurun_out/blk_c{c}.npz", hs=np.array(wl.bandwidths), **out)

@@ -1,7 +1,7 @@
 """Summarise FG_DEBUG_BLOCKS dumps (per query block: cycles, steps, visits, pairs)."""
 import sys
 import numpy as np
-a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 4).astype(float)
+a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 16)[:, :4].astype(float)
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else a.shape[0]
 for r in range(a.shape[0] // nb):
     blk = a[r * nb:(r + 1) * nb]
