@@ -309,11 +309,18 @@ struct TravScratch {
 };
 static TravScratch g_scr;
 
-template <int D, bool AUDIT>
+// Launches with few tasks per resident warp are tail-bound: the last tasks run
+// nearly alone, so per-warp latency (register-starved address rematerialisation,
+// serialised record chains) matters more than warps per SM.  Those launches
+// (D <= 4) use the 3-CTA instantiation (<= 168 registers): C2 sweep -4 %, but
+// C5 (~600 tasks per warp) +10 %.
+constexpr int64_t kFatTasksPerWarp = 16;
+
+template <int D, bool AUDIT, int MB>
 static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
-    // 4 resident CTAs of 128 threads per SM (<= 128 registers): measured best;
-    // capping registers lower spills and runs slower
-    auto kern = traverse_kernel<D, FG_TRAV_MINB, AUDIT>;
+    // 4 resident CTAs of 128 threads per SM (<= 128 registers): measured best
+    // for throughput; capping registers lower spills and runs slower
+    auto kern = traverse_kernel<D, MB, AUDIT>;
     // resident-grid size, cached per (kernel, shared memory size)
     static thread_local const void *c_kern = nullptr;
     static thread_local size_t c_smem = 0;
@@ -358,15 +365,25 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
 
 template <bool AUDIT>
 static int launch_dispatch_t(int D, TravArgs &A, size_t smem, int64_t nb) {
+    constexpr int M = FG_TRAV_MINB;
+    int sms = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const char *env = getenv("FG_FAT_TASKS");  // experiment knob: tasks-per-warp threshold
+    const int64_t thr = env ? atoll(env) : kFatTasksPerWarp;
+    const bool fat = !AUDIT && nb <= thr * (int64_t)sms * M * kTravWarps;
     switch (D) {
-        case 1: return launch_traverse<1, AUDIT>(A, smem, nb);
-        case 2: return launch_traverse<2, AUDIT>(A, smem, nb);
-        case 3: return launch_traverse<3, AUDIT>(A, smem, nb);
-        case 4: return launch_traverse<4, AUDIT>(A, smem, nb);
-        case 5: return launch_traverse<5, AUDIT>(A, smem, nb);
-        case 6: return launch_traverse<6, AUDIT>(A, smem, nb);
-        case 7: return launch_traverse<7, AUDIT>(A, smem, nb);
-        case 8: return launch_traverse<8, AUDIT>(A, smem, nb);
+        case 1: return fat ? launch_traverse<1, AUDIT, 3>(A, smem, nb) : launch_traverse<1, AUDIT, M>(A, smem, nb);
+        case 2: return fat ? launch_traverse<2, AUDIT, 3>(A, smem, nb) : launch_traverse<2, AUDIT, M>(A, smem, nb);
+        case 3: return fat ? launch_traverse<3, AUDIT, 3>(A, smem, nb) : launch_traverse<3, AUDIT, M>(A, smem, nb);
+        case 4: return fat ? launch_traverse<4, AUDIT, 3>(A, smem, nb) : launch_traverse<4, AUDIT, M>(A, smem, nb);
+        case 5: return launch_traverse<5, AUDIT, M>(A, smem, nb);
+        case 6: return launch_traverse<6, AUDIT, M>(A, smem, nb);
+        case 7: return launch_traverse<7, AUDIT, M>(A, smem, nb);
+        case 8: return launch_traverse<8, AUDIT, M>(A, smem, nb);
         default: return FG_EUNSUPPORTED;
     }
 }
