@@ -179,20 +179,93 @@ static void block_ranges(const TreeDev &t, std::vector<int2> &out) {
     }
 }
 
+// Block starts on the device (default mode): a block is a maximal node with
+// <= kQBlock points (a larger leaf -- duplicates -- is cut into runs); every
+// node with > kQBlock points marks its qualifying children, and a block marks
+// its run starts with the run length in a per-point array.  Blocks tile the
+// tree order, so an exclusive scan over the marks numbers them in tree order
+// (identical to the preorder walk of block_ranges).
+__global__ void block_marks_kernel(int64_t nnodes, const int4 *__restrict__ ni, int *__restrict__ len) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= nnodes) return;
+    const int4 e = ni[v];
+    auto emit = [&](const int4 c) {
+        for (int s = 0; s < c.y; s += kQBlock) len[c.x + s] = min(kQBlock, c.y - s);
+    };
+    if (v == 0 && (e.y <= kQBlock || e.z < 0)) emit(e);
+    if (e.y <= kQBlock || e.z < 0) return;
+    for (int k = 0; k < 2; k++) {
+        const int4 c = ni[k == 0 ? e.z : e.w];
+        if (c.y <= kQBlock || c.z < 0) emit(c);
+    }
+}
+
+__global__ void block_flags_kernel(int64_t n, const int *__restrict__ len, int *__restrict__ flag) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = len[i] > 0 ? 1 : 0;
+}
+
+__global__ void block_ranges_kernel(int64_t n, const int *__restrict__ len,
+                                    const int *__restrict__ idx, int2 *__restrict__ range) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && len[i] > 0) range[idx[i]] = make_int2((int)i, len[i]);
+}
+
+static int device_block_ranges(TreeDev &t, int64_t &nqb) {
+    static DBuf s_len, s_flag, s_idx, s_tmp, s_cnt;
+    const int64_t n = t.n;
+    FG_TRY(s_len.reserve(sizeof(int) * (n + 1)));
+    FG_TRY(s_flag.reserve(sizeof(int) * (n + 1)));
+    FG_TRY(s_idx.reserve(sizeof(int) * (n + 1)));
+    FG_CUDA_TRY(cudaMemsetAsync(s_len.p, 0, sizeof(int) * (n + 1), stream()));
+    count_launch();
+    block_marks_kernel<<<(unsigned)((t.nnodes + 255) / 256), 256, 0, stream()>>>(
+        t.nnodes, t.node_i.as<int4>(), s_len.as<int>());
+    count_launch();
+    block_flags_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream()>>>(n + 1, s_len.as<int>(),
+                                                                              s_flag.as<int>());
+    FG_CUDA_TRY(cudaGetLastError());
+    size_t tmp = 0;
+    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, s_flag.as<int>(), s_idx.as<int>(),
+                                              (int)(n + 1), stream()));
+    FG_TRY(s_tmp.reserve(tmp + 16));
+    count_launch();
+    FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(s_tmp.p, tmp, s_flag.as<int>(), s_idx.as<int>(),
+                                              (int)(n + 1), stream()));
+    static int *h_cnt = nullptr;
+    if (!h_cnt) FG_CUDA_TRY(cudaMallocHost(&h_cnt, sizeof(int)));
+    FG_CUDA_TRY(cudaMemcpyAsync(h_cnt, s_idx.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost,
+                                stream()));
+    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    nqb = *h_cnt;
+    FG_TRY(t.qb_range.reserve(sizeof(int2) * (nqb > 0 ? nqb : 1)));
+    count_launch();
+    block_ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
+        n, s_len.as<int>(), s_idx.as<int>(), t.qb_range.as<int2>());
+    FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
 int query_blocks(TreeDev &t) {
     if (t.qb_valid) return FG_OK;
-    std::vector<int2> ranges;
-    block_ranges(t, ranges);
-    const int64_t nqb = (int64_t)ranges.size();
+    int64_t nqb = 0;
+    if (getenv("FG_QBLOCK_MODE") || getenv("FG_QBLOCK_LIMIT")) {
+        // experiment knobs (fixed runs / smaller blocks): the host walk
+        std::vector<int2> ranges;
+        block_ranges(t, ranges);
+        nqb = (int64_t)ranges.size();
+        FG_TRY(t.qb_range.reserve(sizeof(int2) * nqb));
+        FG_CUDA_TRY(cudaMemcpyAsync(t.qb_range.p, ranges.data(), sizeof(int2) * nqb,
+                                    cudaMemcpyHostToDevice, stream()));
+    } else {
+        FG_TRY(device_block_ranges(t, nqb));
+    }
     const int D = t.dim;
-    FG_TRY(t.qb_range.reserve(sizeof(int2) * nqb));
     FG_TRY(t.qb_box.reserve(sizeof(double) * nqb * 2 * D));
     FG_TRY(t.qb_c.reserve(sizeof(double) * nqb * D));
     FG_TRY(t.qb_rad.reserve(sizeof(double) * nqb));
     FG_TRY(t.qb_wmin.reserve(sizeof(double) * nqb));
     FG_TRY(t.qb_wsum.reserve(sizeof(double) * nqb));
-    FG_CUDA_TRY(cudaMemcpyAsync(t.qb_range.p, ranges.data(), sizeof(int2) * nqb,
-                                cudaMemcpyHostToDevice, stream()));
     const unsigned blocks = (unsigned)((nqb * 32 + 255) / 256);
 #define FG_QB(DD)                                                                           \
     case DD:                                                                                \
@@ -209,12 +282,27 @@ int query_blocks(TreeDev &t) {
 #undef FG_QB
     FG_CUDA_TRY(cudaGetLastError());
     {
-        std::vector<double> rad(nqb);
-        FG_CUDA_TRY(cudaMemcpyAsync(rad.data(), t.qb_rad.p, sizeof(double) * nqb,
-                                    cudaMemcpyDeviceToHost, stream()));
+        // median block radius: device sort (radii are non-negative doubles, so
+        // their bit patterns sort like the values), one pinned read-back
+        static DBuf s_sorted, s_tmp;
+        static double *h_med = nullptr;
+        if (!h_med) FG_CUDA_TRY(cudaMallocHost(&h_med, sizeof(double)));
+        FG_TRY(s_sorted.reserve(sizeof(double) * (nqb > 0 ? nqb : 1)));
+        const auto *keys = reinterpret_cast<const unsigned long long *>(t.qb_rad.p);
+        auto *sorted = s_sorted.as<unsigned long long>();
+        size_t tmp = 0;
+        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, sorted, (int)nqb, 0, 64,
+                                                   stream()));
+        FG_TRY(s_tmp.reserve(tmp + 16));
+        count_launch();
+        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(s_tmp.p, tmp, keys, sorted, (int)nqb, 0, 64,
+                                                   stream()));
+        *h_med = 0.0;
+        if (nqb > 0)
+            FG_CUDA_TRY(cudaMemcpyAsync(h_med, s_sorted.as<double>() + nqb / 2, sizeof(double),
+                                        cudaMemcpyDeviceToHost, stream()));
         FG_CUDA_TRY(cudaStreamSynchronize(stream()));
-        std::nth_element(rad.begin(), rad.begin() + nqb / 2, rad.end());
-        t.qb_rad_median = nqb ? rad[nqb / 2] : 0.0;
+        t.qb_rad_median = *h_med;
     }
     t.nqb = nqb;
     t.qb_valid = true;

@@ -170,6 +170,25 @@ __global__ void pack_tree_kernel(int64_t n, const double *__restrict__ xf,
 }
 
 // ------------------------------------------------------------- host side
+__global__ void build_init_kernel(int4 *node_i, int *ctl, int *act0, int *nch, int *choff,
+                                  int *level_begin, int *lb_flag, int grid, int *done,
+                                  int64_t nmax, int n, int root_nch) {
+    const int i = threadIdx.x;
+    for (int k = i; k < grid; k += blockDim.x) lb_flag[k] = 0;
+    if (i < kCtl) ctl[i] = i == kNa ? 1 : i == kNchunks ? root_nch : i == kNextBase ? 1 : 0;
+    if (i == 0) {
+        node_i[0] = make_int4(0, n, -1, -1);
+        act0[0] = 0;
+        nch[0] = root_nch;
+        choff[0] = 0;
+        level_begin[0] = 0;  // level 0 = {root}, level 1 starts at id 1
+        level_begin[1] = 1;
+        // level 0's slot (the root); later slots are zeroed when allocated
+        done[0] = 0;
+        done[nmax] = 0;
+    }
+}
+
 template <int D>
 static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     const int64_t nmax = std::max<int64_t>(2 * n, 2);
@@ -205,25 +224,9 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     A.node_c = t.node_c.as<double>();
     A.node_wr = t.node_wr.as<double2>();
 
-    // level 0: the root owns every point
+    // level 0: the root owns every point (one tiny kernel instead of a string
+    // of host->device copies and memsets)
     const int root_nch = (int)((n + kChunk - 1) / kChunk);
-    struct Init {
-        int4 root;
-        int ctl[kCtl];
-    } init;
-    init.root = make_int4(0, (int)n, -1, -1);
-    for (int k = 0; k < kCtl; k++) init.ctl[k] = 0;
-    init.ctl[kNa] = 1;
-    init.ctl[kNchunks] = root_nch;
-    init.ctl[kNextBase] = 1;
-    const int zero = 0;
-    FG_CUDA_TRY(cudaMemcpyAsync(t.node_i.p, &init.root, sizeof(int4), cudaMemcpyHostToDevice, stream()));
-    FG_CUDA_TRY(cudaMemcpyAsync(B.ctl.p, init.ctl, sizeof(init.ctl), cudaMemcpyHostToDevice, stream()));
-    FG_CUDA_TRY(cudaMemcpyAsync(B.act[0].p, &zero, sizeof(int), cudaMemcpyHostToDevice, stream()));
-    FG_CUDA_TRY(cudaMemcpyAsync(B.nch.p, &root_nch, sizeof(int), cudaMemcpyHostToDevice, stream()));
-    FG_CUDA_TRY(cudaMemcpyAsync(B.choff.p, &zero, sizeof(int), cudaMemcpyHostToDevice, stream()));
-    const int lb01[2] = {0, 1};  // level 0 = {root}, level 1 starts at id 1
-    FG_CUDA_TRY(cudaMemcpyAsync(B.level_begin.p, lb01, sizeof(lb01), cudaMemcpyHostToDevice, stream()));
 
     // resident grid for the cooperative launch (cached per dimension)
     static int grid_cache[kMaxDim + 1] = {0};
@@ -242,10 +245,11 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     FG_TRY(B.lb_flag.reserve(sizeof(int) * grid));
     FG_TRY(B.lb_agg.reserve(sizeof(unsigned long long) * grid));
     FG_TRY(B.lb_incl.reserve(sizeof(unsigned long long) * grid));
-    FG_CUDA_TRY(cudaMemsetAsync(B.lb_flag.p, 0, sizeof(int) * grid, stream()));
-    // level 0's slot (the root); later slots are zeroed when they are allocated
-    FG_CUDA_TRY(cudaMemsetAsync(B.done.p, 0, sizeof(int), stream()));
-    FG_CUDA_TRY(cudaMemsetAsync(B.done.as<int>() + nmax, 0, sizeof(int), stream()));
+    count_launch();
+    build_init_kernel<<<1, 256, 0, stream()>>>(A.node_i, A.ctl, A.act[0], A.nch, A.choff,
+                                               A.level_begin, B.lb_flag.as<int>(), grid,
+                                               B.done.as<int>(), nmax, (int)n, root_nch);
+    FG_CUDA_TRY(cudaGetLastError());
     A.lb_flag = B.lb_flag.as<int>();
     A.lb_agg = B.lb_agg.as<unsigned long long>();
     A.lb_incl = B.lb_incl.as<unsigned long long>();
@@ -254,18 +258,7 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     count_launch();
     FG_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)build_coop_kernel<D>, grid,
                                             kBuildThreads, args, 0, stream()));
-    int ctl[kCtl];
-    FG_CUDA_TRY(cudaMemcpyAsync(ctl, B.ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, stream()));
-    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
-    FG_REQUIRE(!ctl[kOverflow] && ctl[kNa] == 0, FG_ECUDA, "tree build: node capacity exceeded");
-    const int levels = ctl[kLevels];
-    std::vector<int> lb(levels + 1);
-    FG_CUDA_TRY(cudaMemcpyAsync(lb.data(), B.level_begin.p, sizeof(int) * (levels + 1),
-                                cudaMemcpyDeviceToHost, stream()));
-    FG_TRY(t.level_begin_dev.reserve(sizeof(int) * (levels + 1)));
-    FG_CUDA_TRY(cudaMemcpyAsync(t.level_begin_dev.p, B.level_begin.p, sizeof(int) * (levels + 1),
-                                cudaMemcpyDeviceToDevice, stream()));
-    // final packing
+    // final packing (needs nothing from the host)
     FG_TRY(t.pw.reserve(sizeof(double) * n * packed_stride(D)));
     FG_TRY(t.perm.reserve(sizeof(int64_t) * n));
     count_launch();
@@ -273,14 +266,36 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
         n, B.xf.as<double>(), B.wf.as<double>(), B.idxf.as<int>(), t.pw.as<double>(),
         t.perm.as<int64_t>());
     FG_CUDA_TRY(cudaGetLastError());
-    double2 rootwr;
-    FG_CUDA_TRY(cudaMemcpyAsync(&rootwr, t.node_wr.p, sizeof(double2), cudaMemcpyDeviceToHost,
+    // one pinned read-back and one synchronisation: control block, validation
+    // flags, root statistics, level starts
+    struct Readback {
+        int ctl[kCtl];
+        int bad;
+        double2 rootwr;
+        int lb[kMaxLevels + 2];
+    };
+    static Readback *rb = nullptr;
+    if (!rb) FG_CUDA_TRY(cudaMallocHost(&rb, sizeof(Readback)));
+    FG_CUDA_TRY(cudaMemcpyAsync(rb->ctl, B.ctl.p, sizeof(rb->ctl), cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaMemcpyAsync(&rb->bad, B.bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    FG_CUDA_TRY(cudaMemcpyAsync(&rb->rootwr, t.node_wr.p, sizeof(double2), cudaMemcpyDeviceToHost,
+                                stream()));
+    FG_CUDA_TRY(cudaMemcpyAsync(rb->lb, B.level_begin.p, sizeof(rb->lb), cudaMemcpyDeviceToHost,
                                 stream()));
     FG_CUDA_TRY(cudaStreamSynchronize(stream()));
+    FG_REQUIRE(!(rb->bad & 1), FG_EINVAL, "weights must be positive");
+    FG_REQUIRE(!(rb->bad & 2), FG_EINVAL, "points must be finite");
+    t.fp32_ok = !(rb->bad & 4);
+    FG_REQUIRE(!rb->ctl[kOverflow] && rb->ctl[kNa] == 0, FG_ECUDA,
+               "tree build: node capacity exceeded");
+    const int levels = rb->ctl[kLevels];
+    FG_TRY(t.level_begin_dev.reserve(sizeof(int) * (levels + 1)));
+    FG_CUDA_TRY(cudaMemcpyAsync(t.level_begin_dev.p, B.level_begin.p, sizeof(int) * (levels + 1),
+                                cudaMemcpyDeviceToDevice, stream()));
     t.levels = levels;
-    t.nnodes = ctl[kNextBase];
-    t.level_begin.assign(lb.begin(), lb.end());
-    t.total_w = rootwr.x;
+    t.nnodes = rb->ctl[kNextBase];
+    t.level_begin.assign(rb->lb, rb->lb + levels + 1);
+    t.total_w = rb->rootwr.x;
     return FG_OK;
 }
 
@@ -291,7 +306,9 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_REQUIRE(leaf >= 1, FG_EINVAL, "leaf threshold must be at least 1");
     FG_REQUIRE(dim <= kMaxDim, FG_EUNSUPPORTED, "dimension > 8 is not supported by this build");
     FG_REQUIRE(n < (int64_t)1 << 30, FG_EUNSUPPORTED, "more than 2^30 points per tree");
-    BuildBufs B;
+    // build scratch is kept between builds (grow-only): a per-step tree costs
+    // no allocation calls
+    static BuildBufs B;
     const int64_t nmax = std::max<int64_t>(2 * n, 2);
     const int64_t maxchunks = n / kChunk + nmax + 2;
     for (int k = 0; k < 2; k++) {
@@ -329,18 +346,14 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
         d_points, d_weights, n, dim, B.x[0].as<double>(), B.w[0].as<double>(),
         B.idx[0].as<int>(), B.bad.as<int>());
     FG_CUDA_TRY(cudaGetLastError());
-    int bad = 0;
-    FG_CUDA_TRY(cudaMemcpyAsync(&bad, B.bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-    FG_CUDA_TRY(cudaStreamSynchronize(stream()));
-    FG_REQUIRE(!(bad & 1), FG_EINVAL, "weights must be positive");
-    FG_REQUIRE(!(bad & 2), FG_EINVAL, "points must be finite");
+    // (validation flags are read back with the build's results: invalid
+    // inputs still build a finite tree -- NaN compares false -- then raise)
     t.n = n;
     t.dim = dim;
     t.leaf = leaf;
     t.stride = packed_stride(dim);
     t.mom_valid = t.mom0_valid = false;
     t.qb_valid = false;
-    t.fp32_ok = !(bad & 4);
     t.pf_valid = false;
     t.mom_items_valid = false;
     switch (dim) {
