@@ -363,6 +363,28 @@ def test_fp32_base_cases_within_eps(fg, oracle, D, offset, wspan):
         _fp32_base(True)
 
 
+@pytest.mark.parametrize("D", [5, 7])
+def test_direct_fp32_stream_dot_form_and_large_items(fg, oracle, D):
+    """D >= 5 streams FP32 records converted from the FP64 points (DESIGN.md
+    "Direct stream", "Dot form"), with base items of up to 256 points at
+    bandwidths of the order of the block radius: every run of a sweep from far
+    below to far above the block radius stays within eps of the exhaustive sum,
+    with FP32 pairs in play, far from the origin too."""
+    rng = np.random.default_rng(70 + D)
+    n = 8000
+    pts = rng.standard_t(3.0, (n, D)) * rng.uniform(0.5, 2.0, D) + 1e3
+    w = rng.uniform(0.5, 1.5, n)
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    hs = [0.05, 0.3, 1.0, 3.0]
+    for eps in (0.01, 1e-4):
+        res = fg.sweep_run(fg.RunConfig(bandwidth=hs[0], epsilon=eps), t, t, hs)
+        for h, r in zip(hs, res):
+            exact = oracle.naive_sum(pts, pts, w, h, threads=0)
+            assert oracle.max_rel_error(r.values, exact) <= eps, (h, eps)
+        if eps == 0.01:
+            assert sum(r.counters.fp32_pairs for r in res[1:]) > 0
+
+
 def test_fp32_base_cases_off_outside_fp32_range(fg, oracle):
     """Weights outside the FP32 base case's safe range fall back to FP64."""
     rng = np.random.default_rng(5)
