@@ -153,6 +153,10 @@ struct TreeDev {
     bool fp32_ok = true;  // coordinates and weights fit the FP32 base case's range
     // FP32 records for the traversal's FP32 base case (fp32_pack, fg_traverse.cu)
     bool pf_valid = false;
+    // per node (|weighted mean offset from the centre|, weighted mean squared
+    // offset): the traversal's Jensen mass bound (node_stats_js, fg_traverse.cu)
+    bool js_valid = false;
+    DBuf node_js;
     DBuf pf;      // float n x fstride: coords about the anchor centre, then weight
     DBuf anchor;  // int n: the point's maximal node with <= 32 points (BFS id)
     int64_t nqb = 0;
@@ -184,6 +188,8 @@ int tree_export(const TreeDev &t, int64_t *perm, int64_t *start, int64_t *end, d
                 double *hi, double *center, double *weight, double *inf_radius,
                 int64_t *left, int64_t *right);
 int moments_refresh(TreeDev &t, double h, int plimit);
+int mom_items(TreeDev &t);  // (node, chunk) work items, shared with node_js
+int node_js(TreeDev &t);    // Jensen statistics per node (fg_moments.cu)
 int moments_multi(TreeDev &t, const double *hs, int nh, int plimit, DBuf &dst);
 int moments_export(const TreeDev &t, double *out);
 int query_blocks(TreeDev &t);

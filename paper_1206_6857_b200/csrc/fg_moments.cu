@@ -181,7 +181,7 @@ mom_combine_kernel(const int *__restrict__ off, const double *__restrict__ parti
 }
 
 // items of a tree (bandwidth-independent, built once per tree)
-static int mom_items(TreeDev &t) {
+int mom_items(TreeDev &t) {
     if (t.mom_items_valid) return FG_OK;
     const int64_t nn = t.nnodes;
     FG_TRY(t.mom_off.reserve(sizeof(int) * (nn + 1)));
@@ -241,6 +241,110 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     mom_combine_kernel<<<(unsigned)nn, 256, 0, stream()>>>(
         t.mom_off.as<int>(), s_partial.as<double>(), K, T.inv_fact.as<double>(), dst.as<double>());
     FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
+// ---- Jensen node statistics (the traversal's mass bound, entry_bounds) ----
+// Per (node, chunk) item: sum w, sum w u_d, sum w |u|^2 with u = r - c (c the
+// node's centre); a warp per node then adds its items' partials (lanes strided
+// over the items, a fixed-order warp reduction: deterministic) and stores
+// (|m|, s2) = (|sum w u| / W, sum w |u|^2 / W).
+template <int D>
+__global__ void js_partial_kernel(int nitems, const int2 *__restrict__ items,
+                                  const int4 *__restrict__ node_i, const double *__restrict__ node_c,
+                                  const double *__restrict__ pw, double *__restrict__ partial) {
+    constexpr int S = packed_stride(D);
+    const int lane = threadIdx.x & 31;
+    const int it = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (it >= nitems) return;
+    const int2 item = items[it];
+    const int4 ni = node_i[item.x];
+    double c[D], m[D], ws = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        c[d] = node_c[(int64_t)item.x * D + d];
+        m[d] = 0.0;
+    }
+    const int b = ni.x + item.y * kMomChunk, e = min(b + kMomChunk, ni.x + ni.y);
+    for (int i = b + lane; i < e; i += 32) {
+        double y[D], w;
+        load_point_w<D>(pw + (int64_t)i * S, y, w);
+        ws += w;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const double u = y[d] - c[d];
+            m[d] = fma(w, u, m[d]);
+            s2 = fma(w * u, u, s2);
+        }
+    }
+    ws = warp_sum(ws);
+    s2 = warp_sum(s2);
+#pragma unroll
+    for (int d = 0; d < D; d++) m[d] = warp_sum(m[d]);
+    if (lane == 0) {
+        double *o = partial + (int64_t)it * (D + 2);
+        o[0] = ws;
+        o[1] = s2;
+#pragma unroll
+        for (int d = 0; d < D; d++) o[2 + d] = m[d];
+    }
+}
+
+template <int D>
+__global__ void js_combine_kernel(int64_t nn, const int *__restrict__ off,
+                                  const double *__restrict__ partial, double2 *__restrict__ js) {
+    const int lane = threadIdx.x & 31;
+    const int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (v >= nn) return;
+    double a[D + 2];
+#pragma unroll
+    for (int k = 0; k < D + 2; k++) a[k] = 0.0;
+    for (int it = off[v] + lane; it < off[v + 1]; it += 32)
+#pragma unroll
+        for (int k = 0; k < D + 2; k++) a[k] += partial[(int64_t)it * (D + 2) + k];
+#pragma unroll
+    for (int k = 0; k < D + 2; k++) a[k] = warp_sum(a[k]);
+    double mm = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double md = a[2 + d] / a[0];
+        mm = fma(md, md, mm);
+    }
+    if (lane == 0) js[v] = make_double2(sqrt(mm), a[1] / a[0]);
+}
+
+template <int D>
+static int node_js_t(TreeDev &t) {
+    FG_TRY(mom_items(t));
+    static DBuf s_part;
+    FG_TRY(s_part.reserve(sizeof(double) * (size_t)std::max(t.mom_nitems, 1) * (D + 2)));
+    FG_TRY(t.node_js.reserve(sizeof(double2) * t.nnodes));
+    count_launch();
+    js_partial_kernel<D><<<(unsigned)(((int64_t)t.mom_nitems * 32 + 255) / 256), 256, 0, stream()>>>(
+        t.mom_nitems, t.mom_items.as<int2>(), t.node_i.as<int4>(), t.node_c.as<double>(),
+        t.pw.as<double>(), s_part.as<double>());
+    count_launch();
+    js_combine_kernel<D><<<(unsigned)((t.nnodes * 32 + 255) / 256), 256, 0, stream()>>>(
+        t.nnodes, t.mom_off.as<int>(), s_part.as<double>(), t.node_js.as<double2>());
+    FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
+int node_js(TreeDev &t) {
+    if (t.js_valid) return FG_OK;
+    int st;
+    switch (t.dim) {
+        case 1: st = node_js_t<1>(t); break;
+        case 2: st = node_js_t<2>(t); break;
+        case 3: st = node_js_t<3>(t); break;
+        case 4: st = node_js_t<4>(t); break;
+        case 5: st = node_js_t<5>(t); break;
+        case 6: st = node_js_t<6>(t); break;
+        case 7: st = node_js_t<7>(t); break;
+        default: st = node_js_t<8>(t); break;
+    }
+    FG_TRY(st);
+    t.js_valid = true;
     return FG_OK;
 }
 

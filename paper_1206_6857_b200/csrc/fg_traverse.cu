@@ -506,6 +506,10 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     A.r_box = r.node_box.as<double>();
     A.r_c = r.node_c.as<double>();
     A.r_wr = r.node_wr.as<double2>();
+    if (!getenv("FG_NO_JENSEN")) {  // experiment knob: K_lo-only mass bounds
+        FG_TRY(node_js(r));
+        A.r_js = r.node_js.as<double2>();
+    }
     A.q_pw = q.pw.as<double>();
     A.qb_range = q.qb_range.as<int2>();
     A.qb_box = q.qb_box.as<double>();

@@ -60,6 +60,7 @@ struct TravArgs {
     const double *r_box;
     const double *r_c;
     const double2 *r_wr;
+    const double2 *r_js;  // per node: |weighted mean offset from the centre|, weighted mean |r - c|^2
     int mom_K;
     // query blocks
     const double *q_pw;
@@ -156,14 +157,21 @@ __device__ __forceinline__ double required_tokens(double wr, double err, double 
 }
 
 // Box bounds of (query block box in shared memory, reference node) and both
-// kernel bounds (summation_engine.py:315-328).
+// kernel bounds (summation_engine.py:315-328), plus lb: the mass lower bound
+// per unit weight used for G_min, max(K_lo, Jensen's bound).  Jensen: with the
+// node's weights as probabilities, sum_r w_r K(x - r) >= W_R exp(-E|x - r|^2
+// / 2h^2), and E|x - r|^2 = |x - c|^2 - 2 (x - c).m + s2 <= (|x - c| + |m|)^2
+// - |m|^2 + s2 (c the node's centre, m the weighted mean offset from it, s2
+// the weighted mean squared offset; node_js = (|m|, s2)) -- far tighter than
+// K_lo (the farthest pair) for a wide node, so G_min, the token budget and
+// the prunes it admits grow (Theorem 2 needs only a valid lower bound).
 template <int D>
 __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq, int node,
-                                             double neg_inv, double &klo, double &khi, double &mn,
+                                             double neg_inv, double &klo, double &khi, double &lb,
                                              const double *s_tab) {
     const double *rbox = A.r_box + (int64_t)node * 2 * D;
-    double mx = 0.0;
-    mn = 0.0;
+    const double *rc = A.r_c + (int64_t)node * D;
+    double mx = 0.0, mn = 0.0, dq = 0.0;
 #pragma unroll
     for (int d = 0; d < D; d++) {
         const double qlo = sq[d], qhi = sq[D + d];
@@ -174,9 +182,21 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
         const double s1 = qhi - rlo, s2 = rhi - qlo;
         const double s = s1 > s2 ? s1 : s2;
         mx += s * s;
+        const double c = __ldg(rc + d);
+        const double e = fmax(fabs(qlo - c), fabs(qhi - c));
+        dq += e * e;
     }
     khi = fg_exp_fast(mn * neg_inv, s_tab);
     klo = fg_exp_fast(mx * neg_inv, s_tab);
+    lb = klo;
+    if (A.r_js) {
+        const double2 js = __ldg(A.r_js + node);
+        const double r = sqrt(dq) * (1.0 + 0x1.0p-50) + js.x;
+        // (1 + 2^-40) covers the roundings of the squared distances, the
+        // square root and the stored statistics (all <= ~2^-50 relative)
+        const double ex = (r * r - js.x * js.x + js.y) * (1.0 + 0x1.0p-40);
+        if (ex < mx) lb = fmax(klo, fg_exp_fast(ex * neg_inv, s_tab) * (1.0 - 0x1.0p-40));
+    }
 }
 
 // Exact contribution of reference points [rs, rs+rc) to this lane's query
@@ -830,7 +850,7 @@ traverse_kernel(const TravArgs A) {
     int *sn = A.st_node + gw * A.stack_cap;
     double *skl = A.st_f + gw * A.stack_cap * 3;
     double *skh = skl + A.stack_cap;
-    double *smn = skh + A.stack_cap;
+    double *slb = skh + A.stack_cap;  // mass lower bound per unit weight (entry_bounds' lb)
     int2 *sl = A.ser_list + gw * A.stack_cap;
     const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -934,15 +954,15 @@ traverse_kernel(const TravArgs A) {
         int head = 0, cnt = 1;
         const int cap = A.stack_cap;
         {
-            double klo, khi, mn;
-            entry_bounds<D>(A, sq, 0, H.neg_inv, klo, khi, mn, s_tab);
+            double klo, khi, lb;
+            entry_bounds<D>(A, sq, 0, H.neg_inv, klo, khi, lb, s_tab);
             if (lane == 0) {
                 sn[0] = 0;
                 skl[0] = klo;
                 skh[0] = khi;
-                smn[0] = mn;
+                slb[0] = lb;
             }
-            mass = A.r_wr[0].x * klo;
+            mass = A.r_wr[0].x * lb;
         }
         __syncwarp();
 
@@ -961,7 +981,7 @@ traverse_kernel(const TravArgs A) {
             cnt -= nb;
             const bool act = lane < nb;
             int node = 0;
-            double klo = 0.0, khi = 0.0, mn = 0.0;
+            double klo = 0.0, khi = 0.0, lb = 0.0;
             int4 ni = make_int4(0, 0, -1, -1);
             double2 wr = make_double2(0.0, 0.0);
             if (act) {
@@ -970,7 +990,7 @@ traverse_kernel(const TravArgs A) {
                 node = sn[slot];
                 klo = skl[slot];
                 khi = skh[slot];
-                mn = smn[slot];
+                lb = slb[slot];
                 ni = A.r_ni[node];
                 wr = A.r_wr[node];
             }
@@ -998,7 +1018,7 @@ traverse_kernel(const TravArgs A) {
             double settled = 0.0, est_add = 0.0;
             if (fd) {
                 const double dl = WR * klo, du = WR * khi - WR;
-                settled = dl;
+                settled = WR * lb;  // (>= dl = W_R K_lo)
                 est_add = 0.5 * (dl + du + WR);
             }
 
@@ -1038,7 +1058,7 @@ traverse_kernel(const TravArgs A) {
                 const unsigned hm = __ballot_sync(kFull, ((ser_mask >> lane) & 1u) && meth == 2);
                 const unsigned om = ser_mask & ~hm;
                 if ((ser_mask >> lane) & 1u) {
-                    settled = WR * klo;
+                    settled = WR * lb;
                     const int slot = meth == 2 ? nh + __popc(hm & lt_mask)
                                                : A.stack_cap - 1 - no - __popc(om & lt_mask);
                     sl[slot] = make_int2(node, p | (meth << 8));
@@ -1073,15 +1093,15 @@ traverse_kernel(const TravArgs A) {
                     sn[slot] = ch;
                     skl[slot] = cl;
                     skh[slot] = chh;
-                    smn[slot] = cm;
-                    child_sum += A.r_wr[ch].x * cl;
+                    slb[slot] = cm;
+                    child_sum += A.r_wr[ch].x * cm;
                 }
             }
             cnt += 2 * __popc(split_mask);
             // one reduction per step: popped entries leave the frontier, settled
             // ones and pushed children enter the mass bound (base cases move
             // into the per-point exact sums)
-            mass += warp_sum(settled + child_sum - (act ? WR * klo : 0.0));
+            mass += warp_sum(settled + child_sum - (act ? WR * lb : 0.0));
             if (mass < 0.0) mass = 0.0;
 
             PH_MARK(2);

@@ -355,6 +355,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     t.mom_valid = t.mom0_valid = false;
     t.qb_valid = false;
     t.pf_valid = false;
+    t.js_valid = false;
     t.mom_items_valid = false;
     switch (dim) {
         case 1: return build_levels<1>(n, leaf, B, t);
