@@ -195,7 +195,7 @@ __device__ __forceinline__ void entry_bounds(const TravArgs &A, const double *sq
         // (1 + 2^-40) covers the roundings of the squared distances, the
         // square root and the stored statistics (all <= ~2^-50 relative)
         const double ex = (r * r - js.x * js.x + js.y) * (1.0 + 0x1.0p-40);
-        if (ex < mx) lb = fmax(klo, fg_exp_fast(ex * neg_inv, s_tab) * (1.0 - 0x1.0p-40));
+        if (ex < mx) lb = fmin(khi, fmax(klo, fg_exp_fast(ex * neg_inv, s_tab) * (1.0 - 0x1.0p-40)));
     }
 }
 
@@ -1002,7 +1002,9 @@ traverse_kernel(const TravArgs A) {
             const double gmin = fmax((pmin + mass) * kMassSafety, gfloor);
 
             // ---- finite-difference prune (summation_engine.py:327-351)
-            const double fd_err = 0.5 * WR * (khi - klo);
+            // finite difference over [lb, K_hi] (lb >= K_lo: the Jensen bound of
+            // entry_bounds; every query's contribution lies in W_R [lb, K_hi])
+            const double fd_err = 0.5 * WR * (khi - lb);
             // W / (eps G_min): one uniform division per step instead of one per entry
             const double den = H.eps * gmin;
             const double tok_scale = den > 0.0 ? A.total_w / den : CUDART_INF;
@@ -1017,9 +1019,8 @@ traverse_kernel(const TravArgs A) {
                 audit_append(A, fd_mask, 1, (int)b, (int)steps, WR, fd_err, gmin, req);
             double settled = 0.0, est_add = 0.0;
             if (fd) {
-                const double dl = WR * klo, du = WR * khi - WR;
-                settled = WR * lb;  // (>= dl = W_R K_lo)
-                est_add = 0.5 * (dl + du + WR);
+                settled = WR * lb;
+                est_add = 0.5 * WR * (lb + khi);
             }
 
             PH_MARK(0);
