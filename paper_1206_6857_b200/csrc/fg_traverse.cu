@@ -282,8 +282,10 @@ int query_blocks(TreeDev &t) {
 #undef FG_QB
     FG_CUDA_TRY(cudaGetLastError());
     {
-        // median block radius: device sort (radii are non-negative doubles, so
-        // their bit patterns sort like the values), one pinned read-back
+        // median block radius: device sort on the high 32 bits (radii are
+        // non-negative doubles, so their bit patterns sort like the values; the
+        // low bits only reorder radii within 2^-20 of each other -- the median
+        // drives heuristics only), one pinned read-back
         static DBuf s_sorted, s_tmp;
         static double *h_med = nullptr;
         if (!h_med) FG_CUDA_TRY(cudaMallocHost(&h_med, sizeof(double)));
@@ -291,11 +293,11 @@ int query_blocks(TreeDev &t) {
         const auto *keys = reinterpret_cast<const unsigned long long *>(t.qb_rad.p);
         auto *sorted = s_sorted.as<unsigned long long>();
         size_t tmp = 0;
-        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, sorted, (int)nqb, 0, 64,
+        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, sorted, (int)nqb, 32, 64,
                                                    stream()));
         FG_TRY(s_tmp.reserve(tmp + 16));
         count_launch();
-        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(s_tmp.p, tmp, keys, sorted, (int)nqb, 0, 64,
+        FG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(s_tmp.p, tmp, keys, sorted, (int)nqb, 32, 64,
                                                    stream()));
         *h_med = 0.0;
         if (nqb > 0)
