@@ -369,10 +369,19 @@ constexpr int f32_fd() { return (D + 3) & ~3; }
 // per-warp shared memory of the batch, in doubles: CAP AoS records of
 // fstride floats, then the item table (32 x {offset, count, offset vector})
 // D >= 5 streams FP32 records converted from the FP64 points instead (see
-// "Direct FP32 stream" below): one window of kF32Win converted records
+// "Direct FP32 stream" below): one window of f32_win converted records
 template <int D>
 constexpr bool f32_direct() { return D >= 5; }
-constexpr int kF32Win = kAnchorMax;
+// FP64 staging buffer in records: two kAnchorMax buffers (double-buffered FP64
+// items) at D <= 4; one at D >= 5, where the query coordinates take the
+// shared memory instead (registers are the scarcer resource there)
+template <int D>
+constexpr int stage_recs() { return D <= 5 ? 2 * kAnchorMax : kAnchorMax; }
+template <int D>
+constexpr bool stage_db() { return stage_recs<D>() >= 2 * kAnchorMax; }
+// records per direct-stream window (two windows fill the staging buffer)
+template <int D>
+constexpr int f32_win() { return stage_recs<D>() / 2; }
 #ifndef FG_DOT_FORM
 #define FG_DOT_FORM 1
 #endif
@@ -382,7 +391,7 @@ template <int D>
 constexpr int dstride() { return (D + 2 + 3) & ~3; }
 template <int D>
 constexpr int f32_smem_doubles() {
-    return f32_direct<D>() ? kF32Win * dstride<D>() / 2
+    return f32_direct<D>() ? f32_win<D>() * dstride<D>() / 2
                            : (f32_cap<D>() * fstride<D>() + 32 * (2 + f32_fd<D>())) / 2;
 }
 
@@ -392,12 +401,12 @@ constexpr int f32_smem_doubles() {
 // rather than in registers: the traversal kernel is register-bound, and the
 // FP32 batch loop is scheduled tighter with the 4D registers back.
 template <int D>
-constexpr bool xs_smem() { return D <= 4; }
+constexpr bool xs_smem() { return true; }
 template <int D>
 constexpr int xs_doubles() { return xs_smem<D>() ? kQBlock * D : 0; }
 template <int D>
 constexpr int warp_fixed_doubles() {
-    return ((3 * D + 1) & ~1) + 2 * kAnchorMax * packed_stride(D) + f32_smem_doubles<D>() +
+    return ((3 * D + 1) & ~1) + stage_recs<D>() * packed_stride(D) + f32_smem_doubles<D>() +
            xs_doubles<D>();
 }
 
@@ -680,22 +689,22 @@ __device__ __forceinline__ void window_f32(const unsigned long long (&xf2)[D], c
            ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
 }
 
-// cp.async the FP64 points of stream window [w0, w0 + kF32Win) into `dst`:
+// cp.async the FP64 points of stream window [w0, w0 + f32_win) into `dst`:
 // item t of the stream (lanes of `items`, in lane order) covers stream
 // positions [off, off + cnt) and tree positions [start, start + cnt).
 template <int D>
 __device__ __forceinline__ void stage_window(const double *__restrict__ pw, unsigned items, int off,
                                              int cnt, int start, int w0, double *dst) {
-    constexpr int S = packed_stride(D);
+    constexpr int S = packed_stride(D), W = f32_win<D>();
     const int lane = threadIdx.x & 31;
-    const unsigned ov = __ballot_sync(kFull, ((items >> lane) & 1u) && off < w0 + kF32Win &&
+    const unsigned ov = __ballot_sync(kFull, ((items >> lane) & 1u) && off < w0 + W &&
                                                  off + cnt > w0);
     for (unsigned m = ov; m; m &= m - 1) {
         const int i = __ffs(m) - 1;
         const int o = __shfl_sync(kFull, off, i);
         const int c = __shfl_sync(kFull, cnt, i);
         const int st = __shfl_sync(kFull, start, i);
-        const int p0 = max(o, w0), p1 = min(o + c, w0 + kF32Win);
+        const int p0 = max(o, w0), p1 = min(o + c, w0 + W);
         for (int p = p0 + lane; p < p1; p += 32) {
             const double *src = pw + (int64_t)(st + p - o) * S;
             double *d = dst + (p - w0) * S;
@@ -841,7 +850,7 @@ traverse_kernel(const TravArgs A) {
     double *sq = smem + wib * (warp_fixed_doubles<D>() + ((A.K + 1) & ~1));
     double *sqc = sq + 2 * D;
     double *sbuf = sq + ((3 * D + 1) & ~1);
-    float *fst = reinterpret_cast<float *>(sbuf + 2 * kAnchorMax * S);
+    float *fst = reinterpret_cast<float *>(sbuf + stage_recs<D>() * S);
     int *itab = reinterpret_cast<int *>(fst + f32_cap<D>() * fstride<D>());  // offsets, counts
     float *idl = reinterpret_cast<float *>(itab + 64);                       // 32 x FD
     double *loc = sq + warp_fixed_doubles<D>();
@@ -1190,23 +1199,24 @@ traverse_kernel(const TravArgs A) {
                 }
                 double sum32[kQPL] = {0.0, 0.0};
                 int wb = 0;
-                for (int w0 = 0; w0 < total; w0 += kF32Win) {
+                constexpr int W = f32_win<D>();
+                for (int w0 = 0; w0 < total; w0 += W) {
                     // the next window's copy overlaps this window's conversion + math
-                    if (w0 + kF32Win < total)
-                        stage_window<D>(A.r_pw, f32_mask, off, rcm, ni.x, w0 + kF32Win,
-                                        sbuf + (wb ^ 1) * kF32Win * S);
+                    if (w0 + W < total)
+                        stage_window<D>(A.r_pw, f32_mask, off, rcm, ni.x, w0 + W,
+                                        sbuf + (wb ^ 1) * W * S);
                     else
                         __pipeline_commit();
                     __pipeline_wait_prior(1);
                     __syncwarp();
-                    const int n = min(kF32Win, total - w0), n4 = (n + 3) & ~3;
+                    const int n = min(W, total - w0), n4 = (n + 3) & ~3;
                     double s0, s1;
                     if (dot_step) {
-                        convert_window_dot<D>(sbuf + wb * kF32Win * S, n, n4, sqc, sdot, fst);
+                        convert_window_dot<D>(sbuf + wb * W * S, n, n4, sqc, sdot, fst);
                         __syncwarp();
                         window_dot<D>(xf2, aq2, fst, n4, s0, s1);
                     } else {
-                        convert_window<D>(sbuf + wb * kF32Win * S, n, n4, sqc, fst);
+                        convert_window<D>(sbuf + wb * W * S, n, n4, sqc, fst);
                         __syncwarp();
                         window_f32<D>(xf2, fst, n4, s2, s0, s1);
                     }
@@ -1305,7 +1315,7 @@ traverse_kernel(const TravArgs A) {
                 double contrib[kQPL] = {0.0, 0.0};
                 if ((small64 >> i) & 1u) {
                     const unsigned rest = small64 & ~((2u << i) - 1u);
-                    if (rest) {
+                    if (stage_db<D>() && rest) {
                         stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1,
                                         sbuf + (bi ^ 1) * kAnchorMax * S);
                         __pipeline_wait_prior(1);
@@ -1326,7 +1336,11 @@ traverse_kernel(const TravArgs A) {
                                                      : base_case<D, true>(x[0], bp, rc, H.neg_inv, s_tab);
                     }
                     __syncwarp();
-                    bi ^= 1;
+                    if constexpr (stage_db<D>()) {
+                        bi ^= 1;
+                    } else if (rest) {  // single buffer: stage the next item now
+                        stage_points<D>(A.r_pw, ni.x, ni.y, __ffs(rest) - 1, sbuf);
+                    }
                 } else {
                     const double *rp = A.r_pw + (int64_t)rs * S;
                     double x[kQPL][D];
@@ -1365,7 +1379,7 @@ traverse_kernel(const TravArgs A) {
             constexpr int PF = default_plimit_c(D);
             constexpr int kRing = 4;
             const int slot = (A.K + D + 1) & ~1;
-            const bool ring = A.plimit == PF && kRing * slot <= 2 * kAnchorMax * S;
+            const bool ring = A.plimit == PF && kRing * slot <= stage_recs<D>() * S;
             auto stage_item = [&](int k) {
                 const int node = sl[k].x;
                 double *dst = sbuf + (k % kRing) * slot;
