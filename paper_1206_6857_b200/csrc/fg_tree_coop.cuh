@@ -494,19 +494,43 @@ build_coop_kernel(const BuildArgs B) {
             int *idxn = B.idx[cur ^ 1];
             const unsigned lt = (1u << lane) - 1u;
             int nl = 0, nr = 0;
+            // the next round's point is loaded while this round is scattered
+            double yc[D], wc = 0.0;
+            int ic = 0;
+            if (cb + lane < ce) {
+#pragma unroll
+                for (int d = 0; d < D; d++) yc[d] = x[(int64_t)d * n + cb + lane];
+                wc = w[cb + lane];
+                ic = idx[cb + lane];
+            }
             for (int base = cb; base < ce; base += 32) {
                 const int i = base + lane;
                 const bool in = i < ce;
-                const bool goes_left = in && x[(int64_t)sd * n + i] < mid;
+                double yv[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) yv[d] = yc[d];
+                const double wv = wc;
+                const int iv = ic;
+                if (i + 32 < ce) {
+#pragma unroll
+                    for (int d = 0; d < D; d++) yc[d] = x[(int64_t)d * n + i + 32];
+                    wc = w[i + 32];
+                    ic = idx[i + 32];
+                }
+                double xs = yv[0];
+#pragma unroll
+                for (int d = 0; d < D; d++)
+                    if (d == sd) xs = yv[d];
+                const bool goes_left = in && xs < mid;
                 const unsigned lm = __ballot_sync(kFull, goes_left);
                 const unsigned rm = __ballot_sync(kFull, in && !goes_left);
                 if (in) {
                     const int dst = goes_left ? left_base + nl + __popc(lm & lt)
                                               : right_base + nr + __popc(rm & lt);
 #pragma unroll
-                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = x[(int64_t)d * n + i];
-                    wn[dst] = w[i];
-                    idxn[dst] = idx[i];
+                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = yv[d];
+                    wn[dst] = wv;
+                    idxn[dst] = iv;
                 }
                 nl += __popc(lm);
                 nr += __popc(rm);
