@@ -77,6 +77,7 @@ __device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int le
                 hi[d] = -CUDART_INF;
                 sm[d] = 0.0;
             }
+            #pragma unroll 4
             for (int i = b + lane; i < e; i += 32) {
 #pragma unroll
                 for (int d = 0; d < D; d++) {
@@ -106,6 +107,7 @@ __device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int le
             const double mid = 0.5 * (lo[sd] + hi[sd]);
             double rad = 0.0;
             int cnt = 0;
+            #pragma unroll 4
             for (int i = b + lane; i < e; i += 32) {
 #pragma unroll
                 for (int d = 0; d < D; d++) rad = fmax(rad, fabs(x[(int64_t)d * n + i] - ctr[d]));
@@ -126,7 +128,8 @@ __device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int le
             }
             if (lane == 0) B.node_wr[node] = make_double2(ws, rad);
             if (!split) {
-                for (int i = b + lane; i < e; i += 32) {
+                #pragma unroll 4
+            for (int i = b + lane; i < e; i += 32) {
 #pragma unroll
                     for (int d = 0; d < D; d++) B.xf[(int64_t)d * n + i] = x[(int64_t)d * n + i];
                     B.wf[i] = w[i];
@@ -134,20 +137,44 @@ __device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int le
                 }
                 continue;
             }
-            // stable warp partition, 32 points per round, in order
+            // stable warp partition, 32 points per round, in order; the next
+            // round's point is loaded while this round is scattered
             int cl = 0, cr = 0;
+            double yc[D], wc = 0.0;
+            int ic = 0;
+            if (b + lane < e) {
+#pragma unroll
+                for (int d = 0; d < D; d++) yc[d] = x[(int64_t)d * n + b + lane];
+                wc = w[b + lane];
+                ic = idx[b + lane];
+            }
             for (int base = b; base < e; base += 32) {
                 const int i = base + lane;
                 const bool in = i < e;
-                const bool goes_left = in && x[(int64_t)sd * n + i] < mid;
+                double yv[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) yv[d] = yc[d];
+                const double wv = wc;
+                const int iv = ic;
+                if (i + 32 < e) {
+#pragma unroll
+                    for (int d = 0; d < D; d++) yc[d] = x[(int64_t)d * n + i + 32];
+                    wc = w[i + 32];
+                    ic = idx[i + 32];
+                }
+                double xs = yv[0];
+#pragma unroll
+                for (int d = 0; d < D; d++)
+                    if (d == sd) xs = yv[d];
+                const bool goes_left = in && xs < mid;
                 const unsigned lm = __ballot_sync(kFull, goes_left);
                 const unsigned rm = __ballot_sync(kFull, in && !goes_left);
                 if (in) {
                     const int dst = goes_left ? b + cl + __popc(lm & lt) : b + nl + cr + __popc(rm & lt);
 #pragma unroll
-                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = x[(int64_t)d * n + i];
-                    wn[dst] = w[i];
-                    idxn[dst] = idx[i];
+                    for (int d = 0; d < D; d++) xn[(int64_t)d * n + dst] = yv[d];
+                    wn[dst] = wv;
+                    idxn[dst] = iv;
                 }
                 cl += __popc(lm);
                 cr += __popc(rm);
@@ -231,6 +258,7 @@ build_coop_kernel(const BuildArgs B) {
                 hi[d] = -CUDART_INF;
                 sm[d] = 0.0;
             }
+            #pragma unroll 4
             for (int i = cb + lane; i < ce; i += 32) {
 #pragma unroll
                 for (int d = 0; d < D; d++) {
@@ -328,6 +356,7 @@ build_coop_kernel(const BuildArgs B) {
             for (int d = 0; d < D; d++) ctr[d] = B.node_c[(int64_t)node * D + d];
             double rad = 0.0;
             int cnt = 0;
+            #pragma unroll 4
             for (int i = cb + lane; i < ce; i += 32) {
 #pragma unroll
                 for (int d = 0; d < D; d++) rad = fmax(rad, fabs(x[(int64_t)d * n + i] - ctr[d]));
@@ -477,7 +506,8 @@ build_coop_kernel(const BuildArgs B) {
             const int ce = min(cb + kChunk, ni.x + ni.y);
             const int sd = B.split_dim[s];
             if (sd < 0) {
-                for (int i = cb + lane; i < ce; i += 32) {
+                #pragma unroll 4
+            for (int i = cb + lane; i < ce; i += 32) {
 #pragma unroll
                     for (int d = 0; d < D; d++) B.xf[(int64_t)d * n + i] = x[(int64_t)d * n + i];
                     B.wf[i] = w[i];
