@@ -43,7 +43,7 @@ __global__ void moments_rescale_kernel(int64_t total, int K, const double *__res
 // No level-by-level dependency: two launches for the whole tree.
 constexpr int kMomChunk = 256;
 constexpr int kMomWarps = 8;
-constexpr int kMomKPL = kMaxK / 32;  // coefficients per lane
+constexpr int kMomKPLMax = kMaxK / 32;  // coefficients per lane (largest K)
 
 __global__ void mom_items_count_kernel(int64_t nn, const int4 *__restrict__ node_i,
                                        int *__restrict__ cnt) {
@@ -59,7 +59,10 @@ __global__ void mom_items_fill_kernel(int64_t nn, const int4 *__restrict__ node_
     for (int j = 0; j < c; j++) items[off[v] + j] = make_int2((int)v, j);
 }
 
-template <int D>
+// KPL: coefficient slots per lane, ceil(K / 32) rounded up to a power of two
+// (a kernel sized for the expansion at hand keeps its registers -- and so its
+// occupancy -- to what K needs)
+template <int D, int kMomKPL>
 __global__ void __launch_bounds__(32 * kMomWarps)
 mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__restrict__ node_i,
                    const double *__restrict__ node_c, const double *__restrict__ pw, int p,
@@ -217,9 +220,14 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     static DBuf s_partial;
     FG_TRY(s_partial.reserve(sizeof(double) * (size_t)t.mom_nitems * K));
     const size_t smem = sizeof(double) * 32 * D * kMaxOrder * kMomWarps;
-    auto kern = mom_partial_kernel<D>;
-    static int c_grid[kMaxDim + 1] = {0};
-    if (!c_grid[D]) {
+    const int kpl = (K + 31) / 32;
+    auto kern = kpl <= 1 ? mom_partial_kernel<D, 1>
+                : kpl <= 2 ? mom_partial_kernel<D, 2>
+                : kpl <= 4 ? mom_partial_kernel<D, 4>
+                           : mom_partial_kernel<D, kMomKPLMax>;
+    const int ki = kpl <= 1 ? 0 : kpl <= 2 ? 1 : kpl <= 4 ? 2 : 3;
+    static int c_grid[kMaxDim + 1][4] = {};
+    if (!c_grid[D][ki]) {
         int dev = 0, sms = 0, occ = 0;
         FG_CUDA_TRY(cudaGetDevice(&dev));
         FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -227,9 +235,9 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
             FG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem));
         FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kMomWarps, smem));
-        c_grid[D] = sms * std::max(occ, 1);
+        c_grid[D][ki] = sms * std::max(occ, 1);
     }
-    const int grid = std::max(1, std::min(c_grid[D], (t.mom_nitems + kMomWarps - 1) / kMomWarps));
+    const int grid = std::max(1, std::min(c_grid[D][ki], (t.mom_nitems + kMomWarps - 1) / kMomWarps));
     count_launch();
     kern<<<grid, 32 * kMomWarps, smem, stream()>>>(t.mom_nitems, t.mom_items.as<int2>(),
                                                   t.node_i.as<int4>(), t.node_c.as<double>(),
