@@ -385,6 +385,25 @@ def test_direct_fp32_stream_dot_form_and_large_items(fg, oracle, D):
             assert sum(r.counters.fp32_pairs for r in res[1:]) > 0
 
 
+def test_fat_and_throughput_instantiations_agree(fg, monkeypatch):
+    """Tail-bound launches (few tasks per warp, D <= 4) run the 3-CTA/SM
+    traversal instantiation, large ones the 4-CTA one (DESIGN.md "Fat
+    launches"): the same tasks give bit-identical results either way."""
+    rng = np.random.default_rng(91)
+    pts = rng.random((12000, 3))
+    w = rng.uniform(0.5, 1.5, 12000)
+    t = fg.build_tree(fg.PointStore(pts, w), 25)
+    hs = [0.004, 0.03, 0.2]
+    cfg = fg.RunConfig(bandwidth=hs[0], epsilon=0.01)
+    monkeypatch.setenv("FG_FAT_TASKS", "1000000")
+    fat = fg.sweep_run(cfg, t, t, hs)
+    monkeypatch.setenv("FG_FAT_TASKS", "0")
+    thin = fg.sweep_run(cfg, t, t, hs)
+    for a, b in zip(fat, thin):
+        np.testing.assert_array_equal(a.values, b.values)
+        assert a.counters == b.counters
+
+
 def test_fp32_base_cases_off_outside_fp32_range(fg, oracle):
     """Weights outside the FP32 base case's safe range fall back to FP64."""
     rng = np.random.default_rng(5)
