@@ -50,25 +50,25 @@ namespace fg {
 int g_ref_leaf = 0;
 
 // Base-item granularity by bandwidth relative to the query blocks' median
-// inf-radius r_b (measured on C2: 32-point items win below ~0.05 r_b, 48
-// below ~0.5 r_b, 64 above; the per-bandwidth choice is ~3 % faster than any
-// single size).
+// inf-radius r_b (D >= 5: 32-point items win below ~0.05 r_b, 48 below
+// ~0.4 r_b, then larger).
 // At D >= 5 the direct FP32 stream takes items of any size: at h >~ 0.4 r_b,
 // where nearly every pair is exact, bigger items save traversal steps (C4
 // single runs: 128 points -2 % at 0.44 r_b, 256 points -8..-14 % from 0.6 r_b;
 // C3 -6..-14 % at 1-11 r_b).
 static int ref_leaf_for(const TreeDev &q, double h) {
     if (g_ref_leaf > 0) return g_ref_leaf;
+    // D <= 4: 64 (the anchored FP32 item limit) at every bandwidth -- with the
+    // Jensen mass bound smaller items no longer pay anywhere (C2/C5 single-run
+    // scans: 64 <= 48 <= 32 from 0.003 to 300 r_b, e.g. C2 at 0.42 r_b
+    // 0.54 vs 0.59 ms, C5 at 0.29 r_b 16.2 vs 16.5 ms)
+    if (q.dim <= 4) return 64;
     const double rb = q.qb_rad_median;
     if (!(rb > 0.0)) return 48;
     if (h < 0.05 * rb) return 32;
-    if (q.dim >= 5) {
-        if (h < 0.4 * rb) return 48;
-        if (h < 0.8 * rb) return 128;
-        return 256;
-    }
-    if (h < 0.5 * rb) return 48;
-    return 64;
+    if (h < 0.4 * rb) return 48;
+    if (h < 0.8 * rb) return 128;
+    return 256;
 }
 int g_stack_cap = 4096;
 // h / (median query-block radius) at which a bandwidth's tasks cost most
