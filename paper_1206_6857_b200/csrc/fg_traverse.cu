@@ -58,12 +58,14 @@ int g_ref_leaf = 0;
 // C3 -6..-14 % at 1-11 r_b).
 static int ref_leaf_for(const TreeDev &q, double h) {
     if (g_ref_leaf > 0) return g_ref_leaf;
-    // D <= 4: 64 (the anchored FP32 item limit) at every bandwidth -- with the
-    // Jensen mass bound smaller items no longer pay anywhere (C2/C5 single-run
-    // scans: 64 <= 48 <= 32 from 0.003 to 300 r_b, e.g. C2 at 0.42 r_b
-    // 0.54 vs 0.59 ms, C5 at 0.29 r_b 16.2 vs 16.5 ms)
-    if (q.dim <= 4) return 64;
+    // D <= 4: the anchored FP32 item limit (128) at every bandwidth -- with
+    // the Jensen mass bound smaller items no longer pay anywhere (C2/C5
+    // single-run scans: 64 <= 48 <= 32 from 0.003 to 300 r_b, e.g. C2 at
+    // 0.42 r_b 0.54 vs 0.59 ms, C5 at 0.29 r_b 16.2 vs 16.5 ms)
     const double rb = q.qb_rad_median;
+    if (q.dim <= 4)  // (far below the block radius FP32 items fail their bound;
+                     // FP64 items beyond 64 points are not staged)
+        return rb > 0.0 && h < 0.05 * rb ? kStageMax : kAnchorMax;
     if (!(rb > 0.0)) return 48;
     if (h < 0.05 * rb) return 32;
     if (h < 0.4 * rb) return 48;
