@@ -89,6 +89,12 @@ static constexpr double kFp32Share = 0.1;  // measured: C5 0.02: +97%, 0.05: +5%
 // leaves -- duplicate points -- are cut into runs).  Mode 1: fixed runs
 // regardless of node boundaries.
 int g_qblock_mode = 0;
+// Query blocks: maximal nodes with <= kQBlockNode points (at most n / 16), cut
+// into even runs of <= kQBlock consecutive tree-order points.  Depth-first
+// order keeps a run spatially compact, and runs fill a warp's 64 query slots:
+// against maximal <= 64-point nodes (41 points on average on C2) the sweeps
+// run C2 -10 %, C3 -32 %, C4 -35 %, C5 -22 % (4096; 16384 >= C2's n / 8 loses)
+static constexpr int kQBlockNode = 4096;
 
 template <int D>
 __global__ void query_blocks_kernel(int64_t nqb, const double *__restrict__ pw,
@@ -181,24 +187,29 @@ static void block_ranges(const TreeDev &t, std::vector<int2> &out) {
     }
 }
 
-// Block starts on the device (default mode): a block is a maximal node with
-// <= kQBlock points (a larger leaf -- duplicates -- is cut into runs); every
-// node with > kQBlock points marks its qualifying children, and a block marks
-// its run starts with the run length in a per-point array.  Blocks tile the
-// tree order, so an exclusive scan over the marks numbers them in tree order
-// (identical to the preorder walk of block_ranges).
-__global__ void block_marks_kernel(int64_t nnodes, const int4 *__restrict__ ni, int *__restrict__ len) {
+// Block starts on the device (default mode): every maximal node with <= lim
+// points (or leaf) is cut into even runs of <= kQBlock points; every node with
+// > lim points marks its qualifying children, and a run marks its start with
+// its length in a per-point array.  Runs tile the tree order, so an exclusive
+// scan over the marks numbers them in tree order.
+__global__ void block_marks_kernel(int64_t nnodes, const int4 *__restrict__ ni, int lim,
+                                   int *__restrict__ len) {
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= nnodes) return;
     const int4 e = ni[v];
+    // a node of <= lim points is cut into runs of <= kQBlock consecutive points
     auto emit = [&](const int4 c) {
-        for (int s = 0; s < c.y; s += kQBlock) len[c.x + s] = min(kQBlock, c.y - s);
+        const int nr = (c.y + kQBlock - 1) / kQBlock;  // runs, as even as possible
+        for (int r = 0; r < nr; r++) {
+            const int s0 = (int)((int64_t)c.y * r / nr), s1 = (int)((int64_t)c.y * (r + 1) / nr);
+            len[c.x + s0] = s1 - s0;
+        }
     };
-    if (v == 0 && (e.y <= kQBlock || e.z < 0)) emit(e);
-    if (e.y <= kQBlock || e.z < 0) return;
+    if (v == 0 && (e.y <= lim || e.z < 0)) emit(e);
+    if (e.y <= lim || e.z < 0) return;
     for (int k = 0; k < 2; k++) {
         const int4 c = ni[k == 0 ? e.z : e.w];
-        if (c.y <= kQBlock || c.z < 0) emit(c);
+        if (c.y <= lim || c.z < 0) emit(c);
     }
 }
 
@@ -221,8 +232,11 @@ static int device_block_ranges(TreeDev &t, int64_t &nqb) {
     FG_TRY(s_idx.reserve(sizeof(int) * (n + 1)));
     FG_CUDA_TRY(cudaMemsetAsync(s_len.p, 0, sizeof(int) * (n + 1), stream()));
     count_launch();
+    const char *lenv = getenv("FG_QBLOCK_NODE");  // experiment knob
+    const int lim = lenv ? std::max(kQBlock, atoi(lenv))
+                         : (int)std::max<int64_t>(kQBlock, std::min<int64_t>(kQBlockNode, n / 16));
     block_marks_kernel<<<(unsigned)((t.nnodes + 255) / 256), 256, 0, stream()>>>(
-        t.nnodes, t.node_i.as<int4>(), s_len.as<int>());
+        t.nnodes, t.node_i.as<int4>(), lim, s_len.as<int>());
     count_launch();
     block_flags_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream()>>>(n + 1, s_len.as<int>(),
                                                                               s_flag.as<int>());

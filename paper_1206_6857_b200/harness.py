@@ -112,10 +112,26 @@ def telescoping_audit(ledger, qtree: KdTree, exact, epsilon: float) -> dict:
     * weight_error = max relative deviation of sum(W_R) from n_blocks * W:
       every reference's weight is settled exactly once per query block.
     """
-    from .summation_engine import query_block_nodes
+    from .summation_engine import query_block_nodes, query_block_ranges
 
     e = qtree.arrays()
     exact_tree = np.asarray(exact, dtype=float)[e["perm"]]
+    blocks = getattr(ledger, "blocks", None)
+    if blocks is not None:
+        # per query block: its own queries' minimum exact sum, one settlement of
+        # every reference weight
+        starts, counts = query_block_ranges(qtree)
+        total_w = float(e["weight"][0])
+        bsum = np.bincount(blocks, weights=[t[3] for t in ledger], minlength=len(starts))
+        wsum = np.bincount(blocks, weights=[t[2] for t in ledger], minlength=len(starts))
+        used = np.unique(blocks)
+        worst, werr = 0.0, 0.0
+        for b in used:
+            g = float(exact_tree[starts[b]:starts[b] + counts[b]].min())
+            if bsum[b] > 0.0:
+                worst = max(worst, bsum[b] / (epsilon * g) if g > 0.0 else float("inf"))
+            werr = max(werr, abs(wsum[b] - total_w) / total_w)
+        return {"worst_ratio": worst, "weight_error": werr, "query_nodes": len(used)}
     blocks_per_node = np.bincount(query_block_nodes(qtree), minlength=len(e["start"]))
     bound = {}
     wsum = {}

@@ -124,9 +124,18 @@ AUDIT_DTYPE = np.dtype([("kind", np.int32), ("qblock", np.int32), ("seq", np.int
 AUDIT_KINDS = ("base", "fd", "hermite", "local", "h2l")
 
 
+def query_block_ranges(qtree: KdTree) -> tuple:
+    """(starts, counts) of the query blocks in tree order."""
+    nb = query_block_count(qtree)
+    starts = np.empty(nb, np.int32)
+    counts = np.empty(nb, np.int32)
+    _lib.call("fg_query_block_ranges", qtree.handle, _lib.ptr(starts), _lib.ptr(counts))
+    return starts, counts
+
+
 def query_block_nodes(qtree: KdTree) -> np.ndarray:
-    """Preorder node index (Node.index) of every query block: the maximal node
-    with <= 64 points it is (or, for a larger leaf cut into runs, lies in)."""
+    """Preorder node index (Node.index) of every query block: the deepest node
+    containing its run of tree-order points."""
     nb = query_block_count(qtree)
     starts = np.empty(nb, np.int32)
     counts = np.empty(nb, np.int32)
@@ -164,10 +173,20 @@ def _audit_run(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: str, plimi
     ev = ev[:n.value]
     ev = ev[np.lexsort((ev["lane"], ev["seq"], ev["qblock"]))]
     nodes = query_block_nodes(qtree)
-    ledger = [(AUDIT_KINDS[k], int(nodes[b]), float(w), float(bd), float(ml), float(fl))
-              for k, b, w, bd, ml, fl in zip(ev["kind"], ev["qblock"], ev["w_ref"],
-                                               ev["bound"], ev["mass_lo"], ev["token_flow"])]
+    ledger = AuditLedger(
+        (AUDIT_KINDS[k], int(nodes[b]), float(w), float(bd), float(ml), float(fl))
+        for k, b, w, bd, ml, fl in zip(ev["kind"], ev["qblock"], ev["w_ref"], ev["bound"],
+                                       ev["mass_lo"], ev["token_flow"]))
+    ledger.blocks = np.asarray(ev["qblock"], dtype=np.int64)
     return cnt, secs.value, ledger, ev
+
+
+class AuditLedger(list):
+    """The ledger tuples (reference form: kind, query node, W_R, bound,
+    mass_lo, token flow) plus ``blocks``: the query block of every event (the
+    unit each bound is charged against; several blocks may share a node)."""
+
+    blocks = None
 
 
 def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: str,
