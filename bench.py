@@ -392,7 +392,7 @@ def run_ours(args):
             "config": {"workload": describe(wl), "epsilon": wl.epsilon,
                        "bandwidths": len(wl.bandwidths), "parallelism": f"query-blocks x{world}",
                        "l2": "flushed (512 MiB write) between timed steps",
-                       "engine": {"query_block": 64, "ref_leaf": "64/128 (D <= 4), 32/48/128/256 (D >= 5), by h / median block radius",
+                       "engine": {"query_block": 64, "ref_leaf": "32/64/128 (D <= 4), 32/64/128/256 (D >= 5), by h / median block radius",
                                   "tree_leaf": 25}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(lc1[0] - lc0[0]),

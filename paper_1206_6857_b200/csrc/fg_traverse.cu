@@ -58,18 +58,19 @@ int g_ref_leaf = 0;
 // C3 -6..-14 % at 1-11 r_b).
 static int ref_leaf_for(const TreeDev &q, double h) {
     if (g_ref_leaf > 0) return g_ref_leaf;
-    // D <= 4: the anchored FP32 item limit (128) at every bandwidth -- with
-    // the Jensen mass bound smaller items no longer pay anywhere (C2/C5
-    // single-run scans: 64 <= 48 <= 32 from 0.003 to 300 r_b, e.g. C2 at
-    // 0.42 r_b 0.54 vs 0.59 ms, C5 at 0.29 r_b 16.2 vs 16.5 ms)
     const double rb = q.qb_rad_median;
-    if (q.dim <= 4)  // (far below the block radius FP32 items fail their bound;
-                     // FP64 items beyond 64 points are not staged)
-        return rb > 0.0 && h < 0.05 * rb ? kStageMax : kAnchorMax;
     if (!(rb > 0.0)) return 48;
-    if (h < 0.05 * rb) return 32;
-    if (h < 0.4 * rb) return 48;
-    if (h < 0.8 * rb) return 128;
+    // single-run scans per bandwidth with the Jensen bound and run-based query
+    // blocks (C3, C4, C5; r_b = median block inf-radius): small items where
+    // pruning still bites, bigger ones where nearly every pair is exact
+    if (q.dim <= 4) {  // anchored FP32 items: <= kAnchorMax (128) points
+        if (h < 0.2 * rb) return 32;
+        if (h < 1.0 * rb) return kStageMax;
+        return kAnchorMax;
+    }
+    if (h < 0.1 * rb) return 32;
+    if (h < 0.25 * rb) return 64;
+    if (h < 0.6 * rb) return 128;
     return 256;
 }
 int g_stack_cap = 4096;
