@@ -569,3 +569,27 @@ def test_kde_entry_point_and_torch_ops(fg, oracle):
     assert max(rel(nv[j].cpu().numpy(), exact_mono[j]) for j in range(3)) <= 1e-12
     with pytest.raises(ValueError):
         fg.kde(q, ref, w, [])
+
+
+@pytest.mark.parametrize("index", [2, 3, 4, 5])
+def test_full_size_configs_within_eps(fg, index):
+    """BASELINE.json configs 2-5 at FULL size: the whole DITO sweep (the bench
+    workload for C2) keeps every sampled query within eps of the exhaustive
+    FP64 sums (the size-independent eps contract).  The sweep runs
+    over all M queries; the exhaustive check uses a seeded 20000-query sample
+    (the exhaustive kernel itself is pinned to the oracle and golden vectors
+    above)."""
+    from paper_1206_6857_b200.configs import config
+
+    wl = config(index)
+    rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
+    qt = rt if wl.monochromatic else fg.build_tree(fg.PointStore(wl.queries), 25)
+    hs = list(wl.bandwidths)
+    sweep = fg.sweep_run(fg.RunConfig(bandwidth=hs[0], epsilon=wl.epsilon), qt, rt, hs)
+    assert len(sweep) == len(hs)
+    sample = np.sort(np.random.default_rng(77).choice(wl.m, min(wl.m, 20000), replace=False))
+    exact = fg.naive_sum(wl.query_points()[sample], wl.references, wl.weights, hs).values
+    for j in range(len(hs)):
+        v = sweep[j].values
+        assert v.shape == (wl.m,) and np.all(np.isfinite(v)) and np.all(v > 0.0)
+        assert rel(v[sample], exact[j]) <= wl.epsilon, (index, j, hs[j])
