@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: effective Gaussian pair evaluations per second (M*N*bandwidths / T)
-at eps=0.01 on BASELINE.json's configs[1] (C2: D=3, M=N=1e5, monochromatic,
-10 bandwidths log-spaced 1e-3..1e2 x Silverman h), plus the FP64 roofline
-fraction of the dominant kernel.
+on the largest single-GPU config of BASELINE.json, configs[4] (C5: D=3,
+M=N=4e6, monochromatic, 16 bandwidths log-spaced 1e-3..1e2 x Silverman h,
+eps=0.001), plus the roofline fraction of the dominant kernel.
 
 One step = one full sweep: device kd-tree build (amortised once per sweep, as
 the reference's run_sweep does, cli_harness.py:246-283), then for every
@@ -43,12 +43,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="target CPU time of one bounded oracle sample")
+    # C5 is the largest config that fits one GPU (4e6 points: 128 MB of
+    # points + 16 x 32 MB of values); configs 1-4 are parity cases
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--sample-queries", type=int, default=0,
+                    help="CPU sample size M' (default: BASELINE.md section 3 per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+# seeded query subsamples for the CPU path, run
+# bichromatically against the FULL reference tree (identical per-query sums)
+SAMPLE_QUERIES = {1: 0, 2: 10_000, 3: 4_096, 4: 1_024, 5: 1_024}  # 0 = all queries
 
 
 def workload(index):
@@ -60,6 +67,28 @@ def workload(index):
 def describe(wl):
     return (f"{wl.name}: D={wl.dim}, M=N={wl.n}, {wl.notes.get('mode')}, "
             f"{len(wl.bandwidths)} bandwidths, eps={wl.epsilon}, h_S={wl.h_star:.5g}")
+
+
+def config_dict(wl, world):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": describe(wl), "epsilon": wl.epsilon, "bandwidths": len(wl.bandwidths),
+            "parallelism": f"query shards x{world}",
+            "l2": "GPU arm: 512 MiB L2 flush between timed steps (inputs 128 MB > L2 too)"}
+
+
+def host_info(threads):
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "threads_used": threads,
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
 
 
 # ------------------------------------------------------------- clocks
@@ -124,8 +153,8 @@ class ClockSampler:
 def profiled_traffic():
     """dram read+write bytes per launch of the dominant kernel, from the
     committed `ncu --set full` summary (profiles/, one traversal launch of this
-    same bench command: the whole 10-bandwidth sweep of one step).  Null when
-    no summary is present."""
+    same bench command: the whole sweep of one step).  Null when no summary is
+    present."""
     import glob
     import re
 
@@ -140,55 +169,27 @@ def profiled_traffic():
             return None
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[m.group(2)]
         tot += float(m.group(1)) * scale
+    m = re.search(r"^# launch: (.*)$", txt, re.M)
     return {"bytes_per_launch": tot, "source": os.path.basename(files[-1]),
-            "launch": "one C2 step's sweep launch (10 bandwidths)"}
+            "launch": m.group(1) if m else "see the summary header"}
 
 
 # ------------------------------------------------------------ CPU side
-def cpu_sample(wl, target_seconds, threads):
-    """Bounded sample of the workload on the host with the oracle port of the
-    reference's DFS DITO (oracle/fg_oracle.c: fgo_run_sharded): M' seeded query
-    rows, bichromatic against the full reference tree (identical per-query sums
-    to the monochromatic problem), every bandwidth, `threads` shards.
-    Build + per-bandwidth refresh + run are timed, like run_sweep."""
+def cpu_step_factory(wl, mq, threads):
+    """One step of the reference's algorithm on the host: the oracle port of
+    its DFS DITO (oracle/fg_oracle.c: fgo_run_sharded, `threads` disjoint query
+    shards).  M' seeded query rows, bichromatic against the full reference
+    tree (identical per-query sums to the monochromatic problem).  Mirrors
+    run_sweep's accounting (cli_harness.py:246-283): the reference tree build
+    once per sweep, then per bandwidth refresh_moments + dito_run."""
     import oracle
 
-    rng = np.random.default_rng(4242)
     qp = wl.query_points()
-    mq = 256
-    while True:
-        idx = np.sort(rng.choice(qp.shape[0], min(mq, qp.shape[0]), replace=False))
-        qs = qp[idx]
-        t0 = time.perf_counter()
-        rt = oracle.Tree(wl.references, wl.weights, 25)
-        pl = {1: 8, 2: 8, 3: 6, 4: 4, 5: 4, 6: 2}.get(wl.dim, 1)
-        for h in wl.bandwidths:
-            rt.refresh_moments(h, pl)
-            oracle.run_sharded("dito", qs, rt, h, wl.epsilon, threads=threads)
-        dt = time.perf_counter() - t0
-        if dt >= 0.4 * target_seconds or mq >= qp.shape[0]:
-            break
-        mq = int(min(qp.shape[0], mq * max(2.0, 0.8 * target_seconds / max(dt, 1e-3))))
-    pairs = len(idx) * wl.n * len(wl.bandwidths)
-    return pairs / dt, dt, len(idx)
-
-
-def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port of its DFS DITO)
-    on the host cores, same metric/config, bounded samples per step."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    import oracle
-
-    wl = workload(args.config)
-    threads = os.cpu_count() or 1
-    oracle.lib()
-    # calibrate the per-step sample on a warm-up step
-    _, _, mq = cpu_sample(wl, args.cpu_seconds, threads)
-    rng = np.random.default_rng(4242)
-    idx = np.sort(rng.choice(wl.m, mq, replace=False))
-    qs = wl.query_points()[idx]
+    if mq <= 0 or mq >= qp.shape[0]:
+        qs = qp
+    else:
+        rng = np.random.default_rng(4242)
+        qs = qp[np.sort(rng.choice(qp.shape[0], mq, replace=False))]
     pl = {1: 8, 2: 8, 3: 6, 4: 4, 5: 4, 6: 2}.get(wl.dim, 1)
 
     def step():
@@ -197,7 +198,32 @@ def run_reference(args):
             rt.refresh_moments(h, pl)
             oracle.run_sharded("dito", qs, rt, h, wl.epsilon, threads=threads)
 
-    for _ in range(max(0, args.warmup - 1)):
+    return step, qs.shape[0]
+
+
+def sample_desc(wl, mq, dt):
+    ext = dt * wl.m / mq
+    return (f"{mq} of {wl.m} seeded queries (BASELINE.md section 3) x {len(wl.bandwidths)} "
+            f"bandwidths per step vs the full {wl.n}-point reference tree (bichromatic "
+            f"restatement of the monochromatic sums): tree build + per-bandwidth refresh + "
+            f"DFS DITO, {dt:.1f} s per step; extrapolated full-M step {ext:.4g} s")
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port of its DFS DITO,
+    the reference being pure Python that cannot travel to the GPU box) on all
+    host cores, same metric/config, a bounded query sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    wl = workload(args.config)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    threads = os.cpu_count() or 1
+    oracle.lib()
+    step, mq = cpu_step_factory(wl, args.sample_queries or SAMPLE_QUERIES[args.config], threads)
+    for _ in range(args.warmup):
         step()
     times = []
     for _ in range(args.steps):
@@ -207,18 +233,16 @@ def run_reference(args):
     total = sum(times)
     pairs = mq * wl.n * len(wl.bandwidths) * args.steps
     value = pairs / total
-    sample = (f"{mq} of {wl.m} queries x {len(wl.bandwidths)} bandwidths per step vs the full "
-              f"reference tree (bichromatic restatement of the monochromatic sums), "
-              f"tree build + refresh + DFS DITO")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))), "host_only": True,
+        "n_gpus": world, "host_only": True,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded; SURVEY Appendix C)",
-        "config": {"workload": describe(wl), "sample_queries": mq},
+        "config": config_dict(wl, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample_desc(wl, mq, total / args.steps),
+                         "host": host_info(threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,7 +278,8 @@ def run_ours(args):
     flush = torch.empty(int(512 * 2**20) // 4, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
-    stats = {"kernel_s": 0.0, "pairs": 0, "pairs32": 0, "visits": 0}
+    stats = {"kernel_s": 0.0, "pairs": 0, "pairs32": 0, "visits": 0, "herm": 0,
+             "herm_terms": 0}
 
     def step(record=True):
         vals_d.zero_()
@@ -270,10 +295,13 @@ def run_ours(args):
             results = run_sharded_sweep(cfg, tree, tree, wl.bandwidths, vals_d, rank, world)
         if record:
             for res in results:
+                c = res.counters
                 stats["kernel_s"] += res.seconds
-                stats["pairs"] += res.counters.exact_pairs
-                stats["pairs32"] += res.counters.fp32_pairs
-                stats["visits"] += res.counters.pair_visits
+                stats["pairs"] += c.exact_pairs
+                stats["pairs32"] += c.fp32_pairs
+                stats["visits"] += c.pair_visits
+                stats["herm"] += c.hermite_evals
+                stats["herm_terms"] += c.hermite_terms
         del tree
 
     with torch.cuda.stream(stream):
@@ -306,11 +334,13 @@ def run_ours(args):
     pairs_eff = wl.m * wl.n * len(wl.bandwidths)
     value = pairs_eff * args.steps / total
 
-    # roofline of the dominant kernel (fused traversal + base-case kernel).
-    # Its pair work has two legs: FP64 pairs bound by
-    # the DFMA pipe at F(D) flops per pair, FP32 pairs bound by the SFU at one
-    # ex2 per pair.  peak = the pair rate of the ideal kernel for this step's
-    # FP64/FP32 mix; achieved = pairs evaluated / kernel time.
+    # Roofline of the dominant kernel (the fused traversal + base-case kernel;
+    # DESIGN.md "Roofline").  Its algorithmic work has three legs, each at its
+    # own measured peak: FP64 pairs at F(D) = 3D + 34 flops on the DFMA pipe,
+    # FP32 pairs at one ex2 each on the SFU, Hermite far-field evaluations at
+    # 2 K_p + 31 + 4D FP64 flops each (the dot with the moments, one exp, the
+    # offsets) on the DFMA pipe.  ideal = the time an ideal kernel needs for
+    # exactly this work; frac = ideal / measured kernel time.
     peak = np.zeros(1)
     _lib.call("fg_fp64_peak", _lib.ptr(peak))
     peak_tf = float(peak[0])
@@ -318,23 +348,37 @@ def run_ours(args):
     _lib.call("fg_ex2_peak", _lib.ptr(ex2))
     ex2_gops = float(ex2[0])
     n64, n32, ks = stats["pairs"], stats["pairs32"], stats["kernel_s"]
-    ideal_s = n64 * F_OF_D[D] / (peak_tf * 1e12) + n32 / (ex2_gops * 1e9)
+    herm_flops = 2.0 * stats["herm_terms"] + (31 + 4 * D) * stats["herm"]
+    t64 = n64 * F_OF_D[D] / (peak_tf * 1e12)
+    t32 = n32 / (ex2_gops * 1e9)
+    th = herm_flops / (peak_tf * 1e12)
+    ideal_s = t64 + t32 + th
+    frac = ideal_s / ks if ks else None
+    # achieved/peak in pair units: pairs per second of kernel time against the
+    # pair rate of the ideal kernel on this step's mix
     achieved = (n64 + n32) / ks / 1e9 if ks else 0.0
     peak_mix = (n64 + n32) / ideal_s / 1e9 if ideal_s else None
     roofline = {"bound": "fp64+sfu", "achieved": achieved, "peak": peak_mix, "unit": "Gpair/s",
-                "frac": achieved / peak_mix if peak_mix else None,
+                "frac": frac,
                 "traffic": profiled_traffic(),
-                "kernel": f"traverse_kernel<{D}> (fused traversal + leaf base cases)",
+                "kernel": f"traverse_kernel<{D}> (fused traversal + leaf base cases + far field)",
                 "legs": {"fp64": {"pairs_per_step": n64 / args.steps,
                                   "flops_per_pair": F_OF_D[D], "peak_tflops": peak_tf,
-                                  "achieved_tflops_over_kernel_time":
-                                      n64 * F_OF_D[D] / ks / 1e12 if ks else 0.0},
+                                  "ideal_ms_per_step": 1e3 * t64 / args.steps},
                          "fp32": {"pairs_per_step": n32 / args.steps, "ex2_per_pair": 1,
-                                  "peak_ex2_gops": ex2_gops}},
+                                  "peak_ex2_gops": ex2_gops,
+                                  "ideal_ms_per_step": 1e3 * t32 / args.steps},
+                         "hermite": {"evals_per_step": stats["herm"] / args.steps,
+                                     "flops_per_step": herm_flops / args.steps,
+                                     "flops_per_eval": "2 K_p + 31 + 4D",
+                                     "ideal_ms_per_step": 1e3 * th / args.steps}},
+                "kernel_ms_per_step": 1e3 * ks / args.steps,
                 "kernel_share_of_step": ks / total if total else None,
                 "visits_per_s_in_kernel": stats["visits"] / ks if ks else None,
-                "peak_source": "measured: DFMA microbenchmark fg_fp64_peak and ex2.approx "
-                               "microbenchmark fg_ex2_peak (burst)",
+                "peak_source": "measured in this process: DFMA microbenchmark fg_fp64_peak and "
+                               "ex2.approx microbenchmark fg_ex2_peak (burst; MEASURED_PEAKS.json "
+                               "has no FP64/SFU entry); nominal DFMA 148 x 64 x 2 x 1.965 GHz = "
+                               "37.2 TF/s",
                 "pair_share": {"fp64": n64 / (pairs_eff * args.steps),
                                "fp32": n32 / (pairs_eff * args.steps)}}
 
@@ -375,10 +419,13 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, dt, mq = cpu_sample(wl, args.cpu_seconds, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{mq} of {wl.m} queries x {len(wl.bandwidths)} bandwidths vs the full "
-                         f"reference tree, oracle DFS DITO, {dt:.1f} s"}
+        cstep, mq = cpu_step_factory(wl, args.sample_queries or SAMPLE_QUERIES[args.config],
+                                     threads)
+        t0 = time.perf_counter()
+        cstep()
+        dt = time.perf_counter() - t0
+        cpu = {"value": mq * wl.n * len(wl.bandwidths) / dt, "unit": UNIT, "cores": threads,
+               "kind": "port", "sample": sample_desc(wl, mq, dt), "host": host_info(threads)}
 
     if rank == 0:
         line = {
@@ -389,15 +436,15 @@ def run_ours(args):
             "dtype_note": "FP64 traversal, bounds, series and results; leaf pairs in FP32 where "
                           "their rigorous error bound fits a reserved 10% of eps (DESIGN.md)",
             "data": "synthetic (seeded; SURVEY Appendix C)",
-            "config": {"workload": describe(wl), "epsilon": wl.epsilon,
-                       "bandwidths": len(wl.bandwidths), "parallelism": f"query-blocks x{world}",
-                       "l2": "flushed (512 MiB write) between timed steps",
-                       "engine": {"query_block": 64, "ref_leaf": "32/64/128 (D <= 4), 32/64/128/256 (D >= 5), by h / median block radius",
-                                  "tree_leaf": 25}},
+            "config": config_dict(wl, world),
+            "engine": {"query_block": 64, "tree_leaf": 25,
+                       "ref_leaf": "32/64/128 (D <= 4), 32/64/128/256 (D >= 5), by h / median "
+                                   "block radius"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(lc1[0] - lc0[0]),
             "clocks": clk.summary(),
             "detail": {"kernel_ms_per_step": 1e3 * stats["kernel_s"] / args.steps,
+                       "hermite_evals_per_step": stats["herm"] / args.steps,
                        "visits_per_step": stats["visits"] / args.steps,
                        "exact_pairs_per_step": stats["pairs"] / args.steps,
                        "fp32_pairs_per_step": stats["pairs32"] / args.steps},

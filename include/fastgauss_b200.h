@@ -10,9 +10,19 @@
  *
  * Pointers marked "host or device" are classified with
  * cudaPointerGetAttributes: device/managed memory is used in place, host
- * memory is staged through the engine's device buffers.  All work is issued
- * on the stream set by fg_set_stream (default: the legacy default stream)
- * and every call returns when its results are available to the caller.
+ * memory is staged through the engine's device buffers.  All work of a host
+ * thread is issued on that thread's stream (fg_set_stream; default: the
+ * per-thread default stream) and every call returns when its results are
+ * available to the caller (fg_moments_refresh is stream-ordered instead).
+ *
+ * Ownership and threading: a tree handle owns its
+ * device buffers and its per-tree state; one traversal owns a query tree at a
+ * time, and the reference side is read-only after its refresh.  Concurrent
+ * calls from different host threads on distinct query trees are safe: every
+ * engine scratch buffer belongs to one (host thread, device), each thread
+ * issues on its own stream, and work queued on a tree (moments) is fenced by
+ * the tree's event before any other stream uses it.  A tree's calls run on
+ * the device it was built on.
  *
  * Status codes (every function returns one):
  *   FG_OK 0, FG_EINVAL 1 (-> ValueError), FG_ESTALE 2 (stale moments ->
@@ -51,6 +61,10 @@ typedef struct {
     int64_t exact_pairs; /* query x reference pairs evaluated exactly in FP64 */
     int64_t fp32_pairs;  /* pairs evaluated in FP32 with their error bound charged
                             through the token rule (see fg_set_engine_params) */
+    int64_t hermite_evals; /* (Hermite item, query) evaluations of EVALM: the far-field
+                              leg of the traversal kernel's roofline */
+    int64_t hermite_terms; /* sum over those evaluations of K_p (coefficients used) */
+    int64_t local_evals;   /* queries evaluated against a local expansion (EVALL) */
 } fg_counters;
 
 typedef struct fg_tree fg_tree; /* device-resident kd-tree (KdTree, spatial_index.py:144) */
@@ -75,8 +89,10 @@ int fg_fp64_peak(double *tflops);
 /* measured ex2.approx.f32 (SFU) throughput, Gop/s: the FP32 base case's
  * per-pair limit (one ex2 per pair) */
 int fg_ex2_peak(double *gops);
-/* stream: a cudaStream_t (NULL = legacy default stream) */
+/* the calling thread's stream: a cudaStream_t on the current device (NULL =
+ * the per-thread default stream).  Switching drains the previous stream. */
 int fg_set_stream(void *stream);
+int fg_get_stream(void **stream);
 int fg_set_device(int device);
 int fg_synchronize(void);
 

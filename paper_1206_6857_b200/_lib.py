@@ -9,6 +9,7 @@ raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -31,7 +32,8 @@ _F64 = ctypes.c_double
 class fg_counters(ctypes.Structure):
     _fields_ = [("pair_visits", _I64), ("base_cases", _I64), ("fd_prunes", _I64),
                 ("hermite_prunes", _I64), ("local_prunes", _I64), ("h2l_prunes", _I64),
-                ("exact_pairs", _I64), ("fp32_pairs", _I64)]
+                ("exact_pairs", _I64), ("fp32_pairs", _I64), ("hermite_evals", _I64),
+                ("hermite_terms", _I64), ("local_evals", _I64)]
 
 
 # name -> argtypes (all functions return int status except fg_last_error)
@@ -39,6 +41,7 @@ SIGNATURES = {
     "fg_version": [],
     "fg_last_error": [],
     "fg_set_stream": [_P],
+    "fg_get_stream": [ctypes.POINTER(_P)],
     "fg_set_device": [ctypes.c_int],
     "fg_synchronize": [],
     "fg_naive_sum": [_P, _I64, _P, _P, _I64, _I32, _P, _I32, _P],
@@ -141,4 +144,65 @@ def as_f64(x, ndim=None):
 
 
 def set_stream(stream_handle: int | None) -> None:
+    """Set the calling thread's engine stream (None: per-thread default)."""
     call("fg_set_stream", stream_handle)
+
+
+def get_stream() -> int | None:
+    s = ctypes.c_void_p()
+    call("fg_get_stream", ctypes.byref(s))
+    return s.value
+
+
+@contextlib.contextmanager
+def torch_stream(*objs):
+    """Run the engine on torch's current stream while any of ``objs`` is a
+    CUDA tensor, so the call is ordered after the torch work that produced
+    (or zeroed) those tensors; the thread's previous engine stream is restored
+    afterwards."""
+    t = next((o for o in objs if _is_torch(o) and o.is_cuda), None)
+    if t is None:
+        yield
+        return
+    import torch
+
+    cur = torch.cuda.current_stream(t.device).cuda_stream or None
+    prev = get_stream()
+    if cur == prev:
+        yield
+        return
+    set_stream(cur)
+    try:
+        yield
+    finally:
+        set_stream(prev)
+
+
+def check_out(out, shapes, what: str = "out"):
+    """Validate a caller-supplied output buffer before its raw pointer reaches
+    the C ABI: float64, C-contiguous, writeable, one of ``shapes``; a CUDA
+    tensor must be on the current device.  Raises ValueError."""
+    if out is None:
+        return None
+    shapes = [tuple(int(d) for d in sh) for sh in shapes]
+    if isinstance(out, np.ndarray):
+        ok = (out.dtype == np.float64 and out.flags.c_contiguous and out.flags.writeable
+              and tuple(out.shape) in shapes)
+        if not ok:
+            raise ValueError(f"{what} must be a writeable C-contiguous float64 array of shape "
+                             f"{' or '.join(map(str, shapes))}; got {out.dtype} {out.shape}")
+        return out
+    if _is_torch(out):
+        import torch
+
+        ok = (out.dtype == torch.float64 and out.is_contiguous()
+              and tuple(out.shape) in shapes)
+        if not ok:
+            raise ValueError(f"{what} must be a contiguous float64 tensor of shape "
+                             f"{' or '.join(map(str, shapes))}; got {out.dtype} "
+                             f"{tuple(out.shape)}")
+        if out.is_cuda and out.device.index != torch.cuda.current_device():
+            raise ValueError(f"{what} is on {out.device}, the engine runs on "
+                             f"cuda:{torch.cuda.current_device()}")
+        return out
+    raise ValueError(f"{what} must be a NumPy array or a torch tensor")

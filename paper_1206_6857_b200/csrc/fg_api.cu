@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "fg_internal.cuh"
@@ -17,7 +18,9 @@
 namespace fg {
 
 static thread_local std::string t_last_error;
-static cudaStream_t g_stream = nullptr;
+// the calling thread's stream (fg_set_stream); NULL selects the per-thread
+// default stream, so threads that never set one still run independently
+static thread_local cudaStream_t t_stream = cudaStreamPerThread;
 
 void set_error(const std::string &msg) { t_last_error = msg; }
 static std::atomic<long long> g_launches{0};
@@ -66,7 +69,19 @@ __global__ void ex2_peak_kernel(float *out, int iters) {
     const float s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
     if (s == 12345.678f) out[0] = s;
 }
-cudaStream_t stream() { return g_stream; }
+cudaStream_t stream() { return t_stream; }
+
+int tree_use(TreeDev &t) {
+    if (t.pending && t.ready) FG_CUDA_TRY(cudaStreamWaitEvent(stream(), t.ready, 0));
+    return FG_OK;
+}
+
+int tree_mark(TreeDev &t) {
+    if (!t.ready) FG_CUDA_TRY(cudaEventCreateWithFlags(&t.ready, cudaEventDisableTiming));
+    FG_CUDA_TRY(cudaEventRecord(t.ready, stream()));
+    t.pending = true;
+    return FG_OK;
+}
 
 bool is_device_ptr(const void *ptr) {
     if (!ptr) return false;
@@ -161,11 +176,17 @@ static void compositions(int total, int dims, std::vector<int> &prefix,
 }
 
 static std::mutex g_tab_mu;
-static std::map<std::pair<int, int>, std::unique_ptr<SeriesTables>> g_tables;
+// tables per (device, dim, order): device buffers belong to one device
+static std::map<std::tuple<int, int, int>, std::unique_ptr<SeriesTables>> g_tables;
 
 const SeriesTables *series_tables(int dim, int order, int *status) {
     std::lock_guard<std::mutex> lk(g_tab_mu);
-    auto key = std::make_pair(dim, order);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    auto key = std::make_tuple(dev, dim, order);
     auto it = g_tables.find(key);
     if (it != g_tables.end()) {
         *status = FG_OK;
@@ -239,7 +260,8 @@ const SeriesTables *series_tables(int dim, int order, int *status) {
     }
     auto up = [&](DBuf &dst, const void *src, size_t bytes) -> int {
         FG_TRY(dst.reserve(bytes));
-        FG_CUDA_TRY(cudaMemcpy(dst.p, src, bytes, cudaMemcpyHostToDevice));
+        FG_CUDA_TRY(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, stream()));
+        FG_CUDA_TRY(cudaStreamSynchronize(stream()));
         return FG_OK;
     };
     int st = FG_OK;
@@ -334,7 +356,19 @@ int fg_ex2_peak(double *gops) {
 const char *fg_last_error(void) { return t_last_error.c_str(); }
 
 int fg_set_stream(void *s) {
-    g_stream = reinterpret_cast<cudaStream_t>(s);
+    cudaStream_t ns = s ? reinterpret_cast<cudaStream_t>(s) : cudaStreamPerThread;
+    if (ns != t_stream) {
+        // this thread's scratch may still be in use by work queued on the old
+        // stream: drain it before any call reuses the scratch on the new one
+        FG_CUDA_TRY(cudaStreamSynchronize(t_stream));
+        t_stream = ns;
+    }
+    return FG_OK;
+}
+
+int fg_get_stream(void **s) {
+    FG_REQUIRE(s, FG_EINVAL, "null argument");
+    *s = t_stream == cudaStreamPerThread ? nullptr : reinterpret_cast<void *>(t_stream);
     return FG_OK;
 }
 
@@ -359,7 +393,14 @@ int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap, int32_t fp32_base)
     return FG_OK;
 }
 
-static DBuf g_stage_q, g_stage_r, g_stage_w, g_stage_out;
+struct StageQ;
+struct StageR;
+struct StageW;
+struct StageOut;
+struct SweepOut;
+struct AuditEv;
+struct AuditCnt;
+struct AuditOut;
 
 int fg_naive_sum(const double *queries, int64_t m, const double *references,
                  const double *weights, int64_t n, int32_t dim, const double *bandwidths,
@@ -370,14 +411,15 @@ int fg_naive_sum(const double *queries, int64_t m, const double *references,
     for (int k = 0; k < nh; k++)
         FG_REQUIRE(bandwidths[k] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const void *dq, *dr, *dw;
-    FG_TRY(to_device(queries, sizeof(double) * m * dim, g_stage_q, &dq));
-    FG_TRY(to_device(references, sizeof(double) * n * dim, g_stage_r, &dr));
-    FG_TRY(to_device(weights, sizeof(double) * n, g_stage_w, &dw));
+    FG_TRY(to_device(queries, sizeof(double) * m * dim, scratch<StageQ>(), &dq));
+    FG_TRY(to_device(references, sizeof(double) * n * dim, scratch<StageR>(), &dr));
+    FG_TRY(to_device(weights, sizeof(double) * n, scratch<StageW>(), &dw));
     const bool out_dev = is_device_ptr(out);
     double *dout = out;
     if (!out_dev) {
-        FG_TRY(g_stage_out.reserve(sizeof(double) * m * nh));
-        dout = g_stage_out.as<double>();
+        DBuf &so = scratch<StageOut>();
+        FG_TRY(so.reserve(sizeof(double) * m * nh));
+        dout = so.as<double>();
     }
     FG_TRY(fg::naive_sum((const double *)dq, m, (const double *)dr, (const double *)dw, n, dim,
                          bandwidths, nh, dout));
@@ -401,6 +443,7 @@ int fg_tree_build(const double *points, const double *weights, int64_t n, int32_
     FG_TRY(to_device(points, sizeof(double) * n * dim, sp, &dp));
     if (weights) FG_TRY(to_device(weights, sizeof(double) * n, sw, &dw));
     auto *t = new fg_tree();
+    FG_CUDA_TRY(cudaGetDevice(&t->t.device));
     int st = tree_build((const double *)dp, (const double *)dw, n, dim, leaf_threshold, t->t);
     if (st != FG_OK) {
         delete t;
@@ -412,6 +455,8 @@ int fg_tree_build(const double *points, const double *weights, int64_t n, int32_
 
 int fg_tree_free(fg_tree *tree) {
     if (tree) {
+        DeviceGuard g(tree->t.device);
+        tree_use(tree->t);
         cudaStreamSynchronize(stream());
         delete tree;
     }
@@ -433,6 +478,8 @@ int fg_tree_export(const fg_tree *tree, int64_t *perm, int64_t *start, int64_t *
                    double *lo, double *hi, double *center, double *weight, double *inf_radius,
                    int64_t *left, int64_t *right) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    DeviceGuard g(tree->t.device);
+    FG_TRY(tree_use(const_cast<TreeDev &>(tree->t)));
     return tree_export(tree->t, perm, start, end, lo, hi, center, weight, inf_radius, left,
                        right);
 }
@@ -448,6 +495,8 @@ __global__ void unpack_points_kernel(int64_t n, int dim, int stride, const doubl
 
 int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    DeviceGuard g(tree->t.device);
+    FG_TRY(tree_use(const_cast<TreeDev &>(tree->t)));
     const TreeDev &t = tree->t;
     DBuf tp, tw;
     if (points) FG_TRY(tp.reserve(sizeof(double) * t.n * t.dim));
@@ -465,15 +514,21 @@ int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
 
 int fg_moments_refresh(fg_tree *tree, double h, int32_t plimit) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
-    // stream-ordered: later engine calls on the same stream see the moments;
+    // stream-ordered: later engine calls on the same stream see the moments
+    // (calls on other streams wait for them through the tree's event);
     // errors of the asynchronous work surface at the next synchronising call
+    DeviceGuard g(tree->t.device);
+    FG_TRY(tree_use(tree->t));
     FG_TRY(moments_refresh(tree->t, h, plimit));
     FG_CUDA_TRY(cudaGetLastError());
+    FG_TRY(tree_mark(tree->t));
     return FG_OK;
 }
 
 int fg_moments_export(const fg_tree *tree, double *out, int32_t *K, double *h, int32_t *order) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
+    DeviceGuard g(tree->t.device);
+    FG_TRY(tree_use(const_cast<TreeDev &>(tree->t)));
     const TreeDev &t = tree->t;
     if (K) *K = t.mom_valid ? t.mom_K : 0;
     if (h) *h = t.mom_valid ? t.mom_h : 0.0;
@@ -486,13 +541,19 @@ static int run_impl(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_
                     int32_t plimit, int64_t b0, int64_t b1, int64_t stride, double *values,
                     fg_counters *counters, double *seconds) {
     FG_REQUIRE(qtree && rtree && values, FG_EINVAL, "null argument");
+    FG_REQUIRE(qtree->t.device == rtree->t.device, FG_EINVAL, "trees live on different devices");
+    DeviceGuard g(qtree->t.device);
+    FG_TRY(tree_use(qtree->t));
+    FG_TRY(tree_use(rtree->t));
     const int64_t m = qtree->t.n;
     const bool out_dev = is_device_ptr(values);
     double *dout = values;
     if (!out_dev) {
-        FG_TRY(g_stage_out.reserve(sizeof(double) * m));
-        dout = g_stage_out.as<double>();
-        if (b0 > 0 || stride > 1 || (b1 >= 0 && b1 < (qtree->t.n + 31) / 32)) {
+        DBuf &so = scratch<StageOut>();
+        FG_TRY(so.reserve(sizeof(double) * m));
+        dout = so.as<double>();
+        FG_TRY(query_blocks(qtree->t));
+        if (b0 > 0 || stride > 1 || (b1 >= 0 && b1 < qtree->t.nqb)) {
             // partial range: keep the caller's other entries
             FG_CUDA_TRY(cudaMemcpyAsync(dout, values, sizeof(double) * m,
                                         cudaMemcpyHostToDevice, stream()));
@@ -525,11 +586,16 @@ static int sweep_impl(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, 
         memcpy(hs.data(), bandwidths, sizeof(double) * nh);
     }
     for (double h : hs) FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
+    FG_REQUIRE(qtree->t.device == rtree->t.device, FG_EINVAL, "trees live on different devices");
+    DeviceGuard g(qtree->t.device);
+    FG_TRY(tree_use(qtree->t));
+    FG_TRY(tree_use(rtree->t));
     const int64_t m = qtree->t.n;
     const bool out_dev = is_device_ptr(values);
-    const bool partial = b0 > 0 || stride > 1 || (b1 >= 0 && b1 < (m + 31) / 32);
+    FG_TRY(query_blocks(qtree->t));
+    const bool partial = b0 > 0 || stride > 1 || (b1 >= 0 && b1 < qtree->t.nqb);
     double *dout = values;
-    static DBuf s_out;
+    DBuf &s_out = scratch<SweepOut>();
     if (!out_dev) {
         FG_TRY(s_out.reserve(sizeof(double) * m * nh));
         dout = s_out.as<double>();
@@ -566,6 +632,8 @@ int fg_run_sweep_range(fg_tree *qtree, fg_tree *rtree, const double *bandwidths,
 
 int fg_query_block_ranges(fg_tree *qtree, int32_t *starts, int32_t *counts) {
     FG_REQUIRE(qtree && starts && counts, FG_EINVAL, "null argument");
+    DeviceGuard g(qtree->t.device);
+    FG_TRY(tree_use(qtree->t));
     FG_TRY(query_blocks(qtree->t));
     const int64_t nb = qtree->t.nqb;
     std::vector<int2> rg(nb);
@@ -584,7 +652,11 @@ int fg_run_audit(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
                  fg_audit_event *events, int64_t capacity, int64_t *nevents) {
     FG_REQUIRE(qtree && rtree && values && nevents, FG_EINVAL, "null argument");
     FG_REQUIRE(capacity >= 0 && (capacity == 0 || events), FG_EINVAL, "bad event buffer");
-    static DBuf s_ev, s_cnt, s_out;
+    FG_REQUIRE(qtree->t.device == rtree->t.device, FG_EINVAL, "trees live on different devices");
+    DeviceGuard g(qtree->t.device);
+    FG_TRY(tree_use(qtree->t));
+    FG_TRY(tree_use(rtree->t));
+    DBuf &s_ev = scratch<AuditEv>(), &s_cnt = scratch<AuditCnt>(), &s_out = scratch<AuditOut>();
     FG_TRY(s_ev.reserve(sizeof(fg_audit_event) * std::max<int64_t>(capacity, 1)));
     FG_TRY(s_cnt.reserve(sizeof(unsigned long long)));
     const AuditSink sink{s_ev.p, s_cnt.as<unsigned long long>(), (long long)capacity};
@@ -613,6 +685,8 @@ int fg_run_audit(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
 
 int fg_query_blocks(fg_tree *qtree, int64_t *nblocks) {
     FG_REQUIRE(qtree && nblocks, FG_EINVAL, "null argument");
+    DeviceGuard g(qtree->t.device);
+    FG_TRY(tree_use(qtree->t));
     FG_TRY(query_blocks(qtree->t));
     *nblocks = qtree->t.nqb;
     return FG_OK;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -45,6 +46,8 @@ struct Status {
         }                             \
     } while (0)
 
+// The calling host thread's engine stream (fg_set_stream; default: the
+// per-thread default stream).  Every call of one thread is ordered on it.
 cudaStream_t stream();
 // keep freed pool memory cached (release threshold = max) on the current device
 void pool_init();
@@ -62,7 +65,11 @@ struct DBuf {
     // Stream-ordered allocation from the device's memory pool (kept warm, see
     // pool_init), so per-sweep trees and scratch cost no cudaMalloc/cudaFree.
     void release() {
-        if (p) cudaFreeAsync(p, stream());
+        if (p && cudaFreeAsync(p, stream()) != cudaSuccess) {
+            cudaGetLastError();  // e.g. the stream is gone (thread exit): free synchronously
+            cudaFree(p);
+            cudaGetLastError();
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -85,6 +92,30 @@ struct DBuf {
     template <class T>
     T *as() const { return reinterpret_cast<T *>(p); }
 };
+
+// Scratch owned by one (host thread, device): engine calls from different host
+// threads, or on different devices, never share a buffer (SPEC.md:487 --
+// concurrent traversals own distinct query trees).  `Tag` names
+// the use site; T is default-constructed on first use.
+template <class T>
+struct PerDevice {
+    std::vector<std::unique_ptr<T>> v;
+    T &get() {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) {
+            cudaGetLastError();
+            dev = 0;
+        }
+        if ((int)v.size() <= dev) v.resize(dev + 1);
+        if (!v[dev]) v[dev].reset(new T());
+        return *v[dev];
+    }
+};
+template <class Tag, class T = DBuf>
+T &scratch() {
+    static thread_local PerDevice<T> m;
+    return m.get();
+}
 
 // true when ptr is device (or managed) memory usable by kernels
 bool is_device_ptr(const void *ptr);
@@ -126,6 +157,14 @@ int iset_count(int dim, int order);
 // Node numbering on the device is BFS (level by level); `pre_of_bfs` maps
 // to the reference's preorder numbering for export.
 struct TreeDev {
+    int device = 0;       // the tree's buffers live on this device
+    // per-handle ordering: work queued on one host thread's stream that later
+    // calls (possibly from another thread/stream) must wait for
+    cudaEvent_t ready = nullptr;
+    bool pending = false;
+    ~TreeDev() {
+        if (ready) cudaEventDestroy(ready);
+    }
     int64_t n = 0;
     int dim = 0, leaf = 25, stride = 0;  // stride: doubles per packed point
     int64_t nnodes = 0;
@@ -172,6 +211,27 @@ struct TreeDev {
     DBuf qb_cost;   // uint64 nqb: cycles per block in the last full run
     DBuf qb_order;  // int nqb
     DBuf qb_keys, qb_sort_tmp, qb_iota;
+};
+
+// Make the calling thread's stream wait for asynchronous work queued on the
+// tree by earlier calls (tree_use), and mark such work (tree_mark).
+int tree_use(TreeDev &t);
+int tree_mark(TreeDev &t);
+
+// Selects a tree's device for the duration of a call, restoring the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
 };
 
 }  // namespace fg

@@ -195,7 +195,8 @@ int mom_items(TreeDev &t) {
     mom_items_count_kernel<<<blocks, 256, 0, stream()>>>(nn, t.node_i.as<int4>(), off);
     size_t tmp = 0;
     FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, off, off, (int)(nn + 1), stream()));
-    static DBuf s_tmp;
+    struct MomItemsTmp;
+    DBuf &s_tmp = scratch<MomItemsTmp>();
     FG_TRY(s_tmp.reserve(tmp + 16));
     count_launch();
     FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(s_tmp.p, tmp, off, off, (int)(nn + 1), stream()));
@@ -217,7 +218,8 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     const int K = T.K, p = T.order;
     const double sc = kSqrt2 * h;
     FG_TRY(mom_items(t));
-    static DBuf s_partial;
+    struct MomPartial;
+    DBuf &s_partial = scratch<MomPartial>();
     FG_TRY(s_partial.reserve(sizeof(double) * (size_t)t.mom_nitems * K));
     const size_t smem = sizeof(double) * 32 * D * kMaxOrder * kMomWarps;
     const int kpl = (K + 31) / 32;
@@ -226,7 +228,10 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
                 : kpl <= 4 ? mom_partial_kernel<D, 4>
                            : mom_partial_kernel<D, kMomKPLMax>;
     const int ki = kpl <= 1 ? 0 : kpl <= 2 ? 1 : kpl <= 4 ? 2 : 3;
-    static int c_grid[kMaxDim + 1][4] = {};
+    struct MomGrid {
+        int g[kMaxDim + 1][4] = {};
+    };
+    auto &c_grid = scratch<MomGrid, MomGrid>().g;  // per device
     if (!c_grid[D][ki]) {
         int dev = 0, sms = 0, occ = 0;
         FG_CUDA_TRY(cudaGetDevice(&dev));
@@ -324,7 +329,8 @@ __global__ void js_combine_kernel(int64_t nn, const int *__restrict__ off,
 template <int D>
 static int node_js_t(TreeDev &t) {
     FG_TRY(mom_items(t));
-    static DBuf s_part;
+    struct JsPart;
+    DBuf &s_part = scratch<JsPart>();
     FG_TRY(s_part.reserve(sizeof(double) * (size_t)std::max(t.mom_nitems, 1) * (D + 2)));
     FG_TRY(t.node_js.reserve(sizeof(double2) * t.nnodes));
     count_launch();
@@ -356,7 +362,7 @@ int node_js(TreeDev &t) {
     return FG_OK;
 }
 
-static DBuf g_rescale_fac;
+struct RescaleFac;
 
 int moments_refresh(TreeDev &t, double h, int plimit) {
     FG_REQUIRE(h > 0.0 && std::isfinite(h), FG_EINVAL, "bandwidth must be positive");
@@ -370,6 +376,7 @@ int moments_refresh(TreeDev &t, double h, int plimit) {
     FG_TRY(t.mom.reserve(sizeof(double) * total));
     if (t.mom0_valid && t.mom_K == K && t.mom_order == plimit) {
         // exact rescaling from the base bandwidth: (h0/h)^{|a|} per coefficient
+        DBuf &g_rescale_fac = scratch<RescaleFac>();
         FG_TRY(g_rescale_fac.reserve(sizeof(double) * K));
         count_launch();
         rescale_factors_kernel<<<1, 256, 0, stream()>>>(K, t.mom0_h / h, T->degrees.as<int>(),
@@ -437,7 +444,8 @@ int moments_multi(TreeDev &t, const double *hs, int nh, int plimit, DBuf &dst) {
         FG_TRY(moments_refresh(t, hs[0], plimit));  // base moments at hs[0]
     const int64_t total = t.nnodes * K;
     FG_TRY(dst.reserve(sizeof(double) * total * nh));
-    static DBuf fac;
+    struct MultiFac;
+    DBuf &fac = scratch<MultiFac>();
     FG_TRY(fac.reserve(sizeof(double) * K * nh));
     RatioList rl;
     for (int j = 0; j < nh; j++) {

@@ -195,11 +195,15 @@ static int launch_naive(const double *dq, int64_t m, const double *dr, int64_t n
     return FG_OK;
 }
 
-static DBuf g_naive_q, g_naive_r, g_naive_part;
+struct NaiveScr {
+    DBuf q, r, part;
+};
 
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
               int dim, const double *hs, int nh, double *d_out) {
     const int S = packed_stride(dim);
+    NaiveScr &ns = scratch<NaiveScr, NaiveScr>();
+    DBuf &g_naive_q = ns.q, &g_naive_r = ns.r, &g_naive_part = ns.part;
     FG_TRY(g_naive_q.reserve(sizeof(double) * m * S));
     FG_TRY(g_naive_r.reserve(sizeof(double) * n * S));
     count_launch();

@@ -144,7 +144,14 @@ __global__ void best_method_kernel(const double *__restrict__ geom, int batch, i
 
 using namespace fg;
 
-static DBuf g_s_a, g_s_b, g_s_c, g_s_d, g_s_out, g_s_pw;
+struct SeriesScr {
+    DBuf a, b, c, d, out, pw;
+};
+#define FG_SERIES_SCRATCH                                                          \
+    SeriesScr &ss_ = scratch<SeriesScr, SeriesScr>();                              \
+    DBuf &g_s_a = ss_.a, &g_s_b = ss_.b, &g_s_c = ss_.c, &g_s_d = ss_.d,          \
+         &g_s_out = ss_.out, &g_s_pw = ss_.pw;                                     \
+    (void)g_s_a; (void)g_s_b; (void)g_s_c; (void)g_s_d; (void)g_s_out; (void)g_s_pw
 
 #define FG_DISPATCH_D(DIM, CALL)                                             \
     switch (DIM) {                                                           \
@@ -164,6 +171,7 @@ extern "C" {
 int fg_series_accumulate(int32_t kind, const double *pts, const double *w,
                          const int64_t *offsets, int32_t batch, int32_t dim,
                          const double *centers, int32_t order, double h, double *coeffs) {
+    FG_SERIES_SCRATCH;
     FG_REQUIRE(batch >= 1 && dim >= 1 && offsets && centers && coeffs, FG_EINVAL, "bad args");
     FG_REQUIRE(order >= 1, FG_EINVAL, "truncation order must be at least 1");
     FG_REQUIRE(h > 0.0, FG_EINVAL, "bandwidth must be positive");
@@ -208,6 +216,7 @@ int fg_series_accumulate(int32_t kind, const double *pts, const double *w,
 int fg_series_eval(int32_t kind, const double *coeffs, int32_t k_stored, const double *centers,
                    int32_t batch, int32_t dim, int32_t order, double h, const double *x,
                    const int64_t *offsets, double *out) {
+    FG_SERIES_SCRATCH;
     FG_REQUIRE(batch >= 1 && dim >= 1 && coeffs && centers && x && offsets && out, FG_EINVAL,
                "bad args");
     FG_REQUIRE(order >= 1 && h > 0.0, FG_EINVAL, "bad order or bandwidth");
@@ -243,6 +252,7 @@ int fg_series_eval(int32_t kind, const double *coeffs, int32_t k_stored, const d
 int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
                         const double *src_centers, const double *dst_centers, int32_t batch,
                         int32_t dim, int32_t order_src, int32_t order, double h, double *out) {
+    FG_SERIES_SCRATCH;
     FG_REQUIRE(batch >= 1 && dim >= 1 && coeffs && src_centers && dst_centers && out,
                FG_EINVAL, "bad args");
     FG_REQUIRE(order >= 1 && order_src >= 1 && h > 0.0, FG_EINVAL, "bad order or bandwidth");
@@ -279,6 +289,7 @@ int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
 }
 
 int fg_best_method(const double *geom, int32_t batch, int32_t dim, int32_t plimit, double *out) {
+    FG_SERIES_SCRATCH;
     FG_REQUIRE(geom && out && batch >= 1 && dim >= 1 && plimit >= 1, FG_EINVAL, "bad args");
     FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
     TailArgs T;

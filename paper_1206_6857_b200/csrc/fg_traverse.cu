@@ -226,7 +226,11 @@ __global__ void block_ranges_kernel(int64_t n, const int *__restrict__ len,
 }
 
 static int device_block_ranges(TreeDev &t, int64_t &nqb) {
-    static DBuf s_len, s_flag, s_idx, s_tmp, s_cnt;
+    struct BlockScr {
+        DBuf len, flag, idx, tmp;
+    };
+    BlockScr &bs = scratch<BlockScr, BlockScr>();
+    DBuf &s_len = bs.len, &s_flag = bs.flag, &s_idx = bs.idx, &s_tmp = bs.tmp;
     const int64_t n = t.n;
     FG_TRY(s_len.reserve(sizeof(int) * (n + 1)));
     FG_TRY(s_flag.reserve(sizeof(int) * (n + 1)));
@@ -249,7 +253,7 @@ static int device_block_ranges(TreeDev &t, int64_t &nqb) {
     count_launch();
     FG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(s_tmp.p, tmp, s_flag.as<int>(), s_idx.as<int>(),
                                               (int)(n + 1), stream()));
-    static int *h_cnt = nullptr;
+    static thread_local int *h_cnt = nullptr;
     if (!h_cnt) FG_CUDA_TRY(cudaMallocHost(&h_cnt, sizeof(int)));
     FG_CUDA_TRY(cudaMemcpyAsync(h_cnt, s_idx.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost,
                                 stream()));
@@ -303,8 +307,12 @@ int query_blocks(TreeDev &t) {
         // non-negative doubles, so their bit patterns sort like the values; the
         // low bits only reorder radii within 2^-20 of each other -- the median
         // drives heuristics only), one pinned read-back
-        static DBuf s_sorted, s_tmp;
-        static double *h_med = nullptr;
+        struct MedScr {
+            DBuf sorted, tmp;
+        };
+        MedScr &ms = scratch<MedScr, MedScr>();
+        DBuf &s_sorted = ms.sorted, &s_tmp = ms.tmp;
+        static thread_local double *h_med = nullptr;
         if (!h_med) FG_CUDA_TRY(cudaMallocHost(&h_med, sizeof(double)));
         FG_TRY(s_sorted.reserve(sizeof(double) * (nqb > 0 ? nqb : 1)));
         const auto *keys = reinterpret_cast<const unsigned long long *>(t.qb_rad.p);
@@ -414,7 +422,8 @@ struct TravScratch {
     DBuf st_node, st_f, ser, work, counters, dbg;
     int grid = 0, cap = 0;
 };
-static TravScratch g_scr;
+// per (host thread, device): concurrent traversals never share scratch
+static TravScratch &trav_scratch() { return scratch<TravScratch, TravScratch>(); }
 
 // Launches with few tasks per resident warp are tail-bound: the last tasks run
 // nearly alone, so per-warp latency (register-starved address rematerialisation,
@@ -452,6 +461,7 @@ static int launch_traverse(TravArgs &A, size_t smem, int64_t nblocks) {
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
     const int cap = A.stack_cap;
+    TravScratch &g_scr = trav_scratch();
     if (g_scr.grid < grid || g_scr.cap != cap) {
         const int64_t warps = grid * kTravWarps;
         FG_TRY(g_scr.st_node.reserve(sizeof(int) * warps * cap));
@@ -497,6 +507,26 @@ static int launch_dispatch_t(int D, TravArgs &A, size_t smem, int64_t nb) {
 
 static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
     return A.audit ? launch_dispatch_t<true>(D, A, smem, nb) : launch_dispatch_t<false>(D, A, smem, nb);
+}
+
+// FP32 base cases for these bandwidths?
+static int fp32_enabled(const TreeDev &q, const TreeDev &r, const double *hs, int nh, double eps) {
+    int fp32 = g_fp32_base;
+    if (const char *env = getenv("FG_FP32_BASE")) fp32 = atoi(env);
+    if (!q.fp32_ok || !r.fp32_ok || !(eps > 0.0)) fp32 = 0;
+    for (int j = 0; j < nh; j++)
+        if (!(fabs(-1.4426950408889634 / (2.0 * hs[j] * hs[j])) < 1e30)) fp32 = 0;
+    return fp32;
+}
+
+// Per-tree preparation the traversal needs (each computed once per tree and
+// cached): query blocks, the Jensen node statistics, the anchored FP32 records.
+// Queued before a launch's timing window so that window holds the traversal.
+static int prepare_traversal(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps) {
+    FG_TRY(query_blocks(q));
+    if (!getenv("FG_NO_JENSEN")) FG_TRY(node_js(r));
+    if (fp32_enabled(q, r, hs, nh, eps) && q.dim < 5) FG_TRY(fp32_pack(r));
+    return FG_OK;
 }
 
 // Queue one traversal launch over nh bandwidths (tasks = (bandwidth, query
@@ -581,16 +611,13 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
                                     warp_fixed_doubles<7>(), warp_fixed_doubles<8>()};
         smem = sizeof(double) * (fixd[D] + ((A.K + 1) & ~1)) *kTravWarps;
     }
+    TravScratch &g_scr = trav_scratch();
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
     A.work = g_scr.work.as<unsigned long long>();
     FG_CUDA_TRY(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * kCounters * nh, stream()));
     // FP32 base cases: a share kFp32Share of eps
     // is reserved for their rounding error, the rest drives the traversal
-    int fp32 = g_fp32_base;
-    if (const char *env = getenv("FG_FP32_BASE")) fp32 = atoi(env);
-    if (!q.fp32_ok || !r.fp32_ok || !(eps > 0.0)) fp32 = 0;
-    for (int j = 0; j < nh; j++)
-        if (!(fabs(-1.4426950408889634 / (2.0 * hs[j] * hs[j])) < 1e30)) fp32 = 0;
+    const int fp32 = fp32_enabled(q, r, hs, nh, eps);
     if (fp32 && D < 5) {  // anchored FP32 records (the direct stream at D >= 5 needs none)
         FG_TRY(fp32_pack(r));
         A.r_pf = r.pf.as<float>();
@@ -697,6 +724,9 @@ static void fill_counters(const unsigned long long *c, fg_counters *o) {
     o->h2l_prunes = (int64_t)c[5];
     o->exact_pairs = (int64_t)c[6];
     o->fp32_pairs = (int64_t)c[7];
+    o->hermite_evals = (int64_t)c[9];
+    o->hermite_terms = (int64_t)c[11];
+    o->local_evals = (int64_t)c[10];
 }
 
 int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int plimit,
@@ -719,8 +749,10 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
         FG_CUDA_TRY(cudaEventCreate(&e1));
         FG_CUDA_TRY(cudaMallocHost(&cnt, sizeof(unsigned long long) * kCounters));
     }
+    TravScratch &g_scr = trav_scratch();
     FG_TRY(g_scr.counters.reserve(sizeof(unsigned long long) * kCounters));
     const double *mom = r.mom.as<double>();
+    FG_TRY(prepare_traversal(q, r, &h, 1, eps));
     FG_CUDA_TRY(cudaEventRecord(e0, stream()));
     FG_TRY(queue_traversal(q, r, 1, &h, &mom, eps, mode, plimit, b0, b1, stride, &d_values,
                            g_scr.counters.as<unsigned long long>(), !audit, audit));
@@ -754,10 +786,14 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
     FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
     for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const bool series = mode == FG_DITO;
-    static DBuf s_mom, s_cnt;
+    struct SweepScr {
+        DBuf mom, cnt;
+    };
+    SweepScr &ss = scratch<SweepScr, SweepScr>();
+    DBuf &s_mom = ss.mom, &s_cnt = ss.cnt;
     static thread_local std::vector<cudaEvent_t> evs;
     const int nchunk = (nh + kMaxSweep - 1) / kMaxSweep;
-    while ((int)evs.size() < nchunk + 1) {
+    while ((int)evs.size() < 2 * nchunk) {
         cudaEvent_t e;
         FG_CUDA_TRY(cudaEventCreate(&e));
         evs.push_back(e);
@@ -765,7 +801,6 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
     FG_TRY(s_cnt.reserve(sizeof(unsigned long long) * kCounters * nh));
     FG_TRY(query_blocks(q));
     const int64_t m = q.n;
-    FG_CUDA_TRY(cudaEventRecord(evs[0], stream()));
     for (int c = 0; c < nchunk; c++) {
         const int j0 = c * kMaxSweep, nj = std::min(kMaxSweep, nh - j0);
         std::vector<const double *> moms(nj, nullptr);
@@ -778,9 +813,13 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
             for (int j = 0; j < nj; j++)
                 moms[j] = s_mom.as<double>() + (size_t)j * r.nnodes * r.mom_K;
         }
+        // the event window holds the traversal launch alone (the moment
+        // rescaling above and the per-tree preparation are outside it)
+        FG_TRY(prepare_traversal(q, r, hs + j0, nj, eps));
+        FG_CUDA_TRY(cudaEventRecord(evs[2 * c], stream()));
         FG_TRY(queue_traversal(q, r, nj, hs + j0, moms.data(), eps, mode, plimit, b0, b1, stride,
                                outs.data(), s_cnt.as<unsigned long long>() + kCounters * j0, false));
-        FG_CUDA_TRY(cudaEventRecord(evs[c + 1], stream()));
+        FG_CUDA_TRY(cudaEventRecord(evs[2 * c + 1], stream()));
     }
     std::vector<unsigned long long> hc((size_t)kCounters * nh);
     FG_CUDA_TRY(cudaMemcpyAsync(hc.data(), s_cnt.p, sizeof(unsigned long long) * kCounters * nh,
@@ -789,7 +828,7 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
     for (int c = 0; c < nchunk; c++) {
         const int j0 = c * kMaxSweep, nj = std::min(kMaxSweep, nh - j0);
         float ms = 0.f;
-        FG_CUDA_TRY(cudaEventElapsedTime(&ms, evs[c], evs[c + 1]));
+        FG_CUDA_TRY(cudaEventElapsedTime(&ms, evs[2 * c], evs[2 * c + 1]));
         // one launch serves nj bandwidths: split its time by their summed
         // per-block cycles
         double cyc = 0.0;

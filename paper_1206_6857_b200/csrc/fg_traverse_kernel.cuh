@@ -35,7 +35,7 @@ constexpr int kDbgFields = 16;  // per-block debug record (FG_DEBUG_BLOCKS)
 #ifndef FG_PHASE_PROF
 #define FG_PHASE_PROF 0  // per-block phase cycle counters in the debug record
 #endif
-constexpr int kCounters = 16;  // per-bandwidth device counter slots (9 used)
+constexpr int kCounters = 16;  // per-bandwidth device counter slots (12 used)
 struct TravH {
     double h, neg_inv, inv_h, sc, inv_sc, eps;
     double fp32_rho;              // relative error allowed per FP32 leaf item (0: FP64 only)
@@ -952,7 +952,8 @@ traverse_kernel(const TravArgs A) {
                           A.qb_wsum[b] * fg_exp_fast(dsq * H.neg_inv, s_tab) * (1.0 - 1e-12));
         }
         double tokens = 0.0;    // per block (uniform)
-        unsigned c_vis = 0, c_base = 0, c_fd = 0, c_pairs = 0, c_f32 = 0;
+        unsigned c_vis = 0, c_base = 0, c_fd = 0;
+        unsigned long long c_pairs = 0, c_f32 = 0;  // up to 64 x N_ref per task
         int nh = 0, no = 0;  // deferred series items: Hermite from the front, others from the back
 
         // root entry
@@ -1175,7 +1176,7 @@ traverse_kernel(const TravArgs A) {
                 stage_window<D>(A.r_pw, f32_mask, off, rcm, ni.x, 0, sbuf);
                 if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
                 const double abs_sum = warp_sum(mine ? abs32 : 0.0);
-                c_f32 += (unsigned)qn * (unsigned)total;
+                c_f32 += (unsigned long long)qn * (unsigned)total;
                 c_base += __popc(f32_mask);
                 // both query slots about the block centroid, packed (slot 0, slot 1)
                 unsigned long long xf2[D];
@@ -1247,7 +1248,7 @@ traverse_kernel(const TravArgs A) {
                 }
                 if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
                 const double abs_sum = warp_sum(mine ? abs32 : 0.0);
-                c_f32 += (unsigned)qn * (unsigned)warp_sum(rcm);
+                c_f32 += (unsigned long long)qn * (unsigned)warp_sum(rcm);
                 c_base += __popc(f32_mask);
                 // both query slots about the block centroid, packed (slot 0, slot 1)
                 unsigned long long xf2[D];
@@ -1362,13 +1363,14 @@ traverse_kernel(const TravArgs A) {
                 }
                 if (A.use_tokens) tokens += wri;
                 c_base++;
-                c_pairs += (unsigned)(qn * rc);
+                c_pairs += (unsigned long long)(qn * rc);
             }
             PH_MARK(5);
         }
 
         // ---- deferred series contributions, then the post pass (dito_post, :253-281)
         unsigned c_dh = 0, c_dl = 0, c_h2l = 0;
+        unsigned long long c_hq = 0, c_lq = 0, c_ht = 0;
         bool local_used = false;
         if (nh + no > 0) {
             double x[kQPL][D];
@@ -1399,6 +1401,7 @@ traverse_kernel(const TravArgs A) {
             }
             for (int i = 0; i < nh; i++) {
                 const int p = sl[i].y & 0xff;
+                c_ht += (unsigned long long)A.kp[p] * qn;
                 if (ring) {
                     if (i + kRing - 1 < nh) stage_item(i + kRing - 1);
                     __pipeline_commit();
@@ -1434,6 +1437,7 @@ traverse_kernel(const TravArgs A) {
                 }
             }
             c_dh += nh;
+            c_hq += (unsigned long long)nh * qn;
             // direct-local and H2L items accumulate into the block's local expansion
             for (int k = 0; k < no; k++) {
                 const int2 e = sl[A.stack_cap - 1 - k];
@@ -1453,6 +1457,7 @@ traverse_kernel(const TravArgs A) {
                 __syncwarp();
             }
             if (local_used) {
+                c_lq += qn;
 #pragma unroll 1
                 for (int qi = 0; qi < nq; qi++) {
                     double xq[D];
@@ -1486,9 +1491,12 @@ traverse_kernel(const TravArgs A) {
             atomicAdd(cn + 3, (unsigned long long)c_dh);
             atomicAdd(cn + 4, (unsigned long long)c_dl);
             atomicAdd(cn + 5, (unsigned long long)c_h2l);
-            atomicAdd(cn + 6, (unsigned long long)c_pairs);
-            atomicAdd(cn + 7, (unsigned long long)c_f32);
+            atomicAdd(cn + 6, c_pairs);
+            atomicAdd(cn + 7, c_f32);
             atomicAdd(cn + 8, cyc);
+            if (c_hq) atomicAdd(cn + 9, c_hq);
+            if (c_lq) atomicAdd(cn + 10, c_lq);
+            if (c_ht) atomicAdd(cn + 11, c_ht);
         }
         __syncwarp();
     }

@@ -229,7 +229,10 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
     const int root_nch = (int)((n + kChunk - 1) / kChunk);
 
     // resident grid for the cooperative launch (cached per dimension)
-    static int grid_cache[kMaxDim + 1] = {0};
+    struct GridCache {
+        int g[kMaxDim + 1] = {0};
+    };
+    auto &grid_cache = scratch<GridCache, GridCache>().g;  // per device
     int dev = 0;
     FG_CUDA_TRY(cudaGetDevice(&dev));
     if (!grid_cache[D]) {
@@ -274,7 +277,7 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
         double2 rootwr;
         int lb[kMaxLevels + 2];
     };
-    static Readback *rb = nullptr;
+    static thread_local Readback *rb = nullptr;
     if (!rb) FG_CUDA_TRY(cudaMallocHost(&rb, sizeof(Readback)));
     FG_CUDA_TRY(cudaMemcpyAsync(rb->ctl, B.ctl.p, sizeof(rb->ctl), cudaMemcpyDeviceToHost, stream()));
     FG_CUDA_TRY(cudaMemcpyAsync(&rb->bad, B.bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
@@ -308,7 +311,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_REQUIRE(n < (int64_t)1 << 30, FG_EUNSUPPORTED, "more than 2^30 points per tree");
     // build scratch is kept between builds (grow-only): a per-step tree costs
     // no allocation calls
-    static BuildBufs B;
+    BuildBufs &B = scratch<BuildBufs, BuildBufs>();
     const int64_t nmax = std::max<int64_t>(2 * n, 2);
     const int64_t maxchunks = n / kChunk + nmax + 2;
     for (int k = 0; k < 2; k++) {

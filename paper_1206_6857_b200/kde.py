@@ -75,12 +75,11 @@ def register_torch_ops() -> bool:
         return True
 
     def _on_current_stream(fn):
+        # the engine runs on torch's current stream; the thread's previous
+        # engine stream is restored afterwards
         def wrapped(*args):
-            _lib.set_stream(torch.cuda.current_stream().cuda_stream)
-            try:
+            with _lib.torch_stream(torch.empty(0, device="cuda")):
                 return fn(*args)
-            finally:
-                _lib.set_stream(None)
         return wrapped
 
     @torch.library.custom_op(

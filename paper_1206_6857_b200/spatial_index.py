@@ -306,8 +306,9 @@ def build_tree_device(points, weights=None, leaf_threshold: int = 25) -> KdTree:
         raise ValueError("points must be a non-empty (N, D) array")
     w = None if weights is None else _lib.as_f64(weights).reshape(-1)
     h = ctypes.c_void_p()
-    _lib.call("fg_tree_build", _lib.ptr(pts), _lib.ptr(w), pts.shape[0], pts.shape[1],
-              int(leaf_threshold), ctypes.byref(h))
+    with _lib.torch_stream(pts, w):
+        _lib.call("fg_tree_build", _lib.ptr(pts), _lib.ptr(w), pts.shape[0], pts.shape[1],
+                  int(leaf_threshold), ctypes.byref(h))
     return KdTree(h.value, None, leaf_threshold)
 
 

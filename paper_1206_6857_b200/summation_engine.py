@@ -54,6 +54,9 @@ class TraversalCounters:
     h2l_prunes: int = 0
     exact_pairs: int = 0
     fp32_pairs: int = 0
+    hermite_evals: int = 0
+    hermite_terms: int = 0
+    local_evals: int = 0
 
     @property
     def prunes(self) -> int:
@@ -72,7 +75,8 @@ class TraversalCounters:
     @classmethod
     def _from_c(cls, c: _lib.fg_counters) -> "TraversalCounters":
         return cls(c.pair_visits, c.base_cases, c.fd_prunes, c.hermite_prunes, c.local_prunes,
-                   c.h2l_prunes, c.exact_pairs, c.fp32_pairs)
+                   c.h2l_prunes, c.exact_pairs, c.fp32_pairs, c.hermite_evals,
+                   c.hermite_terms, c.local_evals)
 
 
 @dataclass
@@ -108,9 +112,11 @@ def naive_sum(queries, references, weights, h, out=None) -> ResultVector:
     hs = np.atleast_1d(np.asarray(h, dtype=float))
     if np.any(hs <= 0.0):
         raise ValueError("bandwidth must be positive")
-    vals = out if out is not None else np.empty((hs.shape[0], m))
-    _lib.call("fg_naive_sum", _lib.ptr(q), m, _lib.ptr(r), _lib.ptr(w), n, dim,
-              _lib.ptr(hs), hs.shape[0], _lib.ptr(vals))
+    shapes = [(hs.shape[0], m)] + ([(m,)] if hs.shape[0] == 1 else [])
+    vals = _lib.check_out(out, shapes) if out is not None else np.empty((hs.shape[0], m))
+    with _lib.torch_stream(q, r, w, vals):
+        _lib.call("fg_naive_sum", _lib.ptr(q), m, _lib.ptr(r), _lib.ptr(w), n, dim,
+                  _lib.ptr(hs), hs.shape[0], _lib.ptr(vals))
     if out is None and np.ndim(h) == 0:
         vals = vals[0]
     counters = TraversalCounters(exact_pairs=int(m) * int(n) * int(hs.shape[0]))
@@ -199,7 +205,7 @@ def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: s
                            rtree.moments_order is None or rtree.moments_order < plimit):
         raise RuntimeError("reference moments missing or stale; call refresh_moments "
                            "for this bandwidth first")
-    vals = out if out is not None else np.empty(qtree.n)
+    vals = _lib.check_out(out, [(qtree.n,)]) if out is not None else np.empty(qtree.n)
     if audit:
         cnt, secs, ledger, _ = _audit_run(config, qtree, rtree, mode, plimit, vals)
         if out is None:
@@ -207,15 +213,16 @@ def _run_tree_algorithm(config: RunConfig, qtree: KdTree, rtree: KdTree, mode: s
         return ResultVector(vals, secs, TraversalCounters._from_c(cnt), ledger)
     cnt = _lib.fg_counters()
     secs = ctypes.c_double()
-    if block_range is None:
-        _lib.call("fg_run", qtree.handle, rtree.handle, float(config.bandwidth),
-                  float(config.epsilon), _lib.MODES[mode], int(plimit), _lib.ptr(vals),
-                  ctypes.byref(cnt), ctypes.byref(secs))
-    else:
-        b0, b1, stride = block_range
-        _lib.call("fg_run_range", qtree.handle, rtree.handle, float(config.bandwidth),
-                  float(config.epsilon), _lib.MODES[mode], int(plimit), int(b0), int(b1),
-                  int(stride), _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
+    with _lib.torch_stream(vals):
+        if block_range is None:
+            _lib.call("fg_run", qtree.handle, rtree.handle, float(config.bandwidth),
+                      float(config.epsilon), _lib.MODES[mode], int(plimit), _lib.ptr(vals),
+                      ctypes.byref(cnt), ctypes.byref(secs))
+        else:
+            b0, b1, stride = block_range
+            _lib.call("fg_run_range", qtree.handle, rtree.handle, float(config.bandwidth),
+                      float(config.epsilon), _lib.MODES[mode], int(plimit), int(b0), int(b1),
+                      int(stride), _lib.ptr(vals), ctypes.byref(cnt), ctypes.byref(secs))
     if out is None:
         qtree._set_run_values(vals)
     return ResultVector(vals, secs.value, TraversalCounters._from_c(cnt), None)
@@ -261,22 +268,25 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
         raise ValueError("bandwidths must be positive")
     plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
     nh = hs.shape[0]
-    vals = out if out is not None else (np.empty((nh, qtree.n)) if block_range is None
-                                        else np.zeros((nh, qtree.n)))
+    shapes = [(nh, qtree.n)] + ([(qtree.n,)] if nh == 1 else [])
+    vals = _lib.check_out(out, shapes) if out is not None else (
+        np.empty((nh, qtree.n)) if block_range is None else np.zeros((nh, qtree.n)))
     cnt = (_lib.fg_counters * nh)()
     secs = np.zeros(nh)
-    if block_range is None:
-        _lib.call("fg_run_sweep", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
-                  float(config.epsilon), _lib.MODES[config.algorithm], int(plimit),
-                  _lib.ptr(vals), cnt, _lib.ptr(secs))
-    else:
-        b0, b1, stride = block_range
-        _lib.call("fg_run_sweep_range", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
-                  float(config.epsilon), _lib.MODES[config.algorithm], int(plimit), int(b0),
-                  int(b1), int(stride), _lib.ptr(vals), cnt, _lib.ptr(secs))
+    with _lib.torch_stream(vals):
+        if block_range is None:
+            _lib.call("fg_run_sweep", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
+                      float(config.epsilon), _lib.MODES[config.algorithm], int(plimit),
+                      _lib.ptr(vals), cnt, _lib.ptr(secs))
+        else:
+            b0, b1, stride = block_range
+            _lib.call("fg_run_sweep_range", qtree.handle, rtree.handle, _lib.ptr(hs), nh,
+                      float(config.epsilon), _lib.MODES[config.algorithm], int(plimit),
+                      int(b0), int(b1), int(stride), _lib.ptr(vals), cnt, _lib.ptr(secs))
     if config.algorithm == "dito":
         rtree._moments_refreshed(float(hs[-1]), plimit)
-    return [ResultVector(vals[j], float(secs[j]), TraversalCounters._from_c(cnt[j]), None)
+    rows = vals.reshape(nh, qtree.n)
+    return [ResultVector(rows[j], float(secs[j]), TraversalCounters._from_c(cnt[j]), None)
             for j in range(nh)]
 
 
