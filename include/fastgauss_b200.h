@@ -197,6 +197,13 @@ int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
                         const double *src_centers, const double *dst_centers, int32_t batch,
                         int32_t dim, int32_t order_src, int32_t order, double h,
                         double *out);
+/* The graded-lex index set |alpha| < order (kernel_math.py:111-209) the
+ * kernels use, exported from the same host tables (no GPU needed): K, digits
+ * (K x dim), degrees (K), alpha! (K), prefix counts (order + 1), and the shift
+ * pairs (a, b, s) with digits_a + digits_b = digits_s, degree < order
+ * (npairs x 3).  Every output pointer is nullable (query K / npairs first). */
+int fg_iset_export(int32_t dim, int32_t order, int32_t *K, int32_t *digits, int32_t *degrees,
+                   double *fact, int32_t *prefix, int32_t *npairs, int32_t *pairs);
 /* best_method (error_bounds.py:168-230) on `batch` geometries:
  * geom rows = (min_sq, max_sq, r_ref, r_query, w_ref, n_query, n_ref, h, maxerr);
  * out rows = (method 0/2/3/4, order, bound, cost) as doubles. */

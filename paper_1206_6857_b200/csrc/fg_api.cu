@@ -175,6 +175,53 @@ static void compositions(int total, int dims, std::vector<int> &prefix,
     }
 }
 
+// Host half of the tables (graded-lex digits, degrees, alpha!, prefix counts,
+// shift pairs; kernel_math.py:111-209): no device work, so fg_iset_export
+// serves CPU-only callers from the same source as the kernels' tables.
+static void host_tables(int dim, int order, SeriesTables &T, std::vector<std::vector<int>> &idx) {
+    T.dim = dim;
+    T.order = order;
+    std::vector<int> prefix;
+    idx.clear();
+    for (int deg = 0; deg < order; deg++) compositions(deg, dim, prefix, idx);
+    const int K = (int)idx.size();
+    T.K = K;
+    T.h_digits.assign((size_t)K * kMaxDim, 0);
+    T.h_degrees.resize(K);
+    T.h_fact.resize(K);
+    for (int k = 0; k < K; k++) {
+        int deg = 0;
+        double f = 1.0;
+        for (int d = 0; d < dim; d++) {
+            T.h_digits[(size_t)k * kMaxDim + d] = (uint8_t)idx[k][d];
+            deg += idx[k][d];
+            f *= fact_d(idx[k][d]);
+        }
+        T.h_degrees[k] = deg;
+        T.h_fact[k] = f;
+    }
+    T.h_prefix.resize(order + 1);
+    for (int p = 0; p <= order; p++) {
+        int c = 0;
+        while (c < K && T.h_degrees[c] < p) c++;
+        T.h_prefix[p] = c;
+    }
+    std::map<std::vector<int>, int> pos;
+    for (int k = 0; k < K; k++) pos[idx[k]] = k;
+    T.h_pair_a.clear();
+    T.h_pair_b.clear();
+    T.h_pair_s.clear();
+    for (int a = 0; a < K; a++)
+        for (int b = 0; b < K; b++) {
+            if (T.h_degrees[a] + T.h_degrees[b] >= order) continue;
+            std::vector<int> sv(dim);
+            for (int d = 0; d < dim; d++) sv[d] = idx[a][d] + idx[b][d];
+            T.h_pair_a.push_back(a);
+            T.h_pair_b.push_back(b);
+            T.h_pair_s.push_back(pos[sv]);
+        }
+}
+
 static std::mutex g_tab_mu;
 // tables per (device, dim, order): device buffers belong to one device
 static std::map<std::tuple<int, int, int>, std::unique_ptr<SeriesTables>> g_tables;
@@ -200,46 +247,11 @@ const SeriesTables *series_tables(int dim, int order, int *status) {
         return nullptr;
     }
     auto T = std::make_unique<SeriesTables>();
-    T->dim = dim;
-    T->order = order;
     std::vector<std::vector<int>> idx;
-    std::vector<int> prefix;
-    for (int deg = 0; deg < order; deg++) compositions(deg, dim, prefix, idx);
-    const int K = (int)idx.size();
-    T->K = K;
-    T->h_digits.assign((size_t)K * kMaxDim, 0);
-    T->h_degrees.resize(K);
-    T->h_fact.resize(K);
+    host_tables(dim, order, *T, idx);
+    const int K = T->K;
     std::vector<double> inv(K);
-    for (int k = 0; k < K; k++) {
-        int deg = 0;
-        double f = 1.0;
-        for (int d = 0; d < dim; d++) {
-            T->h_digits[(size_t)k * kMaxDim + d] = (uint8_t)idx[k][d];
-            deg += idx[k][d];
-            f *= fact_d(idx[k][d]);
-        }
-        T->h_degrees[k] = deg;
-        T->h_fact[k] = f;
-        inv[k] = 1.0 / f;
-    }
-    T->h_prefix.resize(order + 1);
-    for (int p = 0; p <= order; p++) {
-        int c = 0;
-        while (c < K && T->h_degrees[c] < p) c++;
-        T->h_prefix[p] = c;
-    }
-    std::map<std::vector<int>, int> pos;
-    for (int k = 0; k < K; k++) pos[idx[k]] = k;
-    for (int a = 0; a < K; a++)
-        for (int b = 0; b < K; b++) {
-            if (T->h_degrees[a] + T->h_degrees[b] >= order) continue;
-            std::vector<int> s(dim);
-            for (int d = 0; d < dim; d++) s[d] = idx[a][d] + idx[b][d];
-            T->h_pair_a.push_back(a);
-            T->h_pair_b.push_back(b);
-            T->h_pair_s.push_back(pos[s]);
-        }
+    for (int k = 0; k < K; k++) inv[k] = 1.0 / T->h_fact[k];
     const int np = (int)T->h_pair_a.size();
     T->npairs = np;
     // CSR by s (stable in pair order) and by a
@@ -699,6 +711,32 @@ int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
     FG_REQUIRE(block_stride >= 1, FG_EINVAL, "block stride must be >= 1");
     return run_impl(qtree, rtree, h, eps, mode, plimit, block_begin, block_end, block_stride,
                     values, counters, seconds);
+}
+
+int fg_iset_export(int32_t dim, int32_t order, int32_t *K, int32_t *digits, int32_t *degrees,
+                   double *fact, int32_t *prefix, int32_t *npairs, int32_t *pairs) {
+    FG_REQUIRE(dim >= 1 && dim <= kMaxDim && order >= 1 && iset_count(dim, order) <= 4096,
+               FG_EINVAL, "index set: need 1 <= dim <= 8, order >= 1, C(dim+order-1, dim) <= 4096");
+    SeriesTables T;
+    std::vector<std::vector<int>> idx;
+    host_tables(dim, order, T, idx);
+    if (K) *K = T.K;
+    if (npairs) *npairs = (int32_t)T.h_pair_a.size();
+    for (int k = 0; k < T.K; k++) {
+        for (int d = 0; d < dim; d++)
+            if (digits) digits[(size_t)k * dim + d] = idx[k][d];
+        if (degrees) degrees[k] = T.h_degrees[k];
+        if (fact) fact[k] = T.h_fact[k];
+    }
+    if (prefix)
+        for (int p = 0; p <= order; p++) prefix[p] = T.h_prefix[p];
+    if (pairs)
+        for (size_t i = 0; i < T.h_pair_a.size(); i++) {
+            pairs[3 * i] = T.h_pair_a[i];
+            pairs[3 * i + 1] = T.h_pair_b[i];
+            pairs[3 * i + 2] = T.h_pair_s[i];
+        }
+    return FG_OK;
 }
 
 }  // extern "C"

@@ -89,3 +89,29 @@ def test_product_path_fails_loudly_without_gpu():
         fg.naive_sum(np.zeros((2, 2)), np.zeros((2, 2)), np.ones(2), 0.5)
     with pytest.raises(RuntimeError):
         fg.build_tree(fg.PointStore(np.random.default_rng(0).random((10, 2))))
+
+
+def test_out_buffers_are_validated_before_the_c_abi():
+    """A caller-supplied ``out`` must be float64, C-contiguous, writeable and
+    exactly shaped before its raw pointer reaches the C ABI (else ValueError):
+    a wrong buffer would otherwise be overrun by the engine's copies."""
+    import paper_1206_6857_b200 as fg
+
+    q = np.zeros((5, 2))
+    r = np.zeros((4, 2))
+    w = np.ones(4)
+    bad = [np.zeros(5, np.float32), np.zeros(4), np.zeros((2, 5)),
+           np.zeros((5, 2))[:, 0], np.zeros(10)[::2]]
+    ro = np.zeros(5)
+    ro.flags.writeable = False
+    bad.append(ro)
+    for out in bad:
+        with pytest.raises(ValueError):
+            fg.naive_sum(q, r, w, 0.5, out=out)
+    with pytest.raises(ValueError):
+        fg.naive_sum(q, r, w, [0.5, 1.0], out=np.zeros(5))  # needs (2, 5)
+    torch = pytest.importorskip("torch")
+    with pytest.raises(ValueError):
+        fg.naive_sum(q, r, w, 0.5, out=torch.zeros(5, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        fg.naive_sum(q, r, w, 0.5, out=torch.zeros(10, dtype=torch.float64)[::2])

@@ -1,10 +1,12 @@
 """Multi-rank query sharding on CPU (gloo, world_size 2).
 
 The engine itself needs a GPU; these tests exercise the host-side sharding
-logic of paper_1206_6857_b200.distributed with the CPU oracle standing in for
-the per-shard compute: the round-robin block deal covers every query exactly
-once, and the collective sum over disjoint supports reproduces the full
-result bit-for-bit.
+logic of paper_1206_6857_b200.distributed -- the engine's own query-block
+partition (``query_block_ranges`` restates fg_traverse.cu's block rule; a gpu
+test pins it to ``fg_query_block_ranges``) dealt round-robin to ranks -- with
+the CPU oracle's DFS DITO standing in for each rank's per-shard compute: the
+deal covers every query exactly once, the collective sum over disjoint
+supports assembles the full vector exactly, and every query is within eps.
 """
 
 import os
@@ -43,13 +45,17 @@ def _worker(rank, world, port, result_path):
     ranges = D.query_block_ranges(ex["start"], ex["end"], ex["left"], ex["right"])
     mine = D.owned_queries(ranges, ex["perm"], rank, world)
     vals = torch.zeros(pts.shape[0], dtype=torch.float64)
+    hits = torch.zeros(pts.shape[0], dtype=torch.float64)
     if mine.size:
-        vals[torch.from_numpy(mine)] = torch.from_numpy(
-            oracle.naive_sum(pts[mine], pts, w, 0.1))
+        tree.refresh_moments(0.1, 6)
+        v, _ = oracle.run_sharded("dito", pts[mine], tree, 0.1, 0.01, threads=1)
+        vals[torch.from_numpy(mine)] = torch.from_numpy(v)
+        hits[torch.from_numpy(mine)] = 1.0
     D.gather_disjoint(vals)
+    D.gather_disjoint(hits)
     if rank == 0:
         full = oracle.naive_sum(pts, pts, w, 0.1)
-        np.save(result_path, np.stack([vals.numpy(), full]))
+        np.save(result_path, np.stack([vals.numpy(), full, hits.numpy()]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -65,6 +71,12 @@ def test_blocks_partition_queries():
         ex = t.export()
         ranges = D.query_block_ranges(ex["start"], ex["end"], ex["left"], ex["right"])
         assert all(1 <= c <= 64 for _, c in ranges)
+        # every block lies inside one maximal node of <= lim points (or a leaf)
+        lim = max(64, min(4096, n // 16))
+        size = ex["end"] - ex["start"]
+        for s, c in ranges:
+            inside = (ex["start"] <= s) & (s + c <= ex["end"])
+            assert np.any(inside & ((size <= lim) | (ex["left"] < 0)))
         pos = np.concatenate([np.arange(s, s + c) for s, c in ranges])
         np.testing.assert_array_equal(pos, np.arange(n))  # tree order, exact cover
         for world in (1, 2, 3, 8):
@@ -84,5 +96,6 @@ def test_shard_blocks_validation():
 def test_gloo_world2_gather_matches_full(tmp_path):
     out = str(tmp_path / "res.npy")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    got, full = np.load(out)
-    np.testing.assert_array_equal(got, full)
+    got, full, hits = np.load(out)
+    np.testing.assert_array_equal(hits, np.ones_like(hits))  # every query exactly once
+    assert np.max(np.abs(got - full) / full) <= 0.01
