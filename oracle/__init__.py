@@ -61,6 +61,7 @@ def lib():
                                     ctypes.c_int, ctypes.c_double, _D]
         L.fgo_naive_sum_mt.argtypes = [_D, ctypes.c_int64, _D, _D, ctypes.c_int64,
                                        ctypes.c_int, ctypes.c_double, _D, ctypes.c_int]
+        L.fgo_naive_sum_comp_mt.argtypes = L.fgo_naive_sum_mt.argtypes
         L.fgo_best_method.argtypes = [ctypes.c_double] * 5 + [ctypes.c_int64] * 2 + [
             ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int,
             _I32, _I32, _D, _D]
@@ -99,15 +100,19 @@ def _f64(a, shape=None):
 
 
 # ----------------------------------------------------------------- engine
-def naive_sum(queries, references, weights, h, threads: int = 1):
-    """summation_engine.py:122-154 restated (exact FP64 sums)."""
+def naive_sum(queries, references, weights, h, threads: int = 1, compensated: bool = False):
+    """summation_engine.py:122-154 restated (exact FP64 sums).  ``compensated``
+    sums the same terms with Neumaier compensation (full-size fixtures)."""
     q = _f64(queries)
     if q.ndim == 1:
         q = q.reshape(1, -1)
     r = _f64(references)
     w = _f64(weights).reshape(-1)
     out = np.empty(q.shape[0])
-    if threads == 1:
+    if compensated:
+        lib().fgo_naive_sum_comp_mt(_dp(q), q.shape[0], _dp(r), _dp(w), r.shape[0], q.shape[1],
+                                    float(h), _dp(out), int(threads))
+    elif threads == 1:
         lib().fgo_naive_sum(_dp(q), q.shape[0], _dp(r), _dp(w), r.shape[0], q.shape[1],
                             float(h), _dp(out))
     else:

@@ -420,6 +420,36 @@ void fgo_naive_sum(const double *q, int64_t m, const double *r, const double *w,
     }
 }
 
+/* naive_sum with Neumaier-compensated accumulation: the same terms, summed to
+ * within a few ulp of their exact sum whatever n -- the fixture for the
+ * exhaustive kernel at full BASELINE sizes (a plain sequential sum of 4e6
+ * terms carries ~1e-12 of its own rounding). */
+void fgo_naive_sum_comp_mt(const double *q, int64_t m, const double *r, const double *w,
+                           int64_t n, int dim, double h, double *out, int nthreads) {
+    const double neg = -0.5 / (h * h);
+#ifdef _OPENMP
+    if (nthreads < 1) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 16) num_threads(nthreads)
+#endif
+    for (int64_t i = 0; i < m; i++) {
+        const double *x = q + i * dim;
+        double s = 0.0, c = 0.0;
+        for (int64_t j = 0; j < n; j++) {
+            const double *y = r + j * dim;
+            double d2 = 0.0;
+            for (int d = 0; d < dim; d++) {
+                const double diff = x[d] - y[d];
+                d2 += diff * diff;
+            }
+            const double v = exp(d2 * neg) * w[j];
+            const double t = s + v;
+            c += fabs(s) >= fabs(v) ? (s - t) + v : (v - t) + s;
+            s = t;
+        }
+        out[i] = s + c;
+    }
+}
+
 void fgo_naive_sum_mt(const double *q, int64_t m, const double *r, const double *w,
                       int64_t n, int dim, double h, double *out, int nthreads) {
 #ifdef _OPENMP

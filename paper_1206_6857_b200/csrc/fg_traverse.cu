@@ -383,17 +383,72 @@ __global__ void fp32_pack_kernel(int64_t n, const double *__restrict__ pw,
         *reinterpret_cast<float4 *>(pf + i * F + k) = make_float4(rec[k], rec[k + 1], rec[k + 2], rec[k + 3]);
 }
 
+#if FG_PAIR_DOT
+// Dot-form record PAIRS (points 2k and 2k + 1 interleaved, so every f32x2
+// operand of the batch loop comes straight from one 8-byte load): per pair
+// {Y_0a, Y_0b, ..., Y_{D-1}a, Y_{D-1}b, B_a, B_b, W_a, W_b, pad} with
+// Y = fl(y - c_a) about the point's own anchor centre, B = fl(|Y|^2) (from the
+// rounded Y, in FP64) and W = fl(w).  Points without an anchor get zeros.
+template <int D>
+__global__ void fp32_pair_pack_kernel(int64_t n, const double *__restrict__ pw,
+                                      const double *__restrict__ ctr,
+                                      const int *__restrict__ anchor, float *__restrict__ pd) {
+    constexpr int S = packed_stride(D);
+    constexpr int P = pstride<D>();
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (2 * k >= n) return;
+    float rec[P];
+#pragma unroll
+    for (int i = 0; i < P; i++) rec[i] = 0.f;
+#pragma unroll
+    for (int hf = 0; hf < 2; hf++) {
+        const int64_t i = 2 * k + hf;
+        if (i >= n) break;
+        const int a = anchor[i];
+        if (a < 0) continue;
+        double b = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float y = (float)(pw[i * S + d] - ctr[(int64_t)a * D + d]);
+            rec[2 * d + hf] = y;
+            b = fma((double)y, (double)y, b);
+        }
+        rec[2 * D + hf] = (float)b;
+        rec[2 * D + 2 + hf] = (float)pw[i * S + D];
+    }
+#pragma unroll
+    for (int i = 0; i < P; i += 4)
+        *reinterpret_cast<float4 *>(pd + k * P + i) = make_float4(rec[i], rec[i + 1], rec[i + 2], rec[i + 3]);
+}
+#endif
+
 static int fp32_pack(TreeDev &t) {
     if (t.pf_valid) return FG_OK;
     const int D = t.dim;
+#if FG_PAIR_DOT
+    const int P = (2 * (D + 2) + 3) & ~3;
+    const int64_t npair = (t.n + 1) / 2;
+    FG_TRY(t.anchor.reserve(sizeof(int) * t.n));
+    FG_TRY(t.pf.reserve(sizeof(float) * npair * P));
+#else
     const int F = (D + 1 + 3) & ~3;
     FG_TRY(t.anchor.reserve(sizeof(int) * t.n));
     FG_TRY(t.pf.reserve(sizeof(float) * t.n * F));
+#endif
     FG_CUDA_TRY(cudaMemsetAsync(t.anchor.p, 0xff, sizeof(int) * t.n, stream()));
     count_launch();
     anchor_kernel<<<(unsigned)((t.nnodes + 255) / 256), 256, 0, stream()>>>(
         t.nnodes, t.node_i.as<int4>(), t.anchor.as<int>());
     FG_CUDA_TRY(cudaGetLastError());
+#if FG_PAIR_DOT
+    const unsigned blocks = (unsigned)((npair + 255) / 256);
+#define FG_PF(DD)                                                                            \
+    case DD:                                                                                 \
+        count_launch();                                                                      \
+        fp32_pair_pack_kernel<DD><<<blocks, 256, 0, stream()>>>(                             \
+            t.n, t.pw.as<double>(), t.node_c.as<double>(), t.anchor.as<int>(), t.pf.as<float>()); \
+        break;
+#else
     const unsigned blocks = (unsigned)((t.n + 255) / 256);
 #define FG_PF(DD)                                                                            \
     case DD:                                                                                 \
@@ -402,6 +457,7 @@ static int fp32_pack(TreeDev &t) {
                                                             t.node_c.as<double>(),           \
                                                             t.anchor.as<int>(), t.pf.as<float>()); \
         break;
+#endif
     switch (D) {
         FG_PF(1) FG_PF(2) FG_PF(3) FG_PF(4) FG_PF(5) FG_PF(6) FG_PF(7) FG_PF(8)
         default: return FG_EUNSUPPORTED;

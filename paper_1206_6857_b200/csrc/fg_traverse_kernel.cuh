@@ -364,6 +364,19 @@ __device__ __forceinline__ void base_case2(const double (&x)[kQPL][D],
 // stays within eps * G (Theorem 2).
 template <int D>
 constexpr int fstride() { return (D + 1 + 3) & ~3; }
+// Anchored FP32 items (D <= 4) in dot form from record PAIRS (fp32_pair_pack,
+// fg_traverse.cu): every f32x2 operand comes straight from shared memory, so
+// the loop needs no register packing.
+#ifndef FG_PAIR_DOT
+#define FG_PAIR_DOT 1
+#endif
+// items whose dot-form bound fails fall back to the difference form (else FP64)
+#ifndef FG_PAIR_DIFF
+#define FG_PAIR_DIFF 1
+#endif
+// floats per record pair: {Y_d a/b} x D, {B a/b}, {W a/b}, padded to 16 bytes
+template <int D>
+constexpr int pstride() { return (2 * (D + 2) + 3) & ~3; }
 // points per staged batch and floats per group offset record
 template <int D>
 constexpr int f32_cap() { return D <= 4 ? 256 : 128; }
@@ -407,10 +420,59 @@ template <int D>
 constexpr bool xs_smem() { return true; }
 template <int D>
 constexpr int xs_doubles() { return xs_smem<D>() ? kQBlock * D : 0; }
+// one 8-byte mbarrier per warp (bulk copies of FP32 record pairs), padded
+constexpr int kMbarDoubles = 2;
 template <int D>
 constexpr int warp_fixed_doubles() {
     return ((3 * D + 1) & ~1) + stage_recs<D>() * packed_stride(D) + f32_smem_doubles<D>() +
-           xs_doubles<D>();
+           kMbarDoubles + xs_doubles<D>();
+}
+// record pairs the anchored batch can stage: the FP64 staging buffer and the
+// FP32 record area are contiguous and idle while a batch runs (the item table
+// follows them)
+template <int D>
+constexpr int pair_cap() {
+    return (stage_recs<D>() * packed_stride(D) * 8 + f32_cap<D>() * fstride<D>() * 4) /
+           (pstride<D>() * 4);
+}
+
+// ---- bulk copies (cp.async.bulk + mbarrier) -------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// orders this thread's generic-proxy shared-memory accesses before later
+// async-proxy (bulk copy) writes to the same bytes
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
 }
 
 __device__ __forceinline__ float ex2_approx(float v) {
@@ -574,6 +636,197 @@ __device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], co
            ((double)f2_lo(acc[2]) + (double)f2_lo(acc[3]));
     sum1 = ((double)f2_hi(acc[0]) + (double)f2_hi(acc[1])) +
            ((double)f2_hi(acc[2]) + (double)f2_hi(acc[3]));
+}
+
+// ---- Anchored dot-form batches from record pairs (D <= 4, FG_PAIR_DOT) -----
+// The exponent (log2 units, s = log2(e) / 2h^2) of query x and record y of an
+// item inside anchor a (centre c_a) is evaluated as
+//     t = A + (-s) B + sum_d X'_d Y_d,  A = fl(-s |X|^2), X' = fl(2 s X),
+// X = fl(fl(x - c_b) - fl(c_a - c_b)) (as in batch_f32), Y and B = fl(|Y|^2)
+// from the record pair: D + 2 FFMA2 and two ex2 per record pair and query
+// slot, no operand packing.
+//
+// Error bound (fp32_pair_bound): the coordinate roundings are those of
+// fp32_item_bound (<= 4 u M per coordinate difference: the C1 sqrt(a) term).
+// The dot form adds roundings that are absolute in t: A and B one rounding
+// each, fl(-s) and X' one relative rounding each, and the D + 1 chained FFMA
+// roundings; every partial sum is bounded by s (|X| + |Y|)^2, so in natural-log
+// units E = (D + 4) u (R_q + R_r)^2 / 2h^2 (one spare term), with R_q, R_r
+// the largest 2-norm offsets of the query box and of the item's node box from
+// c_a (inflated for the coordinate roundings).  rho = 2 (C1 sqrt(a_c) + E +
+// 2^-17), cut at a_c as in fp32_item_bound; the per-item FP32 sums are folded
+// into FP64 after each item, so no FP32 accumulator adds more than 32 terms.
+template <int D>
+__device__ __forceinline__ double fp32_pair_bound(const TravArgs &A, const double *sq, int anc,
+                                                  int node, double inv_h, double klo, double wr,
+                                                  double rho_max, double &abs_err) {
+    const float kf = (float)klo;
+    const double a_max = kf >= 1.17549435e-38f ? (double)(-__logf(kf)) * (1.0 + 0x1.0p-18) + 0x1.0p-18
+                                               : CUDART_INF;
+    const double *abox = A.r_box + (int64_t)anc * 2 * D;
+    const double *nbox = A.r_box + (int64_t)node * 2 * D;
+    const double *ac = A.r_c + (int64_t)anc * D;
+    double M = 0.0, rq2 = 0.0, rr2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < D; d++) {
+        const double c = __ldg(ac + d), cb = sq[2 * D + d];
+        const double qlo = sq[d], qhi = sq[D + d];
+        const double mq = fmax(fabs(qlo - c), fabs(qhi - c));
+        const double mr = fmax(fabs(__ldg(nbox + d) - c), fabs(__ldg(nbox + D + d) - c));
+        M = fmax(M, fmax(fmax(fabs(__ldg(abox + d) - c), fabs(__ldg(abox + D + d) - c)), mq));
+        M = fmax(M, fmax(fabs(c - cb), fmax(fabs(qlo - cb), fabs(qhi - cb))));
+        rq2 += mq * mq;
+        rr2 += mr * mr;
+    }
+    const double c1 = 0x1.0p-21 * sqrt((double)D) * M * inv_h * 0.7071067811865476;
+    const double rs = (sqrt(rq2) + sqrt(rr2)) * (1.0 + 0x1.0p-20) * inv_h;
+    const double e = (D + 4.0) * 0x1.0p-24 * 0.5 * rs * rs * 1.01;
+    const double room = 0.5 * rho_max - 0x1.0p-17 - e;
+    abs_err = CUDART_INF;
+    if (!(room > 0.0)) return CUDART_INF;
+    const double sf = c1 > 0.0 ? room / c1 : CUDART_INF;
+    const double a_c = fmin(fmin(a_max, 80.0), sf * sf * (1.0 - 0x1.0p-40));
+    abs_err = 0x1.0p-140;
+    if (a_max > a_c)
+        abs_err += 2.03 * wr * (double)ex2_approx((float)(-a_c * 1.4426950408889634)) * 1.0001;
+    return 2.0 * (c1 * sqrt(a_c) + e + 0x1.0p-17);
+}
+
+// Stream one staged batch of record pairs: item t has icnt[t] pairs at pair
+// offset ioff[t] and the offset vector idl[t] = fl(c_a - c_b); xs holds the
+// lane's two query slots about c_b (FP32).  Per item the slots' A and X' are
+// formed once, then two record pairs per iteration (four independent chains
+// per slot pair); each item's FP32 sums are folded into FP64.
+// Items whose dot-form bound does not fit (wide items at small h: the dot
+// form's rounding grows with (R_q + R_r)^2 / h^2) but whose difference-form
+// bound does (fp32_item_bound) are flagged kPairDiff in icnt and streamed in
+// the difference form from the same record pairs:
+//     t = -s |X - Y|^2  (D FADD2, D FFMA2/FMUL2, one FMUL2 by -s).
+constexpr int kPairDiff = 1 << 30;
+// One difference-form item (out of line: rare, and it keeps the dot-form
+// loop's register allocation intact).
+template <int D>
+__device__ __noinline__ void item_pairs_diff(const float (&xs)[kQPL][D], const float *pitem,
+                                             int np, const float *dli, unsigned long long nss,
+                                             double &sum0, double &sum1) {
+    constexpr int P = pstride<D>(), P2 = P / 2;
+    unsigned long long xq[kQPL][D];
+#pragma unroll
+    for (int q = 0; q < kQPL; q++)
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float X = xs[q][d] - dli[d];
+            xq[q][d] = f2_pack(X, X);
+        }
+    const unsigned long long *rec = reinterpret_cast<const unsigned long long *>(pitem);
+    unsigned long long acc[kQPL][2] = {{0ull, 0ull}, {0ull, 0ull}};
+#pragma unroll 1
+    for (int j = 0; j < np; j += 2) {
+        const int nu = j + 1 < np ? 2 : 1;
+        unsigned long long r[2][P2];
+#pragma unroll
+        for (int u = 0; u < 2; u++)
+#pragma unroll
+            for (int k = 0; k < P2; k += 2) {
+                // a lone last pair re-reads itself; its second copy is not accumulated
+                const ulonglong2 v =
+                    *reinterpret_cast<const ulonglong2 *>(rec + (j + (u < nu ? u : 0)) * P2 + k);
+                r[u][k] = v.x;
+                r[u][k + 1] = v.y;
+            }
+#pragma unroll
+        for (int q = 0; q < kQPL; q++)
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                unsigned long long f = f2_sub(xq[q][0], r[u][0]);
+                unsigned long long dd = f2_mul(f, f);
+#pragma unroll
+                for (int d = 1; d < D; d++) {
+                    f = f2_sub(xq[q][d], r[u][d]);
+                    f2_fma_acc(dd, f, f);
+                }
+                const unsigned long long e = f2_ex2(f2_mul(dd, nss));
+                if (u < nu) f2_fma_acc(acc[q][u], e, r[u][D + 1]);
+            }
+    }
+    sum0 += ((double)f2_lo(acc[0][0]) + (double)f2_hi(acc[0][0])) +
+            ((double)f2_lo(acc[0][1]) + (double)f2_hi(acc[0][1]));
+    sum1 += ((double)f2_lo(acc[1][0]) + (double)f2_hi(acc[1][0])) +
+            ((double)f2_lo(acc[1][1]) + (double)f2_hi(acc[1][1]));
+}
+
+template <int D>
+__device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const float *pbuf,
+                                            const int *ioff, const int *icnt, const float *idl,
+                                            int nitems, double s, double &sum0, double &sum1) {
+    constexpr int P = pstride<D>(), FD = f32_fd<D>(), P2 = P / 2;
+    const float sf = (float)s, s2f = (float)(2.0 * s);
+    const unsigned long long nss = f2_pack(-sf, -sf);
+#pragma unroll 1
+    for (int it = 0; it < nitems; it++) {
+        const int off = ioff[it], np = icnt[it] & (kPairDiff - 1);
+        if (icnt[it] & kPairDiff) {
+            item_pairs_diff<D>(xs, pbuf + off * P, np, idl + it * FD, nss, sum0, sum1);
+            continue;
+        }
+        unsigned long long xx[kQPL][D], aa[kQPL];
+#pragma unroll
+        for (int q = 0; q < kQPL; q++) {
+            double a = 0.0;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const float X = xs[q][d] - idl[it * FD + d];
+                const float Xp = s2f * X;
+                xx[q][d] = f2_pack(Xp, Xp);
+                a = fma((double)X, (double)X, a);
+            }
+            const float av = (float)(-s * a);
+            aa[q] = f2_pack(av, av);
+        }
+        const unsigned long long *rec = reinterpret_cast<const unsigned long long *>(pbuf + off * P);
+        unsigned long long acc[kQPL][2] = {{0ull, 0ull}, {0ull, 0ull}};
+        int j = 0;
+        for (; j + 2 <= np; j += 2) {
+            unsigned long long r[2][P2];
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int k = 0; k < P2; k += 2) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(rec + (j + u) * P2 + k);
+                    r[u][k] = v.x;
+                    r[u][k + 1] = v.y;
+                }
+#pragma unroll
+            for (int q = 0; q < kQPL; q++)
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    unsigned long long t = f2_fma(r[u][D], nss, aa[q]);
+#pragma unroll
+                    for (int d = 0; d < D; d++) f2_fma_acc(t, xx[q][d], r[u][d]);
+                    f2_fma_acc(acc[q][u], f2_ex2(t), r[u][D + 1]);
+                }
+        }
+        if (j < np) {
+            unsigned long long r[P2];
+#pragma unroll
+            for (int k = 0; k < P2; k += 2) {
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(rec + j * P2 + k);
+                r[k] = v.x;
+                r[k + 1] = v.y;
+            }
+#pragma unroll
+            for (int q = 0; q < kQPL; q++) {
+                unsigned long long t = f2_fma(r[D], nss, aa[q]);
+#pragma unroll
+                for (int d = 0; d < D; d++) f2_fma_acc(t, xx[q][d], r[d]);
+                f2_fma_acc(acc[q][0], f2_ex2(t), r[D + 1]);
+            }
+        }
+        sum0 += ((double)f2_lo(acc[0][0]) + (double)f2_hi(acc[0][0])) +
+                ((double)f2_lo(acc[0][1]) + (double)f2_hi(acc[0][1]));
+        sum1 += ((double)f2_lo(acc[1][0]) + (double)f2_hi(acc[1][0])) +
+                ((double)f2_lo(acc[1][1]) + (double)f2_hi(acc[1][1]));
+    }
 }
 
 // ---- Direct FP32 stream (D >= 5) ------------------------------------------
@@ -857,6 +1110,11 @@ traverse_kernel(const TravArgs A) {
     int *itab = reinterpret_cast<int *>(fst + f32_cap<D>() * fstride<D>());  // offsets, counts
     float *idl = reinterpret_cast<float *>(itab + 64);                       // 32 x FD
     double *loc = sq + warp_fixed_doubles<D>();
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(
+        sbuf + stage_recs<D>() * S + f32_smem_doubles<D>());
+    unsigned mphase = 0;
+    if (lane == 0) mbar_init(mbar, 1);
+    __syncwarp();
     // query coordinates (D <= 4): sx[(d * kQPL + qi) * 32 + lane]
     double *sx = loc - xs_doubles<D>();
     int *sn = A.st_node + gw * A.stack_cap;
@@ -1129,6 +1387,7 @@ traverse_kernel(const TravArgs A) {
                 f32_direct<D>() ? base_mask : __ballot_sync(kFull, ni.y <= kAnchorMax) & base_mask;
             unsigned f32_mask = 0;
             int anc = 0;
+            bool pdiff = false;  // anchored item streamed in the difference form
             double abs32 = 0.0;
             bool dot_step = false;
             if (H.fp32_rho > 0.0 && small_mask && tok_scale < CUDART_INF) {
@@ -1145,7 +1404,18 @@ traverse_kernel(const TravArgs A) {
                         if (use_dot) abs_dot_l = abs_dot;
                     } else {
                         anc = __ldg(A.r_anchor + ni.x);
+#if FG_PAIR_DOT
+                        rho = fp32_pair_bound<D>(A, sq, anc, node, H.inv_h, klo, WR, H.fp32_rho,
+                                                 abs32);
+                        if (FG_PAIR_DIFF && !(rho <= H.fp32_rho && abs32 * tok_scale <= WR)) {
+                            // the difference form from the same records
+                            rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho,
+                                                     abs32);
+                            pdiff = true;
+                        }
+#else
                         rho = fp32_item_bound<D>(A, sq, anc, H.inv_h, klo, WR, H.fp32_rho, abs32);
+#endif
                     }
                     use = rho <= H.fp32_rho && abs32 * tok_scale <= WR;
                 }
@@ -1235,6 +1505,81 @@ traverse_kernel(const TravArgs A) {
                     pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
+#if FG_PAIR_DOT
+            if (!f32_direct<D>() && f32_mask) {
+                // anchored dot-form batch from record pairs: each item's pair range
+                // lands in shared memory with ONE bulk copy issued by its own lane
+                constexpr int CAPP = pair_cap<D>(), FD = f32_fd<D>(), P = pstride<D>();
+                const bool mine = (f32_mask >> lane) & 1u;
+                const int p0 = ni.x >> 1, p1 = (ni.x + ni.y + 1) >> 1;
+                const int np = mine ? p1 - p0 : 0;
+                const int off = warp_excl_scan(np);
+                float dl[D];
+                if (mine) {
+#pragma unroll
+                    for (int d = 0; d < D; d++)
+                        dl[d] = (float)(__ldg(A.r_c + (int64_t)anc * D + d) - sqc[d]);
+                }
+                if (A.use_tokens) tokens += warp_sum(mine ? WR - abs32 * tok_scale : 0.0);
+                const double abs_sum = warp_sum(mine ? abs32 : 0.0);
+                c_f32 += (unsigned long long)qn * (unsigned)warp_sum(mine ? ni.y : 0);
+                c_base += __popc(f32_mask);
+                float xs[kQPL][D];
+                {
+                    double x[kQPL][D];
+                    get_x(x);
+#pragma unroll
+                    for (int q = 0; q < kQPL; q++)
+#pragma unroll
+                        for (int d = 0; d < D; d++) xs[q][d] = (float)(x[q][d] - sqc[d]);
+                }
+                float *pbuf = reinterpret_cast<float *>(sbuf);
+                const double sdot = -H.neg_inv * 1.4426950408889634;
+                double sum32[kQPL] = {0.0, 0.0};
+                unsigned todo = f32_mask;
+                while (todo) {
+                    // the next run of whole items that fits the staging area
+                    const int base = __shfl_sync(kFull, off, __ffs(todo) - 1);
+                    const bool in = ((todo >> lane) & 1u) && off - base + np <= CAPP;
+                    const unsigned batch = __ballot_sync(kFull, in);
+                    todo &= ~batch;
+                    const int bytes = warp_sum(in ? np * P * 4 : 0);
+                    if (in) {
+                        const int t = __popc(batch & lt_mask);
+                        itab[t] = off - base;
+                        itab[32 + t] = np | (pdiff ? kPairDiff : 0);
+#pragma unroll
+                        for (int d = 0; d < D; d++) idl[t * FD + d] = dl[d];
+                    }
+                    // earlier generic accesses of the staging bytes before the
+                    // async-proxy writes; lane 0 arms the warp's barrier
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_expect_tx(mbar, (unsigned)bytes);
+                    __syncwarp();
+                    if (in)
+                        bulk_g2s(pbuf + (off - base) * P, A.r_pf + (int64_t)p0 * P,
+                                 (unsigned)(np * P * 4), mbar);
+                    mbar_wait(mbar, mphase);
+                    mphase ^= 1u;
+                    // the foreign half of a first / last pair carries weight 0
+                    if (in) {
+                        if (ni.x & 1) pbuf[(off - base) * P + 2 * D + 2] = 0.f;
+                        if ((ni.x + ni.y) & 1) pbuf[(off - base + np - 1) * P + 2 * D + 3] = 0.f;
+                    }
+                    __syncwarp();
+                    batch_pairs<D>(xs, pbuf, itab, itab + 32, idl, __popc(batch), sdot, sum32[0],
+                                   sum32[1]);
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int qi = 0; qi < kQPL; qi++) {
+                    pt_est[qi] += sum32[qi];
+                    // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho
+                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                }
+            }
+#else
             if (!f32_direct<D>() && f32_mask) {
                 constexpr int CAP = f32_cap<D>(), FD = f32_fd<D>(), F = fstride<D>();
                 const bool mine = (f32_mask >> lane) & 1u;
@@ -1303,6 +1648,7 @@ traverse_kernel(const TravArgs A) {
                     pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
+#endif
             PH_MARK(4);
             const unsigned base64 = base_mask & ~f32_mask;
             const unsigned small64 = __ballot_sync(kFull, ni.y <= kStageMax) & base_mask & ~f32_mask;

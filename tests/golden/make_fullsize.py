@@ -4,7 +4,9 @@ the unmodified reference by tests/test_oracle_pins.py):
 
   * ``naive``: exact FP64 sums (naive_sum, summation_engine.py:122-154) of a
     seeded query subsample of M' rows against ALL N reference points, at every
-    bandwidth of the config;
+    bandwidth of the config, accumulated with Neumaier compensation (a plain
+    sequential sum of 4e6 terms carries ~1e-12 of its own rounding, the size
+    of the tolerance being tested);
   * ``dito``: the reference's depth-first DITO (summation_engine.py:431-480)
     on the same subsample, bichromatic against the full reference tree (the
     per-query sums equal the monochromatic problem's).
@@ -52,7 +54,7 @@ def main():
         qs = np.ascontiguousarray(wl.query_points()[idx])
         hs = np.array(wl.bandwidths)
         naive = np.stack([oracle.naive_sum(qs, wl.references, wl.weights, h,
-                                           threads=args.threads) for h in hs])
+                                           threads=args.threads, compensated=True) for h in hs])
         t1 = time.time()
         rt = oracle.Tree(wl.references, wl.weights, 25)
         dito = []
