@@ -205,6 +205,14 @@ struct TreeDev {
     DBuf qb_c;      // double nqb x dim
     DBuf qb_rad;    // double nqb
     DBuf qb_wmin;   // double nqb: smallest weight among the block's points
+    // super-nodes: the maximal nodes the blocks are cut from (the far-field
+    // pass settles reference nodes for a whole super-node, fg_far_kernel.cuh)
+    int64_t nsn = 0;
+    DBuf qb_node;   // int nqb: BFS id of the block's super-node
+    DBuf qb_super;  // int nqb: the block's super-node index
+    DBuf sn_node;   // int nsn: BFS node id
+    DBuf sn_first;  // int nsn + 1: first block of each super-node
+    DBuf sn_wmin;   // double nsn: smallest point weight
     DBuf qb_wsum;   // double nqb: total weight of the block's points
     // heaviest-first visiting order from the previous full run's block costs
     bool qb_order_valid = false;

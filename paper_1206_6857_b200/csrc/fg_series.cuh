@@ -281,6 +281,43 @@ __device__ void h2l_warp_add(const double *__restrict__ A, const double *__restr
     }
 }
 
+// C(n, k) for the small digits of the index sets (n <= 2 kMaxOrder)
+__device__ __forceinline__ double binom_small(int n, int k) {
+    double r = 1.0;
+    for (int i = 1; i <= k; i++) r = r * (double)(n - k + i) / (double)i;
+    return r;
+}
+
+// L2L (series_expansion.py:197-217): B'_a = sum_{s >= a} C(s, a) B_s u^{s-a},
+// u = (c_dst - c_src)/sc, multi-index binomials and powers per dimension;
+// lanes own destination coefficients and add into out[a] for a < K.
+template <int D>
+__device__ void l2l_warp_add(const double *__restrict__ B, const double *__restrict__ src_c,
+                             const double *dst_c, int p, int K, double sc,
+                             const uint8_t *__restrict__ digits, double *out) {
+    const int lane = threadIdx.x & 31;
+    double pw[D][kMaxOrder];
+#pragma unroll
+    for (int d = 0; d < D; d++) power_ladder((dst_c[d] - __ldg(src_c + d)) / sc, p - 1, pw[d]);
+    for (int a = lane; a < K; a += 32) {
+        const uint64_t da = digits_of(digits, a);
+        double acc = 0.0;
+        for (int s = 0; s < K; s++) {
+            const uint64_t ds = digits_of(digits, s);
+            double v = __ldg(B + s);
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const int sd = digit(ds, d), ad = digit(da, d);
+                if (sd < ad) ok = false;
+                else v *= binom_small(sd, ad) * pw[d][sd - ad];
+            }
+            if (ok) acc += v;
+        }
+        out[a] += acc;
+    }
+}
+
 // Smallest feasible order of each series method (the order scan of
 // error_bounds.py:196-225).  p == 0 marks an infeasible method.
 // base = an upper bound on W_R exp(-min_sq / 4h^2) (error_bounds.py:196).

@@ -43,6 +43,7 @@
 #include "fg_internal.cuh"
 #include "fg_series.cuh"
 #include "fg_traverse_kernel.cuh"
+#include "fg_far_kernel.cuh"
 
 namespace fg {
 
@@ -194,23 +195,26 @@ static void block_ranges(const TreeDev &t, std::vector<int2> &out) {
 // its length in a per-point array.  Runs tile the tree order, so an exclusive
 // scan over the marks numbers them in tree order.
 __global__ void block_marks_kernel(int64_t nnodes, const int4 *__restrict__ ni, int lim,
-                                   int *__restrict__ len) {
+                                   int *__restrict__ len, int *__restrict__ own) {
     const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (v >= nnodes) return;
     const int4 e = ni[v];
-    // a node of <= lim points is cut into runs of <= kQBlock consecutive points
-    auto emit = [&](const int4 c) {
+    // a node of <= lim points is cut into runs of <= kQBlock consecutive points;
+    // each run start records the node (its super-node)
+    auto emit = [&](const int4 c, int node) {
         const int nr = (c.y + kQBlock - 1) / kQBlock;  // runs, as even as possible
         for (int r = 0; r < nr; r++) {
             const int s0 = (int)((int64_t)c.y * r / nr), s1 = (int)((int64_t)c.y * (r + 1) / nr);
             len[c.x + s0] = s1 - s0;
+            own[c.x + s0] = node;
         }
     };
-    if (v == 0 && (e.y <= lim || e.z < 0)) emit(e);
+    if (v == 0 && (e.y <= lim || e.z < 0)) emit(e, 0);
     if (e.y <= lim || e.z < 0) return;
     for (int k = 0; k < 2; k++) {
-        const int4 c = ni[k == 0 ? e.z : e.w];
-        if (c.y <= lim || c.z < 0) emit(c);
+        const int ch = k == 0 ? e.z : e.w;
+        const int4 c = ni[ch];
+        if (c.y <= lim || c.z < 0) emit(c, ch);
     }
 }
 
@@ -220,18 +224,54 @@ __global__ void block_flags_kernel(int64_t n, const int *__restrict__ len, int *
 }
 
 __global__ void block_ranges_kernel(int64_t n, const int *__restrict__ len,
-                                    const int *__restrict__ idx, int2 *__restrict__ range) {
+                                    const int *__restrict__ idx, const int *__restrict__ own,
+                                    int2 *__restrict__ range, int *__restrict__ qb_node) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n && len[i] > 0) range[idx[i]] = make_int2((int)i, len[i]);
+    if (i < n && len[i] > 0) {
+        range[idx[i]] = make_int2((int)i, len[i]);
+        qb_node[idx[i]] = own[i];
+    }
+}
+
+// super-node numbering: consecutive blocks of one maximal node form a
+// super-node (blocks are in tree order, so each node's blocks are contiguous)
+__global__ void sn_flags_kernel(int64_t nqb, const int *__restrict__ qb_node, int *__restrict__ flag) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b < nqb) flag[b] = (b == 0 || qb_node[b] != qb_node[b - 1]) ? 1 : 0;
+}
+
+__global__ void sn_fill_kernel(int64_t nqb, const int *__restrict__ flag,
+                               const int *__restrict__ incl, const int *__restrict__ qb_node,
+                               int *__restrict__ qb_super, int *__restrict__ sn_node,
+                               int *__restrict__ sn_first) {
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= nqb) return;
+    const int k = incl[b] - 1;
+    qb_super[b] = k;
+    if (flag[b]) {
+        sn_node[k] = qb_node[b];
+        sn_first[k] = (int)b;
+    }
+    if (b == nqb - 1) sn_first[k + 1] = (int)nqb;
+}
+
+__global__ void sn_stats_kernel(int64_t nsn, const int *__restrict__ sn_first,
+                                const double *__restrict__ qb_wmin, double *__restrict__ sn_wmin) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= nsn) return;
+    double m = CUDART_INF;
+    for (int b = sn_first[k]; b < sn_first[k + 1]; b++) m = fmin(m, qb_wmin[b]);
+    sn_wmin[k] = m;
 }
 
 static int device_block_ranges(TreeDev &t, int64_t &nqb) {
     struct BlockScr {
-        DBuf len, flag, idx, tmp;
+        DBuf len, flag, idx, tmp, own;
     };
     BlockScr &bs = scratch<BlockScr, BlockScr>();
-    DBuf &s_len = bs.len, &s_flag = bs.flag, &s_idx = bs.idx, &s_tmp = bs.tmp;
+    DBuf &s_len = bs.len, &s_flag = bs.flag, &s_idx = bs.idx, &s_tmp = bs.tmp, &s_own = bs.own;
     const int64_t n = t.n;
+    FG_TRY(s_own.reserve(sizeof(int) * (n + 1)));
     FG_TRY(s_len.reserve(sizeof(int) * (n + 1)));
     FG_TRY(s_flag.reserve(sizeof(int) * (n + 1)));
     FG_TRY(s_idx.reserve(sizeof(int) * (n + 1)));
@@ -241,7 +281,7 @@ static int device_block_ranges(TreeDev &t, int64_t &nqb) {
     const int lim = lenv ? std::max(kQBlock, atoi(lenv))
                          : (int)std::max<int64_t>(kQBlock, std::min<int64_t>(kQBlockNode, n / 16));
     block_marks_kernel<<<(unsigned)((t.nnodes + 255) / 256), 256, 0, stream()>>>(
-        t.nnodes, t.node_i.as<int4>(), lim, s_len.as<int>());
+        t.nnodes, t.node_i.as<int4>(), lim, s_len.as<int>(), s_own.as<int>());
     count_launch();
     block_flags_kernel<<<(unsigned)((n + 1 + 255) / 256), 256, 0, stream()>>>(n + 1, s_len.as<int>(),
                                                                               s_flag.as<int>());
@@ -260,16 +300,55 @@ static int device_block_ranges(TreeDev &t, int64_t &nqb) {
     FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     nqb = *h_cnt;
     FG_TRY(t.qb_range.reserve(sizeof(int2) * (nqb > 0 ? nqb : 1)));
+    FG_TRY(t.qb_node.reserve(sizeof(int) * (nqb > 0 ? nqb : 1)));
     count_launch();
     block_ranges_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
-        n, s_len.as<int>(), s_idx.as<int>(), t.qb_range.as<int2>());
+        n, s_len.as<int>(), s_idx.as<int>(), s_own.as<int>(), t.qb_range.as<int2>(),
+        t.qb_node.as<int>());
     FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
+// Super-nodes of the device blocks (after device_block_ranges): numbering,
+// first block, smallest weight; the count is read back with the median.
+static int super_nodes(TreeDev &t, int *h_nsn) {
+    struct SnScr {
+        DBuf flag, incl, tmp;
+    };
+    SnScr &ss = scratch<SnScr, SnScr>();
+    const int64_t nqb = t.nqb;
+    FG_TRY(ss.flag.reserve(sizeof(int) * nqb));
+    FG_TRY(ss.incl.reserve(sizeof(int) * nqb));
+    FG_TRY(t.qb_super.reserve(sizeof(int) * nqb));
+    FG_TRY(t.sn_node.reserve(sizeof(int) * nqb));
+    FG_TRY(t.sn_first.reserve(sizeof(int) * (nqb + 1)));
+    FG_TRY(t.sn_wmin.reserve(sizeof(double) * nqb));
+    const unsigned g = (unsigned)((nqb + 255) / 256);
+    count_launch();
+    sn_flags_kernel<<<g, 256, 0, stream()>>>(nqb, t.qb_node.as<int>(), ss.flag.as<int>());
+    size_t tmp = 0;
+    FG_CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tmp, ss.flag.as<int>(), ss.incl.as<int>(),
+                                              (int)nqb, stream()));
+    FG_TRY(ss.tmp.reserve(tmp + 16));
+    count_launch();
+    FG_CUDA_TRY(cub::DeviceScan::InclusiveSum(ss.tmp.p, tmp, ss.flag.as<int>(), ss.incl.as<int>(),
+                                              (int)nqb, stream()));
+    count_launch();
+    sn_fill_kernel<<<g, 256, 0, stream()>>>(nqb, ss.flag.as<int>(), ss.incl.as<int>(),
+                                            t.qb_node.as<int>(), t.qb_super.as<int>(),
+                                            t.sn_node.as<int>(), t.sn_first.as<int>());
+    FG_CUDA_TRY(cudaGetLastError());
+    FG_CUDA_TRY(cudaMemcpyAsync(h_nsn, ss.incl.as<int>() + nqb - 1, sizeof(int),
+                                cudaMemcpyDeviceToHost, stream()));
     return FG_OK;
 }
 
 int query_blocks(TreeDev &t) {
     if (t.qb_valid) return FG_OK;
     int64_t nqb = 0;
+    // super-nodes come with the device block cut (the experiment knobs' host
+    // walks have none: the far-field pass is then off)
+    bool sn_ok = false;
     if (getenv("FG_QBLOCK_MODE") || getenv("FG_QBLOCK_LIMIT")) {
         // experiment knobs (fixed runs / smaller blocks): the host walk
         std::vector<int2> ranges;
@@ -280,7 +359,9 @@ int query_blocks(TreeDev &t) {
                                     cudaMemcpyHostToDevice, stream()));
     } else {
         FG_TRY(device_block_ranges(t, nqb));
+        sn_ok = true;
     }
+    t.nsn = 0;
     const int D = t.dim;
     FG_TRY(t.qb_box.reserve(sizeof(double) * nqb * 2 * D));
     FG_TRY(t.qb_c.reserve(sizeof(double) * nqb * D));
@@ -328,8 +409,20 @@ int query_blocks(TreeDev &t) {
         if (nqb > 0)
             FG_CUDA_TRY(cudaMemcpyAsync(h_med, s_sorted.as<double>() + nqb / 2, sizeof(double),
                                         cudaMemcpyDeviceToHost, stream()));
+        static thread_local int *h_nsn = nullptr;
+        if (!h_nsn) FG_CUDA_TRY(cudaMallocHost(&h_nsn, sizeof(int)));
+        *h_nsn = 0;
+        t.nqb = nqb;
+        if (sn_ok && nqb > 0) FG_TRY(super_nodes(t, h_nsn));
         FG_CUDA_TRY(cudaStreamSynchronize(stream()));
         t.qb_rad_median = *h_med;
+        t.nsn = *h_nsn;
+        if (t.nsn > 0) {
+            count_launch();
+            sn_stats_kernel<<<(unsigned)((t.nsn + 255) / 256), 256, 0, stream()>>>(
+                t.nsn, t.sn_first.as<int>(), t.qb_wmin.as<double>(), t.sn_wmin.as<double>());
+            FG_CUDA_TRY(cudaGetLastError());
+        }
     }
     t.nqb = nqb;
     t.qb_valid = true;
@@ -565,6 +658,95 @@ static int launch_dispatch(int D, TravArgs &A, size_t smem, int64_t nb) {
     return A.audit ? launch_dispatch_t<true>(D, A, smem, nb) : launch_dispatch_t<false>(D, A, smem, nb);
 }
 
+// ------------------------------------------------------- far-field pass
+// (fg_far_kernel.cuh) outputs per (bandwidth in launch, super-node) and the
+// far kernel's per-warp scratch; per (host thread, device) like all scratch
+struct FarScratch {
+    DBuf work, st_node, st_f, ser, flag, tokens, settled, est, loc, rcnt, res;
+    int grid = 0, cap = 0;
+};
+
+template <int D>
+static int launch_far_t(TravArgs &A, int64_t ntask) {
+    auto kern = far_kernel<D>;
+    const size_t smem = sizeof(double) * (((3 * D + 1) & ~1) + ((A.K + 1) & ~1)) * kFarWarps;
+    int dev = 0, sms = 0, occ = 0;
+    FG_CUDA_TRY(cudaGetDevice(&dev));
+    FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFarThreads, smem));
+    const int64_t full = (int64_t)sms * (occ < 1 ? 1 : occ);
+    int64_t grid = std::min<int64_t>(full, (ntask + kFarWarps - 1) / kFarWarps);
+    if (grid < 1) grid = 1;
+    FarScratch &F = scratch<FarScratch, FarScratch>();
+    const int cap = A.stack_cap;
+    if (F.grid < grid || F.cap != cap) {
+        const int64_t warps = grid * kFarWarps;
+        FG_TRY(F.st_node.reserve(sizeof(int) * warps * cap));
+        FG_TRY(F.st_f.reserve(sizeof(double) * warps * cap * 3));
+        FG_TRY(F.ser.reserve(sizeof(int2) * warps * cap));
+        F.grid = (int)grid;
+        F.cap = cap;
+    }
+    A.far_st_node = F.st_node.as<int>();
+    A.far_st_f = F.st_f.as<double>();
+    A.far_ser = F.ser.as<int2>();
+    FG_CUDA_TRY(cudaMemsetAsync(A.far_work, 0, sizeof(unsigned long long), stream()));
+    count_launch();
+    kern<<<(unsigned)grid, kFarThreads, smem, stream()>>>(A);
+    FG_CUDA_TRY(cudaGetLastError());
+    return FG_OK;
+}
+
+// Queue the far-field pass for the launch described by A (nh bandwidths).
+static int queue_far(TreeDev &q, TravArgs &A) {
+    const int64_t ntask = (int64_t)A.nh * q.nsn;
+    FarScratch &F = scratch<FarScratch, FarScratch>();
+    FG_TRY(F.work.reserve(sizeof(unsigned long long)));
+    FG_TRY(F.flag.reserve(sizeof(int) * ntask));
+    FG_TRY(F.tokens.reserve(sizeof(double) * ntask));
+    FG_TRY(F.settled.reserve(sizeof(double) * ntask));
+    FG_TRY(F.est.reserve(sizeof(double) * ntask));
+    FG_TRY(F.rcnt.reserve(sizeof(int) * ntask));
+    FG_TRY(F.res.reserve(sizeof(int) * ntask * kFarResCap));
+    FG_TRY(F.loc.reserve(sizeof(double) * ntask * std::max(A.K, 1)));
+    A.q_ni = q.node_i.as<int4>();
+    A.q_box = q.node_box.as<double>();
+    A.q_c = q.node_c.as<double>();
+    A.q_wr = q.node_wr.as<double2>();
+    A.nsn = q.nsn;
+    A.sn_node = q.sn_node.as<int>();
+    A.sn_wmin = q.sn_wmin.as<double>();
+    A.qb_super = q.qb_super.as<int>();
+    A.far_work = F.work.as<unsigned long long>();
+    A.far_flag = F.flag.as<int>();
+    A.far_tokens = F.tokens.as<double>();
+    A.far_settled = F.settled.as<double>();
+    A.far_est = F.est.as<double>();
+    A.far_loc = F.loc.as<double>();
+    A.far_rcnt = F.rcnt.as<int>();
+    A.far_res = F.res.as<int>();
+    switch (q.dim) {
+        case 1: return launch_far_t<1>(A, ntask);
+        case 2: return launch_far_t<2>(A, ntask);
+        case 3: return launch_far_t<3>(A, ntask);
+        case 4: return launch_far_t<4>(A, ntask);
+        case 5: return launch_far_t<5>(A, ntask);
+        case 6: return launch_far_t<6>(A, ntask);
+        case 7: return launch_far_t<7>(A, ntask);
+        case 8: return launch_far_t<8>(A, ntask);
+        default: return FG_EUNSUPPORTED;
+    }
+}
+
+// The far-field pass is off by default: measured on C5's heaviest bandwidth
+// (h = 0.153, ncu launch list) it costs 433 ms to save ~10 ms of the blocks'
+// 946 ms -- at eps = 0.001 the reference's H2L bound (the (sqrt2 r_R)^p
+// cross[p] term, 448x Hermite's at p = 6) almost never admits a super-node
+// level translation, so S-level work is FD prunes and a few direct locals
+// (DESIGN.md "Far-field pass").  FG_FAR=1 / fg_set_far_pass(1) turn it on.
+int g_far_pass = 0;
+static constexpr int64_t kFarMinBlocks = 4;  // blocks per super-node on average
+
 // FP32 base cases for these bandwidths?
 static int fp32_enabled(const TreeDev &q, const TreeDev &r, const double *hs, int nh, double eps) {
     int fp32 = g_fp32_base;
@@ -739,6 +921,12 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         FG_TRY(q.qb_cost.reserve(sizeof(unsigned long long) * q.nqb));
         A.cost = q.qb_cost.as<unsigned long long>();
         if (q.qb_order_valid) A.order = q.qb_order.as<int>();
+    }
+    {
+        int far = g_far_pass;
+        if (const char *env = getenv("FG_FAR")) far = atoi(env);  // experiment knob
+        if (far && !audit && A.nbl > 0 && q.nsn > 0 && q.nqb >= kFarMinBlocks * q.nsn)
+            FG_TRY(queue_far(q, A));
     }
     if (A.nbl > 0) FG_TRY(launch_dispatch(D, A, smem, A.nbl * nh));
     if (A.cost) {

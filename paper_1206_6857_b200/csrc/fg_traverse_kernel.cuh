@@ -35,7 +35,8 @@ constexpr int kDbgFields = 16;  // per-block debug record (FG_DEBUG_BLOCKS)
 #ifndef FG_PHASE_PROF
 #define FG_PHASE_PROF 0  // per-block phase cycle counters in the debug record
 #endif
-constexpr int kCounters = 16;  // per-bandwidth device counter slots (12 used)
+constexpr int kCounters = 16;  // per-bandwidth device counter slots (13 used)
+constexpr int kFarResCapT = 2048;  // residual entries per far-field task (fg_far_kernel.cuh)
 struct TravH {
     double h, neg_inv, inv_h, sc, inv_sc, eps;
     double fp32_rho;              // relative error allowed per FP32 leaf item (0: FP64 only)
@@ -103,6 +104,23 @@ struct TravArgs {
     int nh;                        // bandwidths in this launch
     int jord[kMaxSweep];           // task group k runs bandwidth jord[k] (heaviest first)
     TravH hp[kMaxSweep];
+    // far-field pass over super-nodes (fg_far_kernel.cuh); far_flag == null: off
+    const int4 *q_ni;              // query tree nodes (BFS): start, count, left, right
+    const double *q_box;
+    const double *q_c;
+    const double2 *q_wr;
+    long long nsn;                 // super-nodes
+    const int *sn_node;            // BFS node of each super-node
+    const double *sn_wmin;         // smallest point weight per super-node (monochromatic)
+    const int *qb_super;           // super-node of each block
+    unsigned long long *far_work;
+    int *far_st_node;              // far kernel per-warp frontier / series scratch
+    double *far_st_f;
+    int2 *far_ser;
+    // per (bandwidth in launch, super-node) task t = j * nsn + k:
+    int *far_flag;                 // 0: abandoned (blocks start at the root), bit 0 ok, bit 1 local
+    double *far_tokens, *far_settled, *far_est, *far_loc;  // far_loc: K per task
+    int *far_rcnt, *far_res;       // residual entries: kFarResCap per task
 };
 
 // Append the events of the lanes in `mask` (each lane passes its own fields).
@@ -1224,7 +1242,35 @@ traverse_kernel(const TravArgs A) {
         // newest) beyond that, which bounds its size.
         int head = 0, cnt = 1;
         const int cap = A.stack_cap;
-        {
+        // far-field pass results of the block's super-node (fg_far_kernel.cuh)
+        int far = 0;
+        long long ft = 0;
+        double far_est = 0.0;
+        if (A.far_flag) {
+            ft = (long long)j * A.nsn + __ldg(A.qb_super + b);
+            far = A.far_flag[ft];
+        }
+        if (far) {
+            // inherit S's leftover tokens, settled mass and node-level estimate;
+            // start from S's residual entries, bounded against this block's box
+            tokens = A.far_tokens[ft];
+            far_est = A.far_est[ft];
+            const int nr = A.far_rcnt[ft];
+            const int *res = A.far_res + ft * kFarResCapT;
+            double lm = 0.0;
+            for (int i = lane; i < nr; i += 32) {
+                const int nd = __ldg(res + i);
+                double klo, khi, lb;
+                entry_bounds<D>(A, sq, nd, H.neg_inv, klo, khi, lb, s_tab);
+                sn[i] = nd;
+                skl[i] = klo;
+                skh[i] = khi;
+                slb[i] = lb;
+                lm += A.r_wr[nd].x * lb;
+            }
+            cnt = nr;
+            mass = A.far_settled[ft] + warp_sum(lm);
+        } else {
             double klo, khi, lb;
             entry_bounds<D>(A, sq, 0, H.neg_inv, klo, khi, lb, s_tab);
             if (lane == 0) {
@@ -1718,7 +1764,16 @@ traverse_kernel(const TravArgs A) {
         unsigned c_dh = 0, c_dl = 0, c_h2l = 0;
         unsigned long long c_hq = 0, c_lq = 0, c_ht = 0;
         bool local_used = false;
-        if (nh + no > 0) {
+        if (far & 2) {
+            // S.local pushed down to this block's centre (translate_l2l,
+            // series_expansion.py:197-217), the block's own local terms added below
+            l2l_warp_add<D>(A.far_loc + ft * A.K,
+                            A.q_c + (int64_t)__ldg(A.sn_node + __ldg(A.qb_super + b)) * D, sqc,
+                            A.plimit, A.K, H.sc, A.digits, loc);
+            __syncwarp();
+            local_used = true;
+        }
+        if (nh + no > 0 || local_used) {
             double x[kQPL][D];
             get_x(x);
             double qc[D];
@@ -1813,7 +1868,7 @@ traverse_kernel(const TravArgs A) {
             }
         }
         PH_MARK(6);
-        const double node_est = warp_sum(lane_est);
+        const double node_est = warp_sum(lane_est) + far_est;
 #pragma unroll
         for (int qi = 0; qi < kQPL; qi++)
             if (valid[qi]) H.out[A.q_perm[qs + lane + 32 * qi]] = pt_est[qi] + node_est;
