@@ -385,6 +385,9 @@ constexpr int fstride() { return (D + 1 + 3) & ~3; }
 // Anchored FP32 items (D <= 4) in dot form from record PAIRS (fp32_pair_pack,
 // fg_traverse.cu): every f32x2 operand comes straight from shared memory, so
 // the loop needs no register packing.
+#ifndef FG_DEFER_CREDIT
+#define FG_DEFER_CREDIT 0
+#endif
 #ifndef FG_PAIR_DOT
 #define FG_PAIR_DOT 1
 #endif
@@ -1419,6 +1422,11 @@ traverse_kernel(const TravArgs A) {
             // one reduction per step: popped entries leave the frontier, settled
             // ones and pushed children enter the mass bound (base cases move
             // into the per-point exact sums)
+#if FG_DEFER_CREDIT
+            // experiment: base items credit only their W_R lb (as a deferred
+            // evaluation would); their exact sums do not feed G_min
+            if ((base_mask >> lane) & 1u) settled = WR * lb;
+#endif
             mass += warp_sum(settled + child_sum - (act ? WR * lb : 0.0));
             if (mass < 0.0) mass = 0.0;
 
@@ -1548,7 +1556,7 @@ traverse_kernel(const TravArgs A) {
 #pragma unroll
                 for (int qi = 0; qi < kQPL; qi++) {
                     pt_est[qi] += sum32[qi];
-                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                    if (!FG_DEFER_CREDIT) pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
 #if FG_PAIR_DOT
@@ -1622,7 +1630,7 @@ traverse_kernel(const TravArgs A) {
                 for (int qi = 0; qi < kQPL; qi++) {
                     pt_est[qi] += sum32[qi];
                     // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho
-                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                    if (!FG_DEFER_CREDIT) pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
 #else
@@ -1691,7 +1699,7 @@ traverse_kernel(const TravArgs A) {
                     pt_est[qi] += sum32[qi];
                     // |sum32 - S| <= rho S + sum(abs) with rho <= fp32_rho, so
                     // sum32 (1 - fp32_rho) - sum(abs) <= S
-                    pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
+                    if (!FG_DEFER_CREDIT) pt_mass[qi] += fmax(sum32[qi] * (1.0 - H.fp32_rho) - abs_sum, 0.0);
                 }
             }
 #endif
@@ -1751,7 +1759,7 @@ traverse_kernel(const TravArgs A) {
 #pragma unroll
                 for (int qi = 0; qi < kQPL; qi++) {
                     pt_est[qi] += contrib[qi];
-                    pt_mass[qi] += contrib[qi];
+                    if (!FG_DEFER_CREDIT) pt_mass[qi] += contrib[qi];
                 }
                 if (A.use_tokens) tokens += wri;
                 c_base++;
