@@ -49,6 +49,10 @@ namespace fg {
 
 // reference-side base-item size: 0 = by bandwidth (ref_leaf_for), else fixed
 int g_ref_leaf = 0;
+#ifndef FG_BIG_ITEM_RATIO
+#define FG_BIG_ITEM_RATIO 4.0
+#endif
+static constexpr double kBigItemRatio = FG_BIG_ITEM_RATIO;  // h / r_b above which items reach kAnchorMax
 
 // Base-item granularity by bandwidth relative to the query blocks' median
 // inf-radius r_b (D >= 5: 32-point items win below ~0.05 r_b, 48 below
@@ -67,6 +71,7 @@ static int ref_leaf_for(const TreeDev &q, double h) {
     if (q.dim <= 4) {  // anchored FP32 items: <= kAnchorMax (128) points
         if (h < 0.2 * rb) return 32;
         if (h < 1.0 * rb) return kStageMax;
+        if (kAnchorMax > 128 && h < kBigItemRatio * rb) return 128;
         return kAnchorMax;
     }
     if (h < 0.1 * rb) return 32;

@@ -19,7 +19,10 @@ constexpr int kQPL = 2;
 constexpr int kQBlock = 32 * kQPL;
 // largest anchored FP32 base item (and anchor) in points (D <= 4): with the
 // Jensen mass bound 128-point items beat 64 (C2 sweep -4.7 %)
-constexpr int kAnchorMax = 128;
+#ifndef FG_ANCHOR_MAX
+#define FG_ANCHOR_MAX 128
+#endif
+constexpr int kAnchorMax = FG_ANCHOR_MAX;
 // FP64 base items up to kStageMax points are staged in shared memory (two
 // buffers of kStageMax records at D <= 5); larger ones read global memory
 constexpr int kStageMax = 64;
