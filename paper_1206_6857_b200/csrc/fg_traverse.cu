@@ -50,7 +50,7 @@ namespace fg {
 // reference-side base-item size: 0 = by bandwidth (ref_leaf_for), else fixed
 int g_ref_leaf = 0;
 #ifndef FG_BIG_ITEM_RATIO
-#define FG_BIG_ITEM_RATIO 4.0
+#define FG_BIG_ITEM_RATIO 1.0
 #endif
 static constexpr double kBigItemRatio = FG_BIG_ITEM_RATIO;  // h / r_b above which items reach kAnchorMax
 
@@ -68,7 +68,10 @@ static int ref_leaf_for(const TreeDev &q, double h) {
     // single-run scans per bandwidth with the Jensen bound and run-based query
     // blocks (C3, C4, C5; r_b = median block inf-radius): small items where
     // pruning still bites, bigger ones where nearly every pair is exact
-    if (q.dim <= 4) {  // anchored FP32 items: <= kAnchorMax (128) points
+    // anchored FP32 items: <= kAnchorMax (256) points; 256-point items above
+    // r_b measured C5 -2.3 % against 128 (and 128 between r_b and 1.5 r_b: no
+    // gain), C2 neutral
+    if (q.dim <= 4) {
         if (h < 0.2 * rb) return 32;
         if (h < 1.0 * rb) return kStageMax;
         if (kAnchorMax > 128 && h < kBigItemRatio * rb) return 128;

@@ -20,7 +20,7 @@ constexpr int kQBlock = 32 * kQPL;
 // largest anchored FP32 base item (and anchor) in points (D <= 4): with the
 // Jensen mass bound 128-point items beat 64 (C2 sweep -4.7 %)
 #ifndef FG_ANCHOR_MAX
-#define FG_ANCHOR_MAX 128
+#define FG_ANCHOR_MAX 256
 #endif
 constexpr int kAnchorMax = FG_ANCHOR_MAX;
 // FP64 base items up to kStageMax points are staged in shared memory (two
@@ -1567,6 +1567,7 @@ traverse_kernel(const TravArgs A) {
                 // anchored dot-form batch from record pairs: each item's pair range
                 // lands in shared memory with ONE bulk copy issued by its own lane
                 constexpr int CAPP = pair_cap<D>(), FD = f32_fd<D>(), P = pstride<D>();
+                static_assert(CAPP >= kAnchorMax / 2 + 1, "one item must fit the pair staging");
                 const bool mine = (f32_mask >> lane) & 1u;
                 const int p0 = ni.x >> 1, p1 = (ni.x + ni.y + 1) >> 1;
                 const int np = mine ? p1 - p0 : 0;
