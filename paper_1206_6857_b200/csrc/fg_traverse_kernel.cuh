@@ -1567,7 +1567,8 @@ traverse_kernel(const TravArgs A) {
                 // anchored dot-form batch from record pairs: each item's pair range
                 // lands in shared memory with ONE bulk copy issued by its own lane
                 constexpr int CAPP = pair_cap<D>(), FD = f32_fd<D>(), P = pstride<D>();
-                static_assert(CAPP >= kAnchorMax / 2 + 1, "one item must fit the pair staging");
+                static_assert(f32_direct<D>() || CAPP >= kAnchorMax / 2 + 1,
+                              "one item must fit the pair staging");
                 const bool mine = (f32_mask >> lane) & 1u;
                 const int p0 = ni.x >> 1, p1 = (ni.x + ni.y + 1) >> 1;
                 const int np = mine ? p1 - p0 : 0;
