@@ -177,6 +177,9 @@ int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
  * (eps = 0 always uses FP64).  Not part of the
  * reference API. */
 int fg_set_engine_params(int32_t ref_leaf, int32_t stack_cap, int32_t fp32_base);
+/* device bounds-check violations counted since the last call (and reset);
+ * -1 when the library was built without -DFG_CHECKS=1 */
+int fg_check_failures(int64_t *count);
 
 /* ---- series algebra (series_expansion.py), batched over `batch` items ---
  * All arrays host or device, row-major per item.  Used by the Python mirror

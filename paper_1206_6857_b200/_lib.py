@@ -68,6 +68,7 @@ SIGNATURES = {
     "fg_series_translate": [_I32, _P, _I32, _P, _P, _I32, _I32, _I32, _I32, _F64, _P],
     "fg_best_method": [_P, _I32, _I32, _I32, _P],
     "fg_iset_export": [_I32, _I32, _P, _P, _P, _P, _P, _P, _P],
+    "fg_check_failures": [_P],
 }
 
 _lib = None

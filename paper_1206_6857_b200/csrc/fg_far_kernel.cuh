@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
             if (act) {
                 int slot = base + lane;
                 if (slot >= cap) slot -= cap;
+                FG_CHECK(slot >= 0 && slot < cap);
                 node = sn[slot];
                 klo = skl[slot];
                 khi = skh[slot];
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
                 overflow = true;
                 break;
             }
+            FG_CHECK(nres + __popc(res_mask) <= kFarResCap);
             if ((res_mask >> lane) & 1u) res[nres + __popc(res_mask & lt_mask)] = node;
             nres += __popc(res_mask);
             double child_sum = 0.0;

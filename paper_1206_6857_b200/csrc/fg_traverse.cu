@@ -1102,3 +1102,16 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
 }
 
 }  // namespace fg
+
+extern "C" int fg_check_failures(int64_t *count) {
+    FG_REQUIRE(count, FG_EINVAL, "null argument");
+#if FG_CHECKS
+    unsigned long long v = 0, z = 0;
+    FG_CUDA_TRY(cudaMemcpyFromSymbol(&v, fg::g_fg_check_fail, sizeof(v)));
+    FG_CUDA_TRY(cudaMemcpyToSymbol(fg::g_fg_check_fail, &z, sizeof(z)));
+    *count = (int64_t)v;
+#else
+    *count = -1;  // this build has no device checks
+#endif
+    return FG_OK;
+}

@@ -12,6 +12,18 @@
 
 namespace fg {
 
+// Device-side bounds checks (a -DFG_CHECKS=1 build; compute-sanitizer is not
+// available on the GPU pool): every violated invariant bumps a counter that
+// fg_check_failures reads back (tools/check_run.py runs the workloads).
+#ifndef FG_CHECKS
+#define FG_CHECKS 0
+#endif
+static __device__ unsigned long long g_fg_check_fail;
+#define FG_CHECK(cond)                                                   \
+    do {                                                                 \
+        if (FG_CHECKS && !(cond)) atomicAdd(&::fg::g_fg_check_fail, 1ull); \
+    } while (0)
+
 constexpr int kTravThreads = 128;
 // queries per lane: a query block has up to 32 * kQPL points (lane l holds
 // queries l and l + 32)
@@ -235,6 +247,7 @@ __device__ __forceinline__ void stage_points(const double *__restrict__ pw, int 
     const int lane = threadIdx.x & 31;
     const int rs = __shfl_sync(kFull, ni_x, i);
     const int rc = __shfl_sync(kFull, ni_y, i);
+    FG_CHECK(rc >= 1 && rc <= kStageMax && rs >= 0);
     for (int l = lane; l < rc; l += 32) {
         const double *src = pw + (int64_t)(rs + l) * S;
         double *dst = buf + l * S;
@@ -1182,6 +1195,7 @@ traverse_kernel(const TravArgs A) {
         unsigned steps = 0;
         const int2 rg = A.qb_range[b];
         const int qs = rg.x, qn = rg.y;
+        FG_CHECK(qn >= 1 && qn <= kQBlock && qs >= 0);
         const int nq = qn > 32 ? 2 : 1;  // query slots in use (warp-uniform)
         bool valid[kQPL];
         if (lane < 2 * D) sq[lane] = A.qb_box[b * 2 * D + lane];
@@ -1262,6 +1276,7 @@ traverse_kernel(const TravArgs A) {
             tokens = A.far_tokens[ft];
             far_est = A.far_est[ft];
             const int nr = A.far_rcnt[ft];
+            FG_CHECK(nr >= 0 && nr <= kFarResCapT && nr <= cap);
             const int *res = A.far_res + ft * kFarResCapT;
             double lm = 0.0;
             for (int i = lane; i < nr; i += 32) {
@@ -1310,6 +1325,7 @@ traverse_kernel(const TravArgs A) {
             if (act) {
                 int slot = base + lane;
                 if (slot >= cap) slot -= cap;
+                FG_CHECK(slot >= 0 && slot < cap);
                 node = sn[slot];
                 klo = skl[slot];
                 khi = skh[slot];
@@ -1385,6 +1401,7 @@ traverse_kernel(const TravArgs A) {
                     settled = WR * lb;
                     const int slot = meth == 2 ? nh + __popc(hm & lt_mask)
                                                : A.stack_cap - 1 - no - __popc(om & lt_mask);
+                    FG_CHECK(slot >= nh && slot < A.stack_cap && nh + no + 32 <= A.stack_cap);
                     sl[slot] = make_int2(node, p | (meth << 8));
                 }
                 nh += __popc(hm);
@@ -1414,6 +1431,7 @@ traverse_kernel(const TravArgs A) {
                     int slot = pos + c;
                     if (slot >= cap) slot -= cap;
                     if (slot >= cap) slot -= cap;
+                    FG_CHECK(slot >= 0 && slot < cap && cnt + 2 * __popc(split_mask) <= cap);
                     sn[slot] = ch;
                     skl[slot] = cl;
                     skh[slot] = chh;
@@ -1616,6 +1634,8 @@ traverse_kernel(const TravArgs A) {
                     __syncwarp();
                     if (lane == 0) mbar_expect_tx(mbar, (unsigned)bytes);
                     __syncwarp();
+                    FG_CHECK(!in || (off - base >= 0 && off - base + np <= CAPP && np >= 1 &&
+                                     np <= kAnchorMax / 2 + 1));
                     if (in)
                         bulk_g2s(pbuf + (off - base) * P, A.r_pf + (int64_t)p0 * P,
                                  (unsigned)(np * P * 4), mbar);
