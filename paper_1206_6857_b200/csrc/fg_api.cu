@@ -193,7 +193,8 @@ static void host_tables(int dim, int order, SeriesTables &T, std::vector<std::ve
         int deg = 0;
         double f = 1.0;
         for (int d = 0; d < dim; d++) {
-            T.h_digits[(size_t)k * kMaxDim + d] = (uint8_t)idx[k][d];
+            // rows hold kMaxDim digits; beyond that only order-1 sets (all zero)
+            if (d < kMaxDim) T.h_digits[(size_t)k * kMaxDim + d] = (uint8_t)idx[k][d];
             deg += idx[k][d];
             f *= fact_d(idx[k][d]);
         }
@@ -239,10 +240,10 @@ const SeriesTables *series_tables(int dim, int order, int *status) {
         *status = FG_OK;
         return it->second.get();
     }
-    if (dim < 1 || dim > kMaxDim || order < 1 || order > kMaxOrder ||
-        iset_count(dim, order) > kMaxK) {
+    if (dim < 1 || dim > kMaxUserDim || (dim > kMaxDim && order > 1) || order < 1 ||
+        order > kMaxOrder || iset_count(dim, order) > kMaxK) {
         set_error("series tables: (dim, order) outside the device limits (dim<=8, order<=8, "
-                  "C(dim+order-1, dim)<=256)");
+                  "C(dim+order-1, dim)<=256; dim<=16 at order 1)");
         *status = FG_EUNSUPPORTED;
         return nullptr;
     }
@@ -443,6 +444,13 @@ int fg_naive_sum(const double *queries, int64_t m, const double *references,
     return FG_OK;
 }
 
+__global__ void pad_coords_kernel(int64_t n, int dim, int kd, const double *__restrict__ src,
+                                  double *__restrict__ dst) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int d = 0; d < kd; d++) dst[i * kd + d] = d < dim ? src[i * dim + d] : 0.0;
+}
+
 int fg_tree_build(const double *points, const double *weights, int64_t n, int32_t dim,
                   int32_t leaf_threshold, fg_tree **out) {
     FG_REQUIRE(out, FG_EINVAL, "null output handle");
@@ -450,13 +458,25 @@ int fg_tree_build(const double *points, const double *weights, int64_t n, int32_
     FG_REQUIRE(points || n == 0, FG_EINVAL, "null points");
     FG_REQUIRE(n >= 1 && dim >= 1, FG_EINVAL, "points must be a non-empty (N, D) array");
     FG_REQUIRE(leaf_threshold >= 1, FG_EINVAL, "leaf threshold must be at least 1");
-    DBuf sp, sw;
+    const int kd = kernel_dim(dim);
+    FG_REQUIRE(kd > 0, FG_EUNSUPPORTED, "dimension > 16 is not supported by this build");
+    DBuf sp, sw, spad;
     const void *dp, *dw = nullptr;
     FG_TRY(to_device(points, sizeof(double) * n * dim, sp, &dp));
     if (weights) FG_TRY(to_device(weights, sizeof(double) * n, sw, &dw));
+    if (kd != dim) {
+        // 9..16 dimensions run as 12 or 16 with zero coordinates appended
+        FG_TRY(spad.reserve(sizeof(double) * n * kd));
+        count_launch();
+        pad_coords_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
+            n, dim, kd, (const double *)dp, spad.as<double>());
+        FG_CUDA_TRY(cudaGetLastError());
+        dp = spad.p;
+    }
     auto *t = new fg_tree();
     FG_CUDA_TRY(cudaGetDevice(&t->t.device));
-    int st = tree_build((const double *)dp, (const double *)dw, n, dim, leaf_threshold, t->t);
+    t->t.dim_user = dim;
+    int st = tree_build((const double *)dp, (const double *)dw, n, kd, leaf_threshold, t->t);
     if (st != FG_OK) {
         delete t;
         return st;
@@ -479,7 +499,7 @@ int fg_tree_info(const fg_tree *tree, int64_t *n, int32_t *dim, int64_t *nnodes,
                  double *total_weight, int32_t *levels) {
     FG_REQUIRE(tree, FG_EINVAL, "null tree");
     if (n) *n = tree->t.n;
-    if (dim) *dim = tree->t.dim;
+    if (dim) *dim = tree->t.dim_user;
     if (nnodes) *nnodes = tree->t.nnodes;
     if (total_weight) *total_weight = tree->t.total_w;
     if (levels) *levels = tree->t.levels;
@@ -496,13 +516,13 @@ int fg_tree_export(const fg_tree *tree, int64_t *perm, int64_t *start, int64_t *
                        right);
 }
 
-__global__ void unpack_points_kernel(int64_t n, int dim, int stride, const double *pw,
+__global__ void unpack_points_kernel(int64_t n, int dim, int kd, int stride, const double *pw,
                                      double *pts, double *w) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     if (pts)
         for (int d = 0; d < dim; d++) pts[i * dim + d] = pw[i * stride + d];
-    if (w) w[i] = pw[i * stride + dim];
+    if (w) w[i] = pw[i * stride + kd];
 }
 
 int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
@@ -510,15 +530,16 @@ int fg_tree_points(const fg_tree *tree, double *points, double *weights) {
     DeviceGuard g(tree->t.device);
     FG_TRY(tree_use(const_cast<TreeDev &>(tree->t)));
     const TreeDev &t = tree->t;
+    const int du = t.dim_user;
     DBuf tp, tw;
-    if (points) FG_TRY(tp.reserve(sizeof(double) * t.n * t.dim));
+    if (points) FG_TRY(tp.reserve(sizeof(double) * t.n * du));
     if (weights) FG_TRY(tw.reserve(sizeof(double) * t.n));
     count_launch();
     unpack_points_kernel<<<(unsigned)((t.n + 255) / 256), 256, 0, stream()>>>(
-        t.n, t.dim, t.stride, t.pw.as<double>(), points ? tp.as<double>() : nullptr,
+        t.n, du, t.dim, t.stride, t.pw.as<double>(), points ? tp.as<double>() : nullptr,
         weights ? tw.as<double>() : nullptr);
     FG_CUDA_TRY(cudaGetLastError());
-    if (points) FG_TRY(from_device(points, tp.p, sizeof(double) * t.n * t.dim));
+    if (points) FG_TRY(from_device(points, tp.p, sizeof(double) * t.n * du));
     if (weights) FG_TRY(from_device(weights, tw.p, sizeof(double) * t.n));
     FG_CUDA_TRY(cudaStreamSynchronize(stream()));
     return FG_OK;
@@ -715,8 +736,10 @@ int fg_run_range(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t m
 
 int fg_iset_export(int32_t dim, int32_t order, int32_t *K, int32_t *digits, int32_t *degrees,
                    double *fact, int32_t *prefix, int32_t *npairs, int32_t *pairs) {
-    FG_REQUIRE(dim >= 1 && dim <= kMaxDim && order >= 1 && iset_count(dim, order) <= 4096,
-               FG_EINVAL, "index set: need 1 <= dim <= 8, order >= 1, C(dim+order-1, dim) <= 4096");
+    FG_REQUIRE(dim >= 1 && dim <= kMaxUserDim && (dim <= kMaxDim || order == 1) && order >= 1 &&
+                   iset_count(dim, order) <= 4096,
+               FG_EINVAL, "index set: need 1 <= dim <= 8 (16 at order 1), order >= 1, "
+                          "C(dim+order-1, dim) <= 4096");
     SeriesTables T;
     std::vector<std::vector<int>> idx;
     host_tables(dim, order, T, idx);

@@ -12,7 +12,13 @@
 
 namespace fg {
 
-constexpr int kMaxDim = 8;      // template-specialised dimensions 1..8
+constexpr int kMaxDim = 8;      // index-set digit rows (series tables) hold 8 dimensions
+// Kernel dimensions: 1..8 natively; 9..12 and 13..16 run as 12 and 16 with the
+// extra coordinates zero (distances, boxes, the split rule and therefore the
+// tree, and every sum are unchanged; the series bounds use the user dimension)
+constexpr int kMaxUserDim = 16;
+inline int kernel_dim(int dim) { return dim <= 8 ? dim : dim <= 12 ? 12 : dim <= 16 ? 16 : -1; }
+constexpr int kDimSlots = 17;  // per-dimension caches indexed by kernel dimension
 constexpr int kMaxOrder = 8;    // series order cap on the device (plimit <= 8)
 constexpr int kMaxK = 256;      // coefficient-count cap per expansion
 constexpr double kSqrt2 = 1.4142135623730951;
@@ -166,7 +172,8 @@ struct TreeDev {
         if (ready) cudaEventDestroy(ready);
     }
     int64_t n = 0;
-    int dim = 0, leaf = 25, stride = 0;  // stride: doubles per packed point
+    int dim = 0, leaf = 25, stride = 0;  // stride: doubles per packed point; dim = kernel dim
+    int dim_user = 0;                    // the caller's dimension (<= dim, see kernel_dim)
     int64_t nnodes = 0;
     int levels = 0;
     double total_w = 0.0;

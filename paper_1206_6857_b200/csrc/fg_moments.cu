@@ -229,7 +229,7 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
                            : mom_partial_kernel<D, kMomKPLMax>;
     const int ki = kpl <= 1 ? 0 : kpl <= 2 ? 1 : kpl <= 4 ? 2 : 3;
     struct MomGrid {
-        int g[kMaxDim + 1][4] = {};
+        int g[kDimSlots][4] = {};
     };
     auto &c_grid = scratch<MomGrid, MomGrid>().g;  // per device
     if (!c_grid[D][ki]) {
@@ -355,7 +355,9 @@ int node_js(TreeDev &t) {
         case 5: st = node_js_t<5>(t); break;
         case 6: st = node_js_t<6>(t); break;
         case 7: st = node_js_t<7>(t); break;
-        default: st = node_js_t<8>(t); break;
+        case 8: st = node_js_t<8>(t); break;
+        case 12: st = node_js_t<12>(t); break;
+        default: st = node_js_t<16>(t); break;
     }
     FG_TRY(st);
     t.js_valid = true;
@@ -395,7 +397,9 @@ int moments_refresh(TreeDev &t, double h, int plimit) {
             case 5: st = moments_direct<5>(t, *T, h, t.mom0); break;
             case 6: st = moments_direct<6>(t, *T, h, t.mom0); break;
             case 7: st = moments_direct<7>(t, *T, h, t.mom0); break;
-            default: st = moments_direct<8>(t, *T, h, t.mom0); break;
+            case 8: st = moments_direct<8>(t, *T, h, t.mom0); break;
+            case 12: st = moments_direct<12>(t, *T, h, t.mom0); break;
+            default: st = moments_direct<16>(t, *T, h, t.mom0); break;
         }
         FG_TRY(st);
         FG_CUDA_TRY(cudaMemcpyAsync(t.mom.p, t.mom0.p, sizeof(double) * total,

@@ -20,14 +20,15 @@ constexpr int kNaiveThreads = 256;
 constexpr int kNaiveTile = 256;
 
 // Pack row-major (n x dim) coordinates (+ optional weights) into records.
+// records of the kernel dimension kd >= dim: coordinates, zero padding, weight
 __global__ void pack_points_kernel(const double *__restrict__ pts, const double *__restrict__ w,
-                                   int64_t n, int dim, int stride, double *__restrict__ out) {
+                                   int64_t n, int dim, int kd, int stride, double *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     double *o = out + i * stride;
-    for (int d = 0; d < dim; d++) o[d] = pts[i * dim + d];
-    o[dim] = w ? w[i] : 1.0;
-    for (int d = dim + 1; d < stride; d++) o[d] = 0.0;
+    for (int d = 0; d < kd; d++) o[d] = d < dim ? pts[i * dim + d] : 0.0;
+    o[kd] = w ? w[i] : 1.0;
+    for (int d = kd + 1; d < stride; d++) o[d] = 0.0;
 }
 
 // CTA-wide min of lo[] and max of hi[]; every thread gets the result
@@ -200,7 +201,9 @@ struct NaiveScr {
 };
 
 int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w, int64_t n,
-              int dim, const double *hs, int nh, double *d_out) {
+              int dim_user, const double *hs, int nh, double *d_out) {
+    const int dim = kernel_dim(dim_user);
+    FG_REQUIRE(dim > 0, FG_EUNSUPPORTED, "naive_sum: dimension > 16 is not supported by this build");
     const int S = packed_stride(dim);
     NaiveScr &ns = scratch<NaiveScr, NaiveScr>();
     DBuf &g_naive_q = ns.q, &g_naive_r = ns.r, &g_naive_part = ns.part;
@@ -208,10 +211,10 @@ int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w
     FG_TRY(g_naive_r.reserve(sizeof(double) * n * S));
     count_launch();
     pack_points_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream()>>>(
-        d_q, nullptr, m, dim, S, g_naive_q.as<double>());
+        d_q, nullptr, m, dim_user, dim, S, g_naive_q.as<double>());
     count_launch();
     pack_points_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
-        d_r, d_w, n, dim, S, g_naive_r.as<double>());
+        d_r, d_w, n, dim_user, dim, S, g_naive_r.as<double>());
     FG_CUDA_TRY(cudaGetLastError());
     const int qpt = dim <= 4 ? 2 : 1;
     const int64_t qtiles = (m + kNaiveThreads * qpt - 1) / (kNaiveThreads * qpt);
@@ -243,9 +246,11 @@ int naive_sum(const double *d_q, int64_t m, const double *d_r, const double *d_w
             FG_NAIVE_CASE(6)
             FG_NAIVE_CASE(7)
             FG_NAIVE_CASE(8)
+            FG_NAIVE_CASE(12)
+            FG_NAIVE_CASE(16)
 #undef FG_NAIVE_CASE
             default:
-                set_error("naive_sum: dimension > 8 is not supported by this build");
+                set_error("naive_sum: dimension > 16 is not supported by this build");
                 return FG_EUNSUPPORTED;
         }
         FG_TRY(st);

@@ -39,7 +39,11 @@ __device__ __forceinline__ uint64_t digits_of(const uint8_t *__restrict__ digits
     return __ldg(reinterpret_cast<const unsigned long long *>(digits) + k);
 }
 
-__device__ __forceinline__ int digit(uint64_t dg, int d) { return (int)((dg >> (8 * d)) & 0xff); }
+// digit d of a packed row (rows hold 8 digits; beyond that only order-1
+// index sets exist, whose digits are all zero)
+__device__ __forceinline__ int digit(uint64_t dg, int d) {
+    return d < 8 ? (int)((dg >> (8 * d)) & 0xff) : 0;
+}
 
 // prod_d table[d][digit_d] (MultiIndexSet.products, kernel_math.py:169-176)
 template <int D, class Table>

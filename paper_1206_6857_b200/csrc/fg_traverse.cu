@@ -386,7 +386,8 @@ int query_blocks(TreeDev &t) {
             t.qb_wsum.as<double>());                                                        \
         break;
     switch (D) {
-        FG_QB(1) FG_QB(2) FG_QB(3) FG_QB(4) FG_QB(5) FG_QB(6) FG_QB(7) FG_QB(8)
+        FG_QB(1) FG_QB(2) FG_QB(3) FG_QB(4) FG_QB(5) FG_QB(6) FG_QB(7) FG_QB(8) FG_QB(12)
+        FG_QB(16)
         default: return FG_EUNSUPPORTED;
     }
 #undef FG_QB
@@ -658,6 +659,8 @@ static int launch_dispatch_t(int D, TravArgs &A, size_t smem, int64_t nb) {
         case 6: return launch_traverse<6, AUDIT, M>(A, smem, nb);
         case 7: return launch_traverse<7, AUDIT, M>(A, smem, nb);
         case 8: return launch_traverse<8, AUDIT, M>(A, smem, nb);
+        case 12: return launch_traverse<12, AUDIT, M>(A, smem, nb);
+        case 16: return launch_traverse<16, AUDIT, M>(A, smem, nb);
         default: return FG_EUNSUPPORTED;
     }
 }
@@ -742,6 +745,8 @@ static int queue_far(TreeDev &q, TravArgs &A) {
         case 6: return launch_far_t<6>(A, ntask);
         case 7: return launch_far_t<7>(A, ntask);
         case 8: return launch_far_t<8>(A, ntask);
+        case 12: return launch_far_t<12>(A, ntask);
+        case 16: return launch_far_t<16>(A, ntask);
         default: return FG_EUNSUPPORTED;
     }
 }
@@ -787,7 +792,8 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     FG_REQUIRE(nh >= 1 && nh <= kMaxSweep, FG_EINVAL, "bad bandwidth count");
     FG_REQUIRE(eps >= 0.0, FG_EINVAL, "epsilon must be non-negative");
     FG_REQUIRE(mode >= FG_DFD && mode <= FG_DITO, FG_EINVAL, "unknown algorithm");
-    FG_REQUIRE(q.dim == r.dim, FG_EINVAL, "query and reference dimensions differ");
+    FG_REQUIRE(q.dim == r.dim && q.dim_user == r.dim_user, FG_EINVAL,
+               "query and reference dimensions differ");
     for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const int D = q.dim;
     const bool series = mode == FG_DITO;
@@ -838,7 +844,8 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
         A.degrees = T->degrees.as<int>();
         A.mom_K = r.mom_K;
         double ct[kMaxOrder + 1], cross[kMaxOrder + 1], floor_c;
-        tail_tables(D, plimit, ct, cross, &floor_c);
+        // the caller's dimension: padded coordinates add nothing to the bounds
+        tail_tables(q.dim_user > 0 ? q.dim_user : D, plimit, ct, cross, &floor_c);
         for (int p = 0; p <= plimit; p++) {
             A.ct[p] = ct[p];
             A.cross[p] = cross[p];
@@ -850,11 +857,12 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
     // points, the FP32 batch
     size_t smem;
     {
-        static const int fixd[9] = {0,
+        static const int fixd[kDimSlots] = {0,
                                     warp_fixed_doubles<1>(), warp_fixed_doubles<2>(),
                                     warp_fixed_doubles<3>(), warp_fixed_doubles<4>(),
                                     warp_fixed_doubles<5>(), warp_fixed_doubles<6>(),
-                                    warp_fixed_doubles<7>(), warp_fixed_doubles<8>()};
+                                    warp_fixed_doubles<7>(), warp_fixed_doubles<8>(), 0, 0, 0,
+                                    warp_fixed_doubles<12>(), 0, 0, 0, warp_fixed_doubles<16>()};
         smem = sizeof(double) * (fixd[D] + ((A.K + 1) & ~1)) *kTravWarps;
     }
     TravScratch &g_scr = trav_scratch();

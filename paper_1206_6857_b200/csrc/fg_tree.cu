@@ -230,7 +230,7 @@ static int build_levels(int64_t n, int leaf, BuildBufs &B, TreeDev &t) {
 
     // resident grid for the cooperative launch (cached per dimension)
     struct GridCache {
-        int g[kMaxDim + 1] = {0};
+        int g[kDimSlots] = {0};
     };
     auto &grid_cache = scratch<GridCache, GridCache>().g;  // per device
     int dev = 0;
@@ -307,7 +307,7 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
     FG_REQUIRE(n >= 1, FG_EINVAL, "points must be a non-empty (N, D) array");
     FG_REQUIRE(dim >= 1, FG_EINVAL, "points must be a non-empty (N, D) array");
     FG_REQUIRE(leaf >= 1, FG_EINVAL, "leaf threshold must be at least 1");
-    FG_REQUIRE(dim <= kMaxDim, FG_EUNSUPPORTED, "dimension > 8 is not supported by this build");
+    FG_REQUIRE(kernel_dim(dim) == dim, FG_EUNSUPPORTED, "kernel dimension must be 1..8, 12 or 16");
     FG_REQUIRE(n < (int64_t)1 << 30, FG_EUNSUPPORTED, "more than 2^30 points per tree");
     // build scratch is kept between builds (grow-only): a per-step tree costs
     // no allocation calls
@@ -368,7 +368,9 @@ int tree_build(const double *d_points, const double *d_weights, int64_t n, int d
         case 5: return build_levels<5>(n, leaf, B, t);
         case 6: return build_levels<6>(n, leaf, B, t);
         case 7: return build_levels<7>(n, leaf, B, t);
-        default: return build_levels<8>(n, leaf, B, t);
+        case 8: return build_levels<8>(n, leaf, B, t);
+        case 12: return build_levels<12>(n, leaf, B, t);
+        default: return build_levels<16>(n, leaf, B, t);
     }
 }
 
@@ -404,7 +406,7 @@ int tree_export(const TreeDev &t, int64_t *perm, int64_t *start, int64_t *end, d
                 double *hi, double *center, double *weight, double *inf_radius, int64_t *left,
                 int64_t *right) {
     const int64_t nn = t.nnodes;
-    const int D = t.dim;
+    const int D = t.dim, DU = t.dim_user > 0 ? t.dim_user : t.dim;
     std::vector<int4> ni(nn);
     std::vector<double> box(nn * 2 * D), ctr(nn * D);
     std::vector<double2> wr(nn);
@@ -422,10 +424,10 @@ int tree_export(const TreeDev &t, int64_t *perm, int64_t *start, int64_t *end, d
         if (end) end[p] = (int64_t)ni[v].x + ni[v].y;
         if (left) left[p] = ni[v].z >= 0 ? pre[ni[v].z] : -1;
         if (right) right[p] = ni[v].w >= 0 ? pre[ni[v].w] : -1;
-        for (int d = 0; d < D; d++) {
-            if (lo) lo[p * D + d] = box[v * 2 * D + d];
-            if (hi) hi[p * D + d] = box[v * 2 * D + D + d];
-            if (center) center[p * D + d] = ctr[v * D + d];
+        for (int d = 0; d < DU; d++) {  // the caller's dimensions (padding dropped)
+            if (lo) lo[p * DU + d] = box[v * 2 * D + d];
+            if (hi) hi[p * DU + d] = box[v * 2 * D + D + d];
+            if (center) center[p * DU + d] = ctr[v * D + d];
         }
         if (weight) weight[p] = wr[v].x;
         if (inf_radius) inf_radius[p] = wr[v].y;
