@@ -823,6 +823,30 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
         const unsigned long long *rec = reinterpret_cast<const unsigned long long *>(pbuf + off * P);
         unsigned long long acc[kQPL][2] = {{0ull, 0ull}, {0ull, 0ull}};
         int j = 0;
+#ifndef FG_PAIR_UNROLL
+#define FG_PAIR_UNROLL 2
+#endif
+        constexpr int PU = FG_PAIR_UNROLL;  // record pairs per iteration (PU x 2 chains)
+        for (; j + PU <= np; j += PU) {
+            unsigned long long r[PU][P2];
+#pragma unroll
+            for (int u = 0; u < PU; u++)
+#pragma unroll
+                for (int k = 0; k < P2; k += 2) {
+                    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(rec + (j + u) * P2 + k);
+                    r[u][k] = v.x;
+                    r[u][k + 1] = v.y;
+                }
+#pragma unroll
+            for (int q = 0; q < kQPL; q++)
+#pragma unroll
+                for (int u = 0; u < PU; u++) {
+                    unsigned long long t = f2_fma(r[u][D], nss, aa[q]);
+#pragma unroll
+                    for (int d = 0; d < D; d++) f2_fma_acc(t, xx[q][d], r[u][d]);
+                    f2_fma_acc(acc[q][u & 1], f2_ex2(t), r[u][D + 1]);
+                }
+        }
         for (; j + 2 <= np; j += 2) {
             unsigned long long r[2][P2];
 #pragma unroll
