@@ -33,7 +33,8 @@ struct Status {
     do {                                                                         \
         cudaError_t _e = (expr);                                                 \
         if (_e != cudaSuccess) {                                                 \
-            ::fg::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+            ::fg::set_error(std::string(#expr) + " (" + __FILE__ + ":" +        \
+                            std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
             return FG_ECUDA;                                                     \
         }                                                                        \
     } while (0)

@@ -43,6 +43,10 @@ __global__ void moments_rescale_kernel(int64_t total, int K, const double *__res
 // No level-by-level dependency: two launches for the whole tree.
 constexpr int kMomChunk = 256;
 constexpr int kMomWarps = 8;
+// power-table orders held per (lane, dimension): padded dimensions (> 8) only
+// carry order-1 index sets, which keeps their shared memory small
+template <int D>
+constexpr int mom_ord() { return D > 8 ? 1 : kMaxOrder; }
 constexpr int kMomKPLMax = kMaxK / 32;  // coefficients per lane (largest K)
 
 __global__ void mom_items_count_kernel(int64_t nn, const int4 *__restrict__ node_i,
@@ -72,16 +76,16 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
     extern __shared__ double sh[];  // per warp: 32 points x D x p powers (weight folded in d=0)
     const int lane = threadIdx.x & 31;
     const int P = p;
-    double *tab = sh + (threadIdx.x >> 5) * 32 * D * kMaxOrder;
+    double *tab = sh + (threadIdx.x >> 5) * 32 * D * mom_ord<D>();
     const int gwarps = gridDim.x * kMomWarps;
-    // per owned coefficient: table offsets d * kMaxOrder + digit_d
+    // per owned coefficient: table offsets d * mom_ord<D>() + digit_d
     int toff[kMomKPL][D];
 #pragma unroll
     for (int j = 0; j < kMomKPL; j++) {
         const int k = lane + 32 * j;
         const uint64_t dg = k < K ? digits_of(digits, k) : 0;
 #pragma unroll
-        for (int d = 0; d < D; d++) toff[j][d] = d * kMaxOrder + digit(dg, d);
+        for (int d = 0; d < D; d++) toff[j][d] = d * mom_ord<D>() + digit(dg, d);
     }
     for (int it = blockIdx.x * kMomWarps + (threadIdx.x >> 5); it < nitems; it += gwarps) {
         const int2 item = items[it];
@@ -106,7 +110,7 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
                 for (int d = 0; d < D; d++) {
                     const double u = (y[d] - c[d]) / sc;
                     double v = d == 0 ? w : 1.0;
-                    double *row = tab + (lane * D + d) * kMaxOrder;
+                    double *row = tab + (lane * D + d) * mom_ord<D>();
                     for (int k = 0; k < P; k++) {
                         row[k] = v;
                         v *= u;
@@ -118,7 +122,7 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
             int q = 0;
             // two points per round: independent product chains
             for (; q + 1 < nv; q += 2) {
-                const double *t0 = tab + q * D * kMaxOrder, *t1 = t0 + D * kMaxOrder;
+                const double *t0 = tab + q * D * mom_ord<D>(), *t1 = t0 + D * mom_ord<D>();
 #pragma unroll
                 for (int j = 0; j < kMomKPL; j++) {
                     if (32 * j < K) {
@@ -133,7 +137,7 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
                 }
             }
             if (q < nv) {
-                const double *t0 = tab + q * D * kMaxOrder;
+                const double *t0 = tab + q * D * mom_ord<D>();
 #pragma unroll
                 for (int j = 0; j < kMomKPL; j++) {
                     if (32 * j < K) {
@@ -221,7 +225,7 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     struct MomPartial;
     DBuf &s_partial = scratch<MomPartial>();
     FG_TRY(s_partial.reserve(sizeof(double) * (size_t)t.mom_nitems * K));
-    const size_t smem = sizeof(double) * 32 * D * kMaxOrder * kMomWarps;
+    const size_t smem = sizeof(double) * 32 * D * mom_ord<D>() * kMomWarps;
     const int kpl = (K + 31) / 32;
     auto kern = kpl <= 1 ? mom_partial_kernel<D, 1>
                 : kpl <= 2 ? mom_partial_kernel<D, 2>

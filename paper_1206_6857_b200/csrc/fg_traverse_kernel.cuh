@@ -824,7 +824,7 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
         unsigned long long acc[kQPL][2] = {{0ull, 0ull}, {0ull, 0ull}};
         int j = 0;
 #ifndef FG_PAIR_UNROLL
-#define FG_PAIR_UNROLL 2
+#define FG_PAIR_UNROLL 4
 #endif
         constexpr int PU = FG_PAIR_UNROLL;  // record pairs per iteration (PU x 2 chains)
         for (; j + PU <= np; j += PU) {

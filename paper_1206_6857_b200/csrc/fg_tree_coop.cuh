@@ -212,7 +212,7 @@ __device__ void build_small_levels(const BuildArgs &B, cg::grid_group &g, int le
 }
 
 template <int D>
-__global__ void __launch_bounds__(kBuildThreads)
+__global__ void __launch_bounds__(kBuildThreads, D > 8 ? 2 : 1)
 build_coop_kernel(const BuildArgs B) {
     cg::grid_group g = cg::this_grid();
     __shared__ typename BlockScanU64::TempStorage scan_tmp;
