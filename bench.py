@@ -382,21 +382,27 @@ def run_ours(args):
                 "pair_share": {"fp64": n64 / (pairs_eff * args.steps),
                                "fp32": n32 / (pairs_eff * args.steps)}}
 
-    # end to end through the public API with host buffers: the step's inputs
-    # come from pinned host memory and all its value vectors go back into a
-    # pinned host array (host <-> device copies inside the timed region)
+    # end to end through the public API with host buffers: every rank builds
+    # its tree from pinned host arrays (H2D inside the step); one rank runs
+    # the whole sweep into a pinned host array, N ranks run their shards into
+    # a device vector, all-reduce it, and rank 0 reads the result back
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         pts_h = torch.from_numpy(wl.references).pin_memory().numpy()
         w_h = torch.from_numpy(wl.weights).pin_memory().numpy()
         out_h = torch.empty((len(wl.bandwidths), wl.m), dtype=torch.float64,
-                            pin_memory=True).numpy()
+                            pin_memory=True)
 
         def e2e_step():
             store = fg.PointStore(pts_h, w_h)
             tree = fg.build_tree(store, 25)
             cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon)
-            return [r.values for r in fg.sweep_run(cfg, tree, tree, wl.bandwidths, out=out_h)]
+            if world == 1:
+                fg.sweep_run(cfg, tree, tree, wl.bandwidths, out=out_h.numpy())
+            else:
+                run_sharded_sweep(cfg, tree, tree, wl.bandwidths, vals_d, rank, world)
+                if rank == 0:
+                    out_h.copy_(vals_d, non_blocking=True)
 
         with torch.cuda.stream(stream):
             e2e_step()
@@ -404,6 +410,8 @@ def run_ours(args):
             for _ in range(max(1, args.steps)):
                 flush.zero_()
                 stream.synchronize()
+                if world > 1:
+                    dist.barrier()
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
@@ -411,10 +419,15 @@ def run_ours(args):
                 e1.record(stream)
                 e1.synchronize()
                 et.append(e0.elapsed_time(e1) * 1e-3)
-        e2e = {"value": pairs_eff * len(et) / sum(et), "unit": UNIT,
-               "h2d_bytes_per_step": int(wl.references.nbytes + wl.weights.nbytes),
+        etot = sum(et)
+        if world > 1:
+            t = torch.tensor([etot], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            etot = float(t.item())
+        e2e = {"value": pairs_eff * len(et) / etot, "unit": UNIT,
+               "h2d_bytes_per_step": int(world * (wl.references.nbytes + wl.weights.nbytes)),
                "d2h_bytes_per_step": int(8 * wl.m * len(wl.bandwidths)),
-               "ms_per_step": 1e3 * sum(et) / len(et)}
+               "ms_per_step": 1e3 * etot / len(et)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
