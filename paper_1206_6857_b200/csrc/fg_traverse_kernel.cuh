@@ -602,6 +602,37 @@ __device__ __forceinline__ void f2_fma_acc(unsigned long long &acc, unsigned lon
 __device__ __forceinline__ unsigned long long f2_ex2(unsigned long long v) {
     return f2_pack(ex2_approx(f2_lo(v)), ex2_approx(f2_hi(v)));
 }
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// 2^t on the FMA pipe (t <= 0, both halves): t is clamped at -125, split as
+// n + f with n = rint(t) (the 1.5 * 2^23 trick) and f in [-0.5, 0.5], 2^f by a
+// degree-5 polynomial (fitted to relative error 2^-23.7; evaluated in FP32
+// Horner form: <= 2^-22.2 over 2e6 points, against ex2.approx's measured
+// 2^-22.7 -- both inside the 2^-17 share fp32_item_bound / fp32_pair_bound
+// reserve for the exponential, weight rounding and accumulation), then n is
+// added to the exponent bits.  Results below 2^-125 come out as ~2^-125:
+// such terms have exponent a > 86 > a_c, inside the bounds' absolute part.
+// It relieves the SFU (one ex2 per pair, the FP32 base case's bound) for a
+// share of the pairs (the FA4 offload).
+__device__ __forceinline__ unsigned long long f2_ex2_poly(unsigned long long t) {
+    const float lo = fmaxf(f2_lo(t), -125.f), hi = fmaxf(f2_hi(t), -125.f);
+    const unsigned long long tc = f2_pack(lo, hi);
+    const unsigned long long M = f2_pack(12582912.f, 12582912.f);
+    const unsigned long long r = f2_add(tc, M);
+    const unsigned long long f = f2_sub(tc, f2_sub(r, M));
+    unsigned long long p = f2_fma(f2_pack(0.00132748f, 0.00132748f), f,
+                                  f2_pack(0.00967553f, 0.00967553f));
+    p = f2_fma(p, f, f2_pack(0.05550718f, 0.05550718f));
+    p = f2_fma(p, f, f2_pack(0.2402212f, 0.2402212f));
+    p = f2_fma(p, f, f2_pack(0.69314694f, 0.69314694f));
+    p = f2_fma(p, f, f2_pack(1.0000001f, 1.0000001f));
+    const unsigned plo = (unsigned)p + ((unsigned)r << 23);
+    const unsigned phi = (unsigned)(p >> 32) + ((unsigned)(r >> 32) << 23);
+    return (unsigned long long)plo | ((unsigned long long)phi << 32);
+}
 
 // Stream one staged batch: nitems items, item t with `cnt` AoS records
 // (fstride floats: coordinates about its anchor, weight) at record offset
@@ -827,6 +858,11 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
 #define FG_PAIR_UNROLL 4
 #endif
         constexpr int PU = FG_PAIR_UNROLL;  // record pairs per iteration (PU x 2 chains)
+#ifndef FG_POLY_CHAINS
+#define FG_POLY_CHAINS 0
+#endif
+        // chains (slot q, pair u) per iteration whose 2^t runs on the FMA pipe
+        constexpr int NPOLY = FG_POLY_CHAINS;
         for (; j + PU <= np; j += PU) {
             unsigned long long r[PU][P2];
 #pragma unroll
@@ -844,7 +880,8 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
                     unsigned long long t = f2_fma(r[u][D], nss, aa[q]);
 #pragma unroll
                     for (int d = 0; d < D; d++) f2_fma_acc(t, xx[q][d], r[u][d]);
-                    f2_fma_acc(acc[q][u & 1], f2_ex2(t), r[u][D + 1]);
+                    const bool poly = u == PU - 1 && (NPOLY >= 2 || (NPOLY == 1 && q == 1));
+                    f2_fma_acc(acc[q][u & 1], poly ? f2_ex2_poly(t) : f2_ex2(t), r[u][D + 1]);
                 }
         }
         for (; j + 2 <= np; j += 2) {
