@@ -142,6 +142,12 @@ int fg_run(fg_tree *qtree, fg_tree *rtree, double h, double eps, int32_t mode,
  * synchronisation at the end.  values (nh x m) host or device, row j in
  * original query order; counters and seconds (nh each, nullable).  rtree's
  * moments are left at the last bandwidth. */
+/* plimit <= 0 in a sweep -> the engine's own series order cap for the
+ * dimension (fg_engine_plimit: 10 at D = 3, where this engine's evaluators run
+ * every order's exact coefficient count; default_plimit(dim) elsewhere).  The
+ * order bounds of error_bounds.py:107-145 hold for any order, so the eps
+ * contract is unchanged; an explicit plimit is honoured as given. */
+int fg_engine_plimit(int32_t dim);
 int fg_run_sweep(fg_tree *qtree, fg_tree *rtree, const double *bandwidths, int32_t nh,
                  double eps, int32_t mode, int32_t plimit, double *values, fg_counters *counters,
                  double *seconds);

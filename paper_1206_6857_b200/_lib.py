@@ -53,6 +53,7 @@ SIGNATURES = {
     "fg_moments_refresh": [_P, _F64, _I32],
     "fg_moments_export": [_P, _P, _P, _P, _P],
     "fg_run": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P],
+    "fg_engine_plimit": [_I32],
     "fg_query_blocks": [_P, _P],
     "fg_query_block_ranges": [_P, _P, _P],
     "fg_run_audit": [_P, _P, _F64, _F64, _I32, _I32, _P, _P, _P, _P, _I64, _P],

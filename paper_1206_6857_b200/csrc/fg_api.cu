@@ -135,6 +135,15 @@ int default_plimit(int dim) {
     return dim <= 6 ? sched[dim] : 1;
 }
 
+// the engine's own order cap (sweeps with plimit <= 0): fg_series.cuh engine_order_c
+int engine_plimit(int dim) {
+    if (const char *env = getenv("FG_ENGINE_ORDER")) {  // experiment knob
+        const int v = atoi(env);
+        if (v >= 1 && v <= kMaxOrder && iset_count(dim, v) <= kMaxK) return v;
+    }
+    return dim >= 1 && dim <= 8 ? engine_order_c(dim) : default_plimit(dim);
+}
+
 static double fact_d(int n) {
     double f = 1.0;
     for (int i = 2; i <= n; i++) f *= (double)i;
@@ -301,6 +310,8 @@ using namespace fg;
 extern "C" {
 
 int fg_version(void) { return 1; }
+
+int fg_engine_plimit(int32_t dim) { return dim >= 1 && dim <= kMaxUserDim ? engine_plimit(dim) : 0; }
 
 int fg_launch_count(int64_t *count) {
     FG_REQUIRE(count, FG_EINVAL, "null pointer");

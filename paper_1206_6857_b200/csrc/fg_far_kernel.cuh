@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
                     }
                     if (possible <= maxerr) {
                         select_method_gpu(bse, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
-                                          A.ct, A.cross, A.kp, (double)s_cnt / 32.0, H.pair_cost,
+                                          A.ct, A.cross, A.kp, (double)s_cnt / 32.0, H.pair_cost, H.herm_c0, H.herm_c1,
                                           meth, p, bound);
                         int p_h, p_l, p_t;
                         double e_h, e_l, e_t;

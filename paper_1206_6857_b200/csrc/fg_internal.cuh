@@ -19,9 +19,31 @@ constexpr int kMaxDim = 8;      // index-set digit rows (series tables) hold 8 d
 constexpr int kMaxUserDim = 16;
 inline int kernel_dim(int dim) { return dim <= 8 ? dim : dim <= 12 ? 12 : dim <= 16 ? 16 : -1; }
 constexpr int kDimSlots = 17;  // per-dimension caches indexed by kernel dimension
-constexpr int kMaxOrder = 8;    // series order cap on the device (plimit <= 8)
+#ifndef FG_MAX_ORDER
+#define FG_MAX_ORDER 10
+#endif
+constexpr int kMaxOrder = FG_MAX_ORDER;   // series order cap on the device
 constexpr int kMaxK = 256;      // coefficient-count cap per expansion
 constexpr double kSqrt2 = 1.4142135623730951;
+
+// the reference's series order cap per dimension (spatial_index.py:39-44)
+__host__ __device__ constexpr int default_plimit_c(int D) {
+    return D == 1 ? 8 : D == 2 ? 8 : D == 3 ? 6 : D == 4 ? 4 : D == 5 ? 4 : D == 6 ? 2 : 1;
+}
+
+// The engine's own Hermite order cap per dimension: the order its evaluators are
+// compiled for.  At D = 3 it exceeds the reference's default_plimit (6): on a
+// GPU the exhaustive-vs-series crossover sits at higher orders (a K_p-term
+// FP64 dot against N_R FP32 pairs), and every order's bound
+// (error_bounds.py:107-117) holds for any p.  Sweeps use it when the caller
+// leaves RunConfig.plimit unset.
+#ifndef FG_ORDER3
+#define FG_ORDER3 10
+#endif
+__host__ __device__ constexpr int engine_order_c(int D) {
+    return D == 3 ? (FG_ORDER3 <= kMaxOrder ? FG_ORDER3 : kMaxOrder) : default_plimit_c(D);
+}
+
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string &msg);
@@ -158,6 +180,7 @@ const SeriesTables *series_tables(int dim, int order, int *status);
 // tail tables (error_bounds.py:73-92): ct[p] = count/denom, cross[p]
 void tail_tables(int dim, int plimit, double *ct, double *cross, double *floor_c);
 int default_plimit(int dim);  // spatial_index.py:39-44
+int engine_plimit(int dim);   // the engine's own order cap (sweeps with plimit <= 0)
 int iset_count(int dim, int order);
 
 // -------------------------------------------------------------- the tree

@@ -373,7 +373,7 @@ struct RescaleFac;
 int moments_refresh(TreeDev &t, double h, int plimit) {
     FG_REQUIRE(h > 0.0 && std::isfinite(h), FG_EINVAL, "bandwidth must be positive");
     FG_REQUIRE(plimit >= 1, FG_EINVAL, "truncation order must be at least 1");
-    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
+    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (10) is not supported");
     int st = FG_OK;
     const SeriesTables *T = series_tables(t.dim, plimit, &st);
     FG_TRY(st);

@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include "fg_device.cuh"
+#include "fg_exp.cuh"
 #include "fg_internal.cuh"
 
 namespace fg {
@@ -73,10 +74,6 @@ __host__ __device__ constexpr int glex_count(int D, int P) {
     long long r = 1;
     for (int i = 1; i <= D; i++) r = r * (P - 1 + i) / i;
     return (int)r;
-}
-
-__host__ __device__ constexpr int default_plimit_c(int D) {
-    return D == 1 ? 8 : D == 2 ? 8 : D == 3 ? 6 : D == 4 ? 4 : D == 5 ? 4 : D == 6 ? 2 : 1;
 }
 
 template <int D, int P>
@@ -148,56 +145,142 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
     return g == 0.0 ? 0.0 : acc * g;  // (no inf * 0 for absurdly distant centres)
 }
 
-// Graded-lex position of a 3-digit index (for the factorised D = 3 EVALM).
-template <int P>
-struct GLexIndex3 {
-    int idx[P][P][P];
-    constexpr GLexIndex3() : idx{} {
-        constexpr GLex<3, P> G{};
-        for (int a = 0; a < P; a++)
-            for (int b = 0; b < P; b++)
-                for (int c = 0; c < P; c++) idx[a][b][c] = -1;
-        for (int k = 0; k < G.K; k++) idx[G.dig[k][0]][G.dig[k][1]][G.dig[k][2]] = k;
+// Nested layout of an order-PP coefficient set (D = 3): rows (a, b) in
+// lexicographic order, row (a, b) holding A_{a,b,c} for c < PP - a - b, each
+// row padded to an even length so that it is read with 16-byte loads.
+template <int PP>
+struct Nest3 {
+    int start[PP][PP];
+    int total;
+    constexpr Nest3() : start{}, total(0) {
+        int o = 0;
+        for (int a = 0; a < PP; a++)
+            for (int b = 0; a + b < PP; b++) {
+                start[a][b] = o;
+                o += ((PP - a - b) + 1) & ~1;
+            }
+        total = o;
     }
 };
 
-// EVALM for D = 3, factorised: sum_a L0[a] sum_b L1[b] sum_c A_abc L2[c], which
-// takes K + C(P+1,2) + P FMAs instead of 3K multiplies (56 + 21 + 6 vs 168 at
-// P = 6).  Terms of degree >= p are masked (coefficient 0).
-template <int P, class ExpF>
-__device__ __forceinline__ double eval_far_fixed3(const double (&x)[3],
-                                                  const double *__restrict__ c,
-                                                  const double *__restrict__ A, int p,
-                                                  double inv_sc, ExpF expf) {
-    constexpr GLexIndex3<P> I{};
-    double lad[3][P], tt = 0.0;  // Hermite polynomials; e^{-|t|^2} applied once
-#pragma unroll
-    for (int d = 0; d < 3; d++) {
-        const double t = (x[d] - c[d]) * inv_sc;
-        tt = fma(t, t, tt);
-        lad[d][0] = 1.0;
-        if (P > 1) lad[d][1] = 2.0 * t;
-#pragma unroll
-        for (int n = 1; n + 1 < P; n++) lad[d][n + 1] = 2.0 * t * lad[d][n] - 2.0 * n * lad[d][n - 1];
+// both query slots of a lane from one pass over the coefficients
+template <int PP>
+__device__ __forceinline__ void far3_nested2(const double (&ta)[3], const double (&tb)[3],
+                                             const double *__restrict__ A, double &va,
+                                             double &vb) {
+    constexpr Nest3<PP> N{};
+    double l1a[PP], l2a[PP], l1b[PP], l2b[PP];
+    l1a[0] = l2a[0] = l1b[0] = l2b[0] = 1.0;
+    if (PP > 1) {
+        l1a[1] = 2.0 * ta[1];
+        l2a[1] = 2.0 * ta[2];
+        l1b[1] = 2.0 * tb[1];
+        l2b[1] = 2.0 * tb[2];
     }
-    double acc = 0.0;
 #pragma unroll
-    for (int a = 0; a < P; a++) {
-        double t1 = 0.0;
+    for (int n = 1; n + 1 < PP; n++) {
+        l1a[n + 1] = 2.0 * ta[1] * l1a[n] - 2.0 * n * l1a[n - 1];
+        l2a[n + 1] = 2.0 * ta[2] * l2a[n] - 2.0 * n * l2a[n - 1];
+        l1b[n + 1] = 2.0 * tb[1] * l1b[n] - 2.0 * n * l1b[n - 1];
+        l2b[n + 1] = 2.0 * tb[2] * l2b[n] - 2.0 * n * l2b[n - 1];
+    }
+    double acca = 0.0, ha = 1.0, ham = 0.0, accb = 0.0, hb = 1.0, hbm = 0.0;
 #pragma unroll
-        for (int b = 0; a + b < P; b++) {
-            double t2 = 0.0;
+    for (int a = 0; a < PP; a++) {
+        double s1a = 0.0, s1b = 0.0;
 #pragma unroll
-            for (int cc = 0; a + b + cc < P; cc++) {
-                const double coef = (a + b + cc < p) ? A[I.idx[a][b][cc]] : 0.0;
-                t2 = fma(coef, lad[2][cc], t2);
+        for (int b = 0; a + b < PP; b++) {
+            const double2 *row = reinterpret_cast<const double2 *>(A + N.start[a][b]);
+            double s2a = 0.0, s2b = 0.0;
+#pragma unroll
+            for (int cc = 0; a + b + cc < PP; cc += 2) {
+                const double2 v = row[cc >> 1];
+                s2a = cc == 0 ? v.x : fma(v.x, l2a[cc], s2a);
+                s2b = cc == 0 ? v.x : fma(v.x, l2b[cc], s2b);
+                if (a + b + cc + 1 < PP) {
+                    s2a = fma(v.y, l2a[cc + 1], s2a);
+                    s2b = fma(v.y, l2b[cc + 1], s2b);
+                }
             }
-            t1 = fma(t2, lad[1][b], t1);
+            s1a = b == 0 ? s2a : fma(s2a, l1a[b], s1a);
+            s1b = b == 0 ? s2b : fma(s2b, l1b[b], s1b);
         }
-        acc = fma(t1, lad[0][a], acc);
+        acca = a == 0 ? s1a : fma(s1a, ha, acca);
+        accb = a == 0 ? s1b : fma(s1b, hb, accb);
+        const double hna = 2.0 * ta[0] * ha - 2.0 * a * ham;
+        ham = ha;
+        ha = hna;
+        const double hnb = 2.0 * tb[0] * hb - 2.0 * a * hbm;
+        hbm = hb;
+        hb = hnb;
     }
-    const double g = expf(-tt);
-    return g == 0.0 ? 0.0 : acc * g;  // (no inf * 0 for absurdly distant centres)
+    va = acca;
+    vb = accb;
+}
+
+// Staging permutation: position of graded-lex coefficient q (< K_p) in the
+// order-p nested layout, all orders 1..PMAX concatenated (off[p] = first entry
+// of order p).  The traversal kernel copies it to shared memory once per CTA.
+template <int PMAX>
+struct Nest3Perm {
+    static constexpr int kTotal = (PMAX * (PMAX + 1) * (PMAX + 2) * (PMAX + 3)) / 24;  // sum of K_p
+    unsigned char pos[kTotal];
+    int off[PMAX + 2];
+    constexpr Nest3Perm() : pos{}, off{} {
+        constexpr GLex<3, PMAX> G{};
+        int o = 0;
+        off[0] = 0;
+        for (int p = 1; p <= PMAX; p++) {
+            off[p] = o;
+            for (int q = 0; q < G.prefix[p]; q++) {
+                const int a = G.dig[q][0], b = G.dig[q][1], c = G.dig[q][2];
+                int st = 0;  // start of row (a, b) in the order-p layout (as Nest3<p>)
+                for (int aa = 0; aa < p; aa++)
+                    for (int bb = 0; aa + bb < p; bb++) {
+                        if (aa < a || (aa == a && bb < b)) st += ((p - aa - bb) + 1) & ~1;
+                    }
+                pos[o + q] = (unsigned char)(st + c);
+            }
+            o += G.prefix[p];
+        }
+        off[PMAX + 1] = o;
+    }
+};
+constexpr int kNest3Slot = 256;    // doubles per staged item: nested coefficients, then the centre
+constexpr int kNest3Centre = 252;  // (the order-10 layout takes 250)
+
+// Polynomial part of EVALM at the item's own order for both query slots of the
+// lane, out of line (one instance per order, the full register budget each;
+// the coefficients are addressed through the dynamic shared-memory window so
+// that the loads stay shared-memory loads across the call).
+template <int PP>
+__device__ __noinline__ double2 far3_order(double a0, double a1, double a2, double b0, double b1,
+                                           double b2, int off) {
+    extern __shared__ double fg_dyn_smem[];
+    const double ta[3] = {a0, a1, a2}, tb[3] = {b0, b1, b2};
+    double2 r;
+    far3_nested2<PP>(ta, tb, fg_dyn_smem + off, r.x, r.y);
+    return r;
+}
+
+// order dispatch (1 <= p <= PMAX <= 12); off = the staged item's offset in
+// doubles from the dynamic shared-memory base (16-byte aligned)
+template <int PMAX>
+__device__ __forceinline__ double2 far3_eval2(int p, const double (&ta)[3], const double (&tb)[3],
+                                              int off) {
+#define FG_FAR3_CASE(PP)                                                                     \
+    case PP:                                                                                 \
+        if constexpr (PP <= PMAX)                                                            \
+            return far3_order<(PP <= PMAX ? PP : 1)>(ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], \
+                                                     off);                                   \
+        break;
+    switch (p) {
+        FG_FAR3_CASE(1) FG_FAR3_CASE(2) FG_FAR3_CASE(3) FG_FAR3_CASE(4) FG_FAR3_CASE(5)
+        FG_FAR3_CASE(6) FG_FAR3_CASE(7) FG_FAR3_CASE(8) FG_FAR3_CASE(9) FG_FAR3_CASE(10)
+        FG_FAR3_CASE(11) FG_FAR3_CASE(12)
+    }
+#undef FG_FAR3_CASE
+    return make_double2(0.0, 0.0);
 }
 
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)
@@ -378,7 +461,8 @@ __device__ __forceinline__ void select_method_gpu(double base, double r_ref, dou
                                                   double n_ref, int dim, double maxerr,
                                                   int plimit, const double *ct,
                                                   const double *cross, const int *kp, double nq,
-                                                  double pair_cost, int &method, int &order,
+                                                  double pair_cost, double herm_c0,
+                                                  double herm_c1, int &method, int &order,
                                                   double &bound) {
     int p_h, p_l, p_t;
     double e_h, e_l, e_t;
@@ -386,7 +470,7 @@ __device__ __forceinline__ void select_method_gpu(double base, double r_ref, dou
                     e_t);
     const double d = (double)dim;
     double c_h = CUDART_INF, c_l = CUDART_INF, c_t = CUDART_INF;
-    if (p_h) c_h = nq * (32.0 * d + kp[p_h] * (d + 1.0));
+    if (p_h) c_h = nq * (herm_c0 + kp[p_h] * herm_c1);
     if (p_l) c_l = n_ref * (32.0 * d + ((kp[p_l] + 31) / 32) * (d + 1.0));
     if (p_t) c_t = 32.0 * d + ((kp[p_t] + 31) / 32) * (double)kp[p_t] * (d + 1.0);
     const double c_x = nq * n_ref * pair_cost;

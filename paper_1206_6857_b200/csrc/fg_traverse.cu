@@ -902,6 +902,11 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
             double c = fp32 ? (3.0 * D + 8.0) / 6.0 : 2.0 * D + 20.0;
             if (const char *env = getenv("FG_PAIR_COST")) c = atof(env);  // experiment knob
             H.pair_cost = c;
+            // Hermite evaluation per query slot: c0 + c1 K_p
+            H.herm_c0 = 32.0 * D;
+            H.herm_c1 = D + 1.0;
+            if (const char *env = getenv("FG_HERM_C0")) H.herm_c0 = atof(env);  // experiment knobs
+            if (const char *env = getenv("FG_HERM_C1")) H.herm_c1 = atof(env);
         }
     }
     // Bandwidth groups run heaviest-first: a (bandwidth, block) task costs most
@@ -996,7 +1001,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     const int D = q.dim;
     if (plimit <= 0) plimit = default_plimit(D);
     if (mode == FG_DITO) {
-        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit > 8 is not supported on the device");
+        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (10) is not supported");
         FG_REQUIRE(r.mom_valid && r.mom_h == h && r.mom_order >= plimit, FG_ESTALE,
                    "reference moments missing or stale; call refresh_moments for this "
                    "bandwidth first");
@@ -1042,7 +1047,9 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
               double *d_values, fg_counters *counters, double *seconds, int64_t b0, int64_t b1,
               int64_t stride) {
     const int D = q.dim;
-    if (plimit <= 0) plimit = default_plimit(D);
+    // the engine's own order cap unless the caller fixes one (padded
+    // dimensions: the caller's dimension decides, as for the bounds)
+    if (plimit <= 0) plimit = engine_plimit(q.dim_user > 0 ? q.dim_user : D);
     FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
     for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const bool series = mode == FG_DITO;

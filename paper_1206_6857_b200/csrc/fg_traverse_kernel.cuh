@@ -61,6 +61,7 @@ struct TravH {
     float ex2_scale;              // -log2(e) / (2 h^2)
     int ref_leaf;                 // reference nodes with <= ref_leaf points are base items
     double pair_cost;             // selector's exhaustive cost per pair (FP32 or FP64 leaves)
+    double herm_c0, herm_c1;      // selector's Hermite cost per query slot: c0 + c1 K_p
 };
 
 // One audit-ledger event (summation_engine.py:250, 350, 394-398): kind 0 base
@@ -1185,13 +1186,20 @@ __device__ __forceinline__ int warp_excl_scan(int v) {
     return s - v;
 }
 
+static __constant__ Nest3Perm<engine_order_c(3)> c_nest3 = Nest3Perm<engine_order_c(3)>();
+
 template <int D, int MINB, bool AUDIT>
 __global__ void __launch_bounds__(kTravThreads, MINB)
 traverse_kernel(const TravArgs A) {
     constexpr int S = packed_stride(D);
     extern __shared__ double smem[];
     __shared__ double s_tab[kExpTab];
+    // staging permutation of the D = 3 Hermite items (graded-lex -> nested)
+    __shared__ unsigned char s_nest[D == 3 ? ((Nest3Perm<engine_order_c(3)>::kTotal + 15) & ~15) : 16];
     exp_table_init(s_tab);
+    if constexpr (D == 3)
+        for (int i = threadIdx.x; i < Nest3Perm<engine_order_c(3)>::kTotal; i += blockDim.x)
+            s_nest[i] = c_nest3.pos[i];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -1447,7 +1455,7 @@ traverse_kernel(const TravArgs A) {
                     }
                     if (possible <= maxerr)
                         select_method_gpu(base, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
-                                          A.ct, A.cross, A.kp, (double)nq, H.pair_cost, meth, p,
+                                          A.ct, A.cross, A.kp, (double)nq, H.pair_cost, H.herm_c0, H.herm_c1, meth, p,
                                           bound);
                 }
                 const bool cand = meth != 0;
@@ -1876,16 +1884,31 @@ traverse_kernel(const TravArgs A) {
             // Hermite items (EVALM): each item's moments and centre are staged
             // through a cp.async ring in the (now idle) FP64 staging buffer,
             // kRing - 1 items ahead of the one being evaluated
-            constexpr int PF = default_plimit_c(D);
+            constexpr int PF = engine_order_c(D);
             constexpr int kRing = 4;
-            const int slot = (A.K + D + 1) & ~1;
-            const bool ring = A.plimit == PF && kRing * slot <= stage_recs<D>() * S;
+            // D = 3: items are staged in the nested layout of their own order
+            // (fg_series.cuh Nest3, 16-byte coefficient loads); other
+            // dimensions keep the graded-lex prefix
+            const int slot = D == 3 ? kNest3Slot : (A.K + D + 1) & ~1;
+            const int coff = D == 3 ? kNest3Centre : A.K;  // the centre inside a slot
+            // the ring may run over the FP32 record area behind the FP64 staging
+            // buffer (contiguous at D <= 4, idle after the traversal loop)
+            constexpr int kRingDoubles =
+                stage_recs<D>() * S + (f32_direct<D>() ? 0 : f32_cap<D>() * fstride<D>() / 2);
+            const bool ring = A.plimit <= PF && kRing * slot <= kRingDoubles;
             auto stage_item = [&](int k) {
-                const int node = sl[k].x;
+                const int2 e = sl[k];
+                const int node = e.x, po = e.y & 0xff, kc = A.kp[po];  // the item's own order
                 double *dst = sbuf + (k % kRing) * slot;
                 const double *mom = H.r_mom + (int64_t)node * A.mom_K;
-                for (int q = lane; q < A.K; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
-                if (lane < D) __pipeline_memcpy_async(dst + A.K + lane, A.r_c + (int64_t)node * D + lane, 8);
+                if constexpr (D == 3) {
+                    const unsigned char *perm = s_nest + c_nest3.off[po];
+                    for (int q = lane; q < kc; q += 32)
+                        __pipeline_memcpy_async(dst + perm[q], mom + q, 8);
+                } else {
+                    for (int q = lane; q < kc; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
+                }
+                if (lane < D) __pipeline_memcpy_async(dst + coff + lane, A.r_c + (int64_t)node * D + lane, 8);
             };
             if (ring) {
 #pragma unroll 1
@@ -1903,15 +1926,28 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_wait_prior(kRing - 1);
                     __syncwarp();
                     const double *buf = sbuf + (i % kRing) * slot;
+                    if constexpr (D == 3) {
+                        // the item's own order, both query slots from one pass
+                        // over the coefficients (an unused slot holds the centroid)
+                        double ta[3], tb[3], qa = 0.0, qb = 0.0;
+#pragma unroll
+                        for (int d = 0; d < 3; d++) {
+                            const double c = buf[kNest3Centre + d];
+                            ta[d] = (x[0][d] - c) * H.inv_sc;
+                            tb[d] = (x[1][d] - c) * H.inv_sc;
+                            qa = fma(ta[d], ta[d], qa);
+                            qb = fma(tb[d], tb[d], qb);
+                        }
+                        const double ga = fg_exp_fast(-qa, s_tab), gb = fg_exp_fast(-qb, s_tab);
+                        const double2 v = far3_eval2<PF>(p, ta, tb, (int)(buf - smem));
+                        // (no inf * 0 for absurdly distant centres)
+                        pt_est[0] += ga == 0.0 ? 0.0 : v.x * ga;
+                        pt_est[1] += gb == 0.0 ? 0.0 : v.y * gb;
+                    } else {
 #pragma unroll 1
-                    for (int qi = 0; qi < nq; qi++) {
-                        double xq[D];
-                        pick_query<D>(x, qi, xq);
-                        if constexpr (D == 3) {
-                            add_slot(pt_est, qi,
-                                     eval_far_fixed3<PF>(xq, buf + A.K, buf, p, H.inv_sc,
-                                                         [&](double v) { return fg_exp_fast(v, s_tab); }));
-                        } else {
+                        for (int qi = 0; qi < nq; qi++) {
+                            double xq[D];
+                            pick_query<D>(x, qi, xq);
                             add_slot(pt_est, qi,
                                      eval_far_fixed<D, PF>(xq, buf + A.K, buf, p, H.inv_sc,
                                                            [&](double v) { return fg_exp_fast(v, s_tab); }));

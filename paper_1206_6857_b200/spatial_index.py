@@ -27,6 +27,12 @@ def default_plimit(dim: int) -> int:
     return _PLIMIT_SCHEDULE.get(dim, 1)
 
 
+def engine_plimit(dim: int) -> int:
+    """The engine's own series-order cap (``fg_engine_plimit``): what sweeps use
+    when ``RunConfig.plimit`` is None.  10 at D = 3, ``default_plimit`` elsewhere."""
+    return int(_lib.lib().fg_engine_plimit(int(dim)))
+
+
 @dataclass
 class PointStore:
     """(N, D) points with positive weights (spatial_index.py:47-80)."""

@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .spatial_index import KdTree, default_plimit
+from .spatial_index import KdTree, default_plimit, engine_plimit
 
 _ALGORITHMS = ("naive", "dfd", "dfdo", "dito")
 
@@ -266,7 +266,8 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
     hs = np.ascontiguousarray(np.atleast_1d(np.asarray(bandwidths, dtype=float)))
     if hs.size == 0 or np.any(hs <= 0.0):
         raise ValueError("bandwidths must be positive")
-    plimit = config.plimit if config.plimit is not None else default_plimit(qtree.dim)
+    # the engine's own order cap unless the caller fixes one (any order keeps eps)
+    plimit = config.plimit if config.plimit is not None else engine_plimit(qtree.dim)
     nh = hs.shape[0]
     shapes = [(nh, qtree.n)] + ([(qtree.n,)] if nh == 1 else [])
     vals = _lib.check_out(out, shapes) if out is not None else (

@@ -433,10 +433,13 @@ def test_sweep_matches_single_runs(fg, alg):
     dev = torch.zeros(len(hs), 8000, dtype=torch.float64, device="cuda")
     sweep_d = fg.sweep_run(cfg, t, t, hs, out=dev)
     run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[alg]
+    # sweeps run at the engine's own order cap; the single runs are given the same
+    pl = fg.engine_plimit(3)
+    assert pl >= fg.default_plimit(3)
     for j, h in enumerate(hs):
         if alg == "dito":
-            t.refresh_moments(h, fg.default_plimit(3))
-        single = run(fg.RunConfig(bandwidth=h, epsilon=0.01, algorithm=alg), t, t)
+            t.refresh_moments(h, pl)
+        single = run(fg.RunConfig(bandwidth=h, epsilon=0.01, algorithm=alg, plimit=pl), t, t)
         np.testing.assert_array_equal(sweep[j].values, single.values)
         np.testing.assert_array_equal(dev[j].cpu().numpy(), single.values)
         assert sweep[j].counters == single.counters

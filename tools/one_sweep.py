@@ -13,6 +13,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--plimit", type=int, default=None)
     args = ap.parse_args()
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200.configs import config
@@ -20,7 +21,7 @@ def main():
     wl = config(args.config)
     rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
     qt = rt if wl.monochromatic else fg.build_tree(fg.PointStore(wl.queries), 25)
-    cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon)
+    cfg = fg.RunConfig(bandwidth=wl.bandwidths[0], epsilon=wl.epsilon, plimit=args.plimit)
     best = None
     for i in range(args.reps):
         res = fg.sweep_run(cfg, qt, rt, wl.bandwidths)

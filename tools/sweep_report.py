@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--algo", default="dito")
     ap.add_argument("--ref-leaf", type=int, default=0)
     ap.add_argument("--sub", type=int, default=2000)
+    ap.add_argument("--plimit", type=int, default=0, help="series order cap (default: default_plimit(D))")
+    ap.add_argument("--hmin", type=float, default=0.0, help="skip bandwidths below this")
     ap.add_argument("--naive", action="store_true", help="also time the full exhaustive kernel")
     ap.add_argument("--sweep", action="store_true",
                     help="one sweep_run over all bandwidths (after a warm-up sweep)")
@@ -40,7 +42,7 @@ def main():
     t_build = time.perf_counter() - t0
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(wl.m, min(args.sub, wl.m), replace=False))
-    pl = fg.default_plimit(wl.dim)
+    pl = args.plimit or fg.default_plimit(wl.dim)
     print(f"{wl.name} N={wl.n} D={wl.dim} build {t_build*1e3:.1f} ms nodes={rt.node_count} "
           f"levels={rt.levels}")
     if args.sweep:
@@ -63,12 +65,14 @@ def main():
         return
     tot = 0.0
     for h in wl.bandwidths:
+        if h < args.hmin:
+            continue
         t0 = time.perf_counter()
         rt.refresh_moments(h, pl)
         t_ref = time.perf_counter() - t0
         run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[args.algo]
         t0 = time.perf_counter()
-        res = run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon), qt, rt)
+        res = run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, plimit=pl), qt, rt)
         t_run = time.perf_counter() - t0
         exact = fg.naive_sum(qp[idx], wl.references, wl.weights, h).values
         err = oracle.max_rel_error(res.values[idx], exact)
