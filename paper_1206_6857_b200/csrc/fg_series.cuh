@@ -145,82 +145,16 @@ __device__ __forceinline__ double eval_far_fixed(const double (&x)[D],
     return g == 0.0 ? 0.0 : acc * g;  // (no inf * 0 for absurdly distant centres)
 }
 
-// Nested layout of an order-PP coefficient set (D = 3): rows (a, b) in
-// lexicographic order, row (a, b) holding A_{a,b,c} for c < PP - a - b, each
-// row padded to an even length so that it is read with 16-byte loads.
-template <int PP>
-struct Nest3 {
-    int start[PP][PP];
-    int total;
-    constexpr Nest3() : start{}, total(0) {
-        int o = 0;
-        for (int a = 0; a < PP; a++)
-            for (int b = 0; a + b < PP; b++) {
-                start[a][b] = o;
-                o += ((PP - a - b) + 1) & ~1;
-            }
-        total = o;
-    }
-};
-
-// both query slots of a lane from one pass over the coefficients
-template <int PP>
-__device__ __forceinline__ void far3_nested2(const double (&ta)[3], const double (&tb)[3],
-                                             const double *__restrict__ A, double &va,
-                                             double &vb) {
-    constexpr Nest3<PP> N{};
-    double l1a[PP], l2a[PP], l1b[PP], l2b[PP];
-    l1a[0] = l2a[0] = l1b[0] = l2b[0] = 1.0;
-    if (PP > 1) {
-        l1a[1] = 2.0 * ta[1];
-        l2a[1] = 2.0 * ta[2];
-        l1b[1] = 2.0 * tb[1];
-        l2b[1] = 2.0 * tb[2];
-    }
-#pragma unroll
-    for (int n = 1; n + 1 < PP; n++) {
-        l1a[n + 1] = 2.0 * ta[1] * l1a[n] - 2.0 * n * l1a[n - 1];
-        l2a[n + 1] = 2.0 * ta[2] * l2a[n] - 2.0 * n * l2a[n - 1];
-        l1b[n + 1] = 2.0 * tb[1] * l1b[n] - 2.0 * n * l1b[n - 1];
-        l2b[n + 1] = 2.0 * tb[2] * l2b[n] - 2.0 * n * l2b[n - 1];
-    }
-    double acca = 0.0, ha = 1.0, ham = 0.0, accb = 0.0, hb = 1.0, hbm = 0.0;
-#pragma unroll
-    for (int a = 0; a < PP; a++) {
-        double s1a = 0.0, s1b = 0.0;
-#pragma unroll
-        for (int b = 0; a + b < PP; b++) {
-            const double2 *row = reinterpret_cast<const double2 *>(A + N.start[a][b]);
-            double s2a = 0.0, s2b = 0.0;
-#pragma unroll
-            for (int cc = 0; a + b + cc < PP; cc += 2) {
-                const double2 v = row[cc >> 1];
-                s2a = cc == 0 ? v.x : fma(v.x, l2a[cc], s2a);
-                s2b = cc == 0 ? v.x : fma(v.x, l2b[cc], s2b);
-                if (a + b + cc + 1 < PP) {
-                    s2a = fma(v.y, l2a[cc + 1], s2a);
-                    s2b = fma(v.y, l2b[cc + 1], s2b);
-                }
-            }
-            s1a = b == 0 ? s2a : fma(s2a, l1a[b], s1a);
-            s1b = b == 0 ? s2b : fma(s2b, l1b[b], s1b);
-        }
-        acca = a == 0 ? s1a : fma(s1a, ha, acca);
-        accb = a == 0 ? s1b : fma(s1b, hb, accb);
-        const double hna = 2.0 * ta[0] * ha - 2.0 * a * ham;
-        ham = ha;
-        ha = hna;
-        const double hnb = 2.0 * tb[0] * hb - 2.0 * a * hbm;
-        hbm = hb;
-        hb = hnb;
-    }
-    va = acca;
-    vb = accb;
+__host__ __device__ constexpr int nest3_group(int m) {  // G(m): doubles of rows 1..m
+    int g = 0;
+    for (int n = 1; n <= m; n++) g += (n + 1) & ~1;
+    return g;
 }
 
 // Staging permutation: position of graded-lex coefficient q (< K_p) in the
-// order-p nested layout, all orders 1..PMAX concatenated (off[p] = first entry
-// of order p).  The traversal kernel copies it to shared memory once per CTA.
+// order-p nested layout of the row machine below, all orders 1..PMAX
+// concatenated (off[p] = first entry of order p).  The traversal kernel copies
+// it to shared memory once per CTA.
 template <int PMAX>
 struct Nest3Perm {
     static constexpr int kTotal = (PMAX * (PMAX + 1) * (PMAX + 2) * (PMAX + 3)) / 24;  // sum of K_p
@@ -234,11 +168,9 @@ struct Nest3Perm {
             off[p] = o;
             for (int q = 0; q < G.prefix[p]; q++) {
                 const int a = G.dig[q][0], b = G.dig[q][1], c = G.dig[q][2];
-                int st = 0;  // start of row (a, b) in the order-p layout (as Nest3<p>)
-                for (int aa = 0; aa < p; aa++)
-                    for (int bb = 0; aa + bb < p; bb++) {
-                        if (aa < a || (aa == a && bb < b)) st += ((p - aa - bb) + 1) & ~1;
-                    }
+                // groups in order of a; inside a group rows by ascending length
+                int st = nest3_group(p - a - b - 1);
+                for (int aa = 0; aa < a; aa++) st += nest3_group(p - aa);
                 pos[o + q] = (unsigned char)(st + c);
             }
             o += G.prefix[p];
@@ -249,38 +181,113 @@ struct Nest3Perm {
 constexpr int kNest3Slot = 256;    // doubles per staged item: nested coefficients, then the centre
 constexpr int kNest3Centre = 252;  // (the order-10 layout takes 250)
 
-// Polynomial part of EVALM at the item's own order for both query slots of the
-// lane, out of line (one instance per order, the full register budget each;
-// the coefficients are addressed through the dynamic shared-memory window so
-// that the loads stay shared-memory loads across the call).
-template <int PP>
-__device__ __noinline__ double2 far3_order(double a0, double a1, double a2, double b0, double b1,
-                                           double b2, int off) {
-    extern __shared__ double fg_dyn_smem[];
-    const double ta[3] = {a0, a1, a2}, tb[3] = {b0, b1, b2};
-    double2 r;
-    far3_nested2<PP>(ta, tb, fg_dyn_smem + off, r.x, r.y);
-    return r;
+// ---- EVALM at D = 3: the row machine ---------------------------------------
+// sum_{a+b+c<p} A_abc H_a(t0) H_b(t1) H_c(t2) e^{-|t|^2} for both query slots of
+// a lane at the item's own order p (exactly K_p coefficient FMAs per slot) from
+// ONE compact code region (~300 instructions for every order).  Straight-line
+// code per order (K_p FMAs unrolled, ~60 KB for orders 1..10) reaches 0.4-0.5
+// of the DFMA peak alone, but inside the traversal kernel, with the 16 warps of
+// an SM at different items and orders, it is bound by instruction fetch (ncu:
+// 66 % of stall samples "no instruction", 22 % issue utilisation; L0 ~6 KB,
+// L1.5 32 KB): profiles/r02_hermite_evaluators.txt.
+// Layout (Nest3Perm): groups a = 0 .. p-1; group a (m = p - a rows) stores its
+// rows in ASCENDING length n = 1 .. m (b = m - n), every row padded to an even
+// length so that it is read with 16-byte loads.  The chain block_1, block_2,
+// ... is specialised on the row length (straight-line inner sums over c, the
+// inner ladder H_c(t2) in registers), entered at block_1 and left after
+// block_m.  Sum_b S_b H_b(t1) is folded by Clenshaw's recurrence
+// y_b = S_b + 2 t1 y_{b+1} - 2 (b + 1) y_{b+2} (result y_0): two FMAs per row
+// and slot and no middle ladder; H_a(t0) is advanced once per group.
+template <int N>
+__device__ __forceinline__ void far3_row_cl(const double *gs, const double (&l2a)[kMaxOrder],
+                                            const double (&l2b)[kMaxOrder], double t1a,
+                                            double t1b, double &twob, double &y1a, double &y2a,
+                                            double &y1b, double &y2b) {
+    const double2 *row = reinterpret_cast<const double2 *>(gs + nest3_group(N - 1));
+    double ea = 0.0, oa = 0.0, eb = 0.0, ob = 0.0;
+#pragma unroll
+    for (int cc = 0; cc < N; cc += 2) {
+        const double2 v = row[cc >> 1];
+        if (cc == 0) {
+            ea = v.x;
+            eb = v.x;
+        } else {
+            ea = fma(v.x, l2a[cc], ea);
+            eb = fma(v.x, l2b[cc], eb);
+        }
+        if (cc + 1 < N) {
+            if (N >= 6) {  // two partial sums per slot on long rows
+                oa = cc == 0 ? v.y * l2a[1] : fma(v.y, l2a[cc + 1], oa);
+                ob = cc == 0 ? v.y * l2b[1] : fma(v.y, l2b[cc + 1], ob);
+            } else {
+                ea = fma(v.y, l2a[cc + 1], ea);
+                eb = fma(v.y, l2b[cc + 1], eb);
+            }
+        }
+    }
+    if (N >= 6) {
+        ea += oa;
+        eb += ob;
+    }
+    if (N == 1) {
+        y1a = ea;
+        y1b = eb;
+    } else {
+        const double na = fma(t1a, y1a, N == 2 ? ea : fma(-twob, y2a, ea));
+        const double nb = fma(t1b, y1b, N == 2 ? eb : fma(-twob, y2b, eb));
+        y2a = y1a;
+        y1a = na;
+        y2b = y1b;
+        y1b = nb;
+    }
+    twob -= 2.0;
 }
 
-// order dispatch (1 <= p <= PMAX <= 12); off = the staged item's offset in
-// doubles from the dynamic shared-memory base (16-byte aligned)
 template <int PMAX>
-__device__ __forceinline__ double2 far3_eval2(int p, const double (&ta)[3], const double (&tb)[3],
-                                              int off) {
-#define FG_FAR3_CASE(PP)                                                                     \
-    case PP:                                                                                 \
-        if constexpr (PP <= PMAX)                                                            \
-            return far3_order<(PP <= PMAX ? PP : 1)>(ta[0], ta[1], ta[2], tb[0], tb[1], tb[2], \
-                                                     off);                                   \
-        break;
-    switch (p) {
-        FG_FAR3_CASE(1) FG_FAR3_CASE(2) FG_FAR3_CASE(3) FG_FAR3_CASE(4) FG_FAR3_CASE(5)
-        FG_FAR3_CASE(6) FG_FAR3_CASE(7) FG_FAR3_CASE(8) FG_FAR3_CASE(9) FG_FAR3_CASE(10)
-        FG_FAR3_CASE(11) FG_FAR3_CASE(12)
+__device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const double (&tb)[3],
+                                             const double *A, double &va, double &vb) {
+    static_assert(PMAX <= kMaxOrder && PMAX <= 12, "row chain covers orders up to 12");
+    double l2a[kMaxOrder], l2b[kMaxOrder];  // registers
+    l2a[0] = l2b[0] = 1.0;
+    l2a[1] = 2.0 * ta[2];
+    l2b[1] = 2.0 * tb[2];
+#pragma unroll
+    for (int n = 1; n + 1 < PMAX; n++) {
+        if (n + 1 < p) {  // (uniform)
+            l2a[n + 1] = 2.0 * ta[2] * l2a[n] - 2.0 * n * l2a[n - 1];
+            l2b[n + 1] = 2.0 * tb[2] * l2b[n] - 2.0 * n * l2b[n - 1];
+        }
     }
-#undef FG_FAR3_CASE
-    return make_double2(0.0, 0.0);
+    const double t1a = 2.0 * ta[1], t1b = 2.0 * tb[1];
+    double acca = 0.0, ha = 1.0, ham = 0.0, accb = 0.0, hb = 1.0, hbm = 0.0, twoa = 0.0;
+    const double *gs = A;
+#pragma unroll 1
+    for (int m = p; m >= 1; m--) {
+        double y1a = 0.0, y2a = 0.0, y1b = 0.0, y2b = 0.0;
+        double twob = 2.0 * m;  // 2 (b + 1) of the row being folded
+        do {
+#define FG_ROWC(N)                                                                  \
+    if constexpr (N <= PMAX) {                                                      \
+        far3_row_cl<N>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b);           \
+        if (m == N) break;                                                          \
+    }
+            FG_ROWC(1) FG_ROWC(2) FG_ROWC(3) FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7)
+            FG_ROWC(8) FG_ROWC(9) FG_ROWC(10) FG_ROWC(11) FG_ROWC(12)
+#undef FG_ROWC
+        } while (0);
+        gs += ((m + 1) >> 1) * (((m + 1) >> 1) + ((m & 1) ? 0 : 1)) * 2;  // G(m)
+        acca = fma(y1a, ha, acca);
+        accb = fma(y1b, hb, accb);
+        const double hna = 2.0 * ta[0] * ha - twoa * ham;
+        const double hnb = 2.0 * tb[0] * hb - twoa * hbm;
+        ham = ha;
+        ha = hna;
+        hbm = hb;
+        hb = hnb;
+        twoa += 2.0;
+    }
+    va = acca;
+    vb = accb;
 }
 
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)

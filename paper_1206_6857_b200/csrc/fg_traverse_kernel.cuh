@@ -1887,7 +1887,7 @@ traverse_kernel(const TravArgs A) {
             constexpr int PF = engine_order_c(D);
             constexpr int kRing = 4;
             // D = 3: items are staged in the nested layout of their own order
-            // (fg_series.cuh Nest3, 16-byte coefficient loads); other
+            // (fg_series.cuh, the row machine: 16-byte coefficient loads); other
             // dimensions keep the graded-lex prefix
             const int slot = D == 3 ? kNest3Slot : (A.K + D + 1) & ~1;
             const int coff = D == 3 ? kNest3Centre : A.K;  // the centre inside a slot
@@ -1939,7 +1939,8 @@ traverse_kernel(const TravArgs A) {
                             qb = fma(tb[d], tb[d], qb);
                         }
                         const double ga = fg_exp_fast(-qa, s_tab), gb = fg_exp_fast(-qb, s_tab);
-                        const double2 v = far3_eval2<PF>(p, ta, tb, (int)(buf - smem));
+                        double2 v;
+                        far3_rows_cl<PF>(p, ta, tb, buf, v.x, v.y);
                         // (no inf * 0 for absurdly distant centres)
                         pt_est[0] += ga == 0.0 ? 0.0 : v.x * ga;
                         pt_est[1] += gb == 0.0 ? 0.0 : v.y * gb;

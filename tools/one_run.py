@@ -34,10 +34,11 @@ def main():
         return
     rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
     qt = rt if wl.monochromatic else fg.build_tree(fg.PointStore(wl.queries), 25)
-    rt.refresh_moments(h, fg.default_plimit(wl.dim))
+    pl = fg.engine_plimit(wl.dim)
+    rt.refresh_moments(h, pl)
     run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[args.algo]
     for _ in range(args.reps):
-        res = run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon), qt, rt)
+        res = run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, plimit=pl), qt, rt)
     print(f"h={h:.5g} kernel {res.seconds*1e3:.3f} ms counters {res.counters}")
 
 

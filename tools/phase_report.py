@@ -29,12 +29,13 @@ def main():
     print("h ms | " + " ".join(f"{n:>9s}" for n in NAMES) + " | top-block share of kernel")
     for j in bws:
         h = wl.bandwidths[j]
-        rt.refresh_moments(h, fg.default_plimit(wl.dim))
+        pl = fg.engine_plimit(wl.dim)
+        rt.refresh_moments(h, pl)
         path = f"/tmp/phase_{os.getpid()}.bin"
         if os.path.exists(path):
             os.remove(path)
         os.environ["FG_DEBUG_BLOCKS"] = path
-        res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon), rt, rt)
+        res = fg.dito_run(fg.RunConfig(bandwidth=h, epsilon=wl.epsilon, plimit=pl), rt, rt)
         del os.environ["FG_DEBUG_BLOCKS"]
         a = np.fromfile(path, dtype=np.uint64).reshape(-1, 16).astype(float)
         os.remove(path)
