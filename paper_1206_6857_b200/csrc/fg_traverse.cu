@@ -902,9 +902,11 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
             double c = fp32 ? (3.0 * D + 8.0) / 6.0 : 2.0 * D + 20.0;
             if (const char *env = getenv("FG_PAIR_COST")) c = atof(env);  // experiment knob
             H.pair_cost = c;
-            // Hermite evaluation per query slot: c0 + c1 K_p
-            H.herm_c0 = 32.0 * D;
-            H.herm_c1 = D + 1.0;
+            // Hermite evaluation per query slot: c0 + c1 K_p.  D = 3 runs the row
+            // machine (fg_series.cuh: one FMA and half a shared-memory load per
+            // coefficient and slot; C5 scan: (40, 2) beats (96, 4) by 1.8 %)
+            H.herm_c0 = D == 3 ? 40.0 : 32.0 * D;
+            H.herm_c1 = D == 3 ? 2.0 : D + 1.0;
             if (const char *env = getenv("FG_HERM_C0")) H.herm_c0 = atof(env);  // experiment knobs
             if (const char *env = getenv("FG_HERM_C1")) H.herm_c1 = atof(env);
         }
