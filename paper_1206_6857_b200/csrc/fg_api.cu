@@ -251,8 +251,8 @@ const SeriesTables *series_tables(int dim, int order, int *status) {
     }
     if (dim < 1 || dim > kMaxUserDim || (dim > kMaxDim && order > 1) || order < 1 ||
         order > kMaxOrder || iset_count(dim, order) > kMaxK) {
-        set_error("series tables: (dim, order) outside the device limits (dim<=8, order<=8, "
-                  "C(dim+order-1, dim)<=256; dim<=16 at order 1)");
+        set_error("series tables: (dim, order) outside the device limits (dim<=8, order<=12, "
+                  "C(dim+order-1, dim)<=384; dim<=16 at order 1)");
         *status = FG_EUNSUPPORTED;
         return nullptr;
     }

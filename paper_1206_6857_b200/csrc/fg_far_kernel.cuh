@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
     const int wib = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * kFarWarps + wib;
     constexpr int kFix = (3 * D + 1) & ~1;
-    double *sq = smem + wib * (kFix + ((A.K + 1) & ~1));  // box lo, hi, centre
+    double *sq = smem + wib * (kFix + ((A.K_loc + 1) & ~1));  // box lo, hi, centre
     double *sqc = sq + 2 * D;
     double *loc = sq + kFix;
     const int cap = A.stack_cap;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
         if (lane < 2 * D) sq[lane] = A.q_box[(int64_t)snode * 2 * D + lane];
         if (lane < D) sqc[lane] = A.q_c[(int64_t)snode * D + lane];
         if (A.use_series)
-            for (int c = lane; c < A.K; c += 32) loc[c] = 0.0;
+            for (int c = lane; c < A.K_loc; c += 32) loc[c] = 0.0;
         __syncwarp();
         const double2 swr = A.q_wr[snode];  // (weight, inf_radius) of S
         const int s_cnt = A.q_ni[snode].y;
@@ -177,12 +177,12 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
                         possible *= pw;
                     }
                     if (possible <= maxerr) {
-                        select_method_gpu(bse, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
+                        select_method_gpu(bse, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit, A.plimit_loc,
                                           A.ct, A.cross, A.kp, (double)s_cnt / 32.0, H.pair_cost, H.herm_c0, H.herm_c1,
                                           meth, p, bound);
                         int p_h, p_l, p_t;
                         double e_h, e_l, e_t;
-                        feasible_orders(bse, r_ref, r_qu, maxerr, A.plimit, A.ct, A.cross, p_h,
+                        feasible_orders(bse, r_ref, r_qu, maxerr, A.plimit, A.plimit_loc, A.ct, A.cross, p_h,
                                         p_l, p_t, e_h, e_l, e_t);
                         dh_ok = p_h != 0;
                     }
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
                 const int meth = e.y >> 8, p = e.y & 0xff;
                 if (meth == 3) {
                     const int4 ni = A.r_ni[e.x];
-                    accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], H.sc,
+                    accumulate_warp<D, kLocK / 32>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], H.sc,
                                        A.digits, A.inv_fact, loc, false);
                 } else {
                     h2l_warp_add<D>(H.r_mom + (int64_t)e.x * A.mom_K, A.r_c + (int64_t)e.x * D, qc,
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kFarThreads) far_kernel(const TravArgs A) {
         }
         const double est = warp_sum(lane_est);
         if (!overflow && local_used)
-            for (int c = lane; c < A.K; c += 32) A.far_loc[t * A.K + c] = loc[c];
+            for (int c = lane; c < A.K_loc; c += 32) A.far_loc[t * A.K_loc + c] = loc[c];
         if (lane == 0) {
             A.far_flag[t] = overflow ? 0 : (1 | (local_used ? 2 : 0));
             A.far_tokens[t] = tokens;

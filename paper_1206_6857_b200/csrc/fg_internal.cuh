@@ -20,10 +20,14 @@ constexpr int kMaxUserDim = 16;
 inline int kernel_dim(int dim) { return dim <= 8 ? dim : dim <= 12 ? 12 : dim <= 16 ? 16 : -1; }
 constexpr int kDimSlots = 17;  // per-dimension caches indexed by kernel dimension
 #ifndef FG_MAX_ORDER
-#define FG_MAX_ORDER 10
+#define FG_MAX_ORDER 12
 #endif
 constexpr int kMaxOrder = FG_MAX_ORDER;   // series order cap on the device
-constexpr int kMaxK = 256;      // coefficient-count cap per expansion
+constexpr int kMaxK = 384;      // coefficient-count cap per expansion (K = 364 at D = 3, order 12)
+// local expansions (direct local, H2L, L2L) are held per warp in shared memory:
+// their order is capped lower (any feasible method keeps the error guarantee)
+constexpr int kLocOrder = 10;
+constexpr int kLocK = 256;
 constexpr double kSqrt2 = 1.4142135623730951;
 
 // the reference's series order cap per dimension (spatial_index.py:39-44)
@@ -38,7 +42,7 @@ __host__ __device__ constexpr int default_plimit_c(int D) {
 // (error_bounds.py:107-117) holds for any p.  Sweeps use it when the caller
 // leaves RunConfig.plimit unset.
 #ifndef FG_ORDER3
-#define FG_ORDER3 10
+#define FG_ORDER3 12
 #endif
 __host__ __device__ constexpr int engine_order_c(int D) {
     return D == 3 ? (FG_ORDER3 <= kMaxOrder ? FG_ORDER3 : kMaxOrder) : default_plimit_c(D);

@@ -230,10 +230,11 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     auto kern = kpl <= 1 ? mom_partial_kernel<D, 1>
                 : kpl <= 2 ? mom_partial_kernel<D, 2>
                 : kpl <= 4 ? mom_partial_kernel<D, 4>
+                : kpl <= 8 ? mom_partial_kernel<D, 8>
                            : mom_partial_kernel<D, kMomKPLMax>;
-    const int ki = kpl <= 1 ? 0 : kpl <= 2 ? 1 : kpl <= 4 ? 2 : 3;
+    const int ki = kpl <= 1 ? 0 : kpl <= 2 ? 1 : kpl <= 4 ? 2 : kpl <= 8 ? 3 : 4;
     struct MomGrid {
-        int g[kDimSlots][4] = {};
+        int g[kDimSlots][5] = {};
     };
     auto &c_grid = scratch<MomGrid, MomGrid>().g;  // per device
     if (!c_grid[D][ki]) {
@@ -373,7 +374,7 @@ struct RescaleFac;
 int moments_refresh(TreeDev &t, double h, int plimit) {
     FG_REQUIRE(h > 0.0 && std::isfinite(h), FG_EINVAL, "bandwidth must be positive");
     FG_REQUIRE(plimit >= 1, FG_EINVAL, "truncation order must be at least 1");
-    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (10) is not supported");
+    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (12) is not supported");
     int st = FG_OK;
     const SeriesTables *T = series_tables(t.dim, plimit, &st);
     FG_TRY(st);

@@ -291,7 +291,7 @@ int fg_series_translate(int32_t kind, const double *coeffs, int32_t k_stored,
 int fg_best_method(const double *geom, int32_t batch, int32_t dim, int32_t plimit, double *out) {
     FG_SERIES_SCRATCH;
     FG_REQUIRE(geom && out && batch >= 1 && dim >= 1 && plimit >= 1, FG_EINVAL, "bad args");
-    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (10) is not supported");
+    FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (12) is not supported");
     TailArgs T;
     double floor_c;
     tail_tables(dim, plimit, T.ct, T.cross, &floor_c);

@@ -158,7 +158,7 @@ __host__ __device__ constexpr int nest3_group(int m) {  // G(m): doubles of rows
 template <int PMAX>
 struct Nest3Perm {
     static constexpr int kTotal = (PMAX * (PMAX + 1) * (PMAX + 2) * (PMAX + 3)) / 24;  // sum of K_p
-    unsigned char pos[kTotal];
+    unsigned short pos[kTotal];
     int off[PMAX + 2];
     constexpr Nest3Perm() : pos{}, off{} {
         constexpr GLex<3, PMAX> G{};
@@ -171,15 +171,16 @@ struct Nest3Perm {
                 // groups in order of a; inside a group rows by ascending length
                 int st = nest3_group(p - a - b - 1);
                 for (int aa = 0; aa < a; aa++) st += nest3_group(p - aa);
-                pos[o + q] = (unsigned char)(st + c);
+                pos[o + q] = (unsigned short)(st + c);
             }
             o += G.prefix[p];
         }
         off[PMAX + 1] = o;
     }
 };
-constexpr int kNest3Slot = 256;    // doubles per staged item: nested coefficients, then the centre
-constexpr int kNest3Centre = 252;  // (the order-10 layout takes 250)
+// doubles per staged item (nested coefficients, then the centre in the last
+// four): the order-10 layout takes 250, the order-12 layout 406
+__host__ __device__ constexpr int nest3_slot(int plimit) { return plimit <= 10 ? 256 : 512; }
 
 // ---- EVALM at D = 3: the row machine ---------------------------------------
 // sum_{a+b+c<p} A_abc H_a(t0) H_b(t1) H_c(t2) e^{-|t|^2} for both query slots of
@@ -202,12 +203,16 @@ template <int N>
 __device__ __forceinline__ void far3_row_cl(const double *gs, const double (&l2a)[kMaxOrder],
                                             const double (&l2b)[kMaxOrder], double t1a,
                                             double t1b, double &twob, double &y1a, double &y2a,
-                                            double &y1b, double &y2b) {
+                                            double &y1b, double &y2b, double2 &pre) {
     const double2 *row = reinterpret_cast<const double2 *>(gs + nest3_group(N - 1));
+    // the row's first pair was loaded one block ahead (`pre`); load the next
+    // row's now (inside the staged slot even when this is the group's last row)
+    const double2 first = pre;
+    pre = *reinterpret_cast<const double2 *>(gs + nest3_group(N));
     double ea = 0.0, oa = 0.0, eb = 0.0, ob = 0.0;
 #pragma unroll
     for (int cc = 0; cc < N; cc += 2) {
-        const double2 v = row[cc >> 1];
+        const double2 v = cc == 0 ? first : row[cc >> 1];
         if (cc == 0) {
             ea = v.x;
             eb = v.x;
@@ -265,10 +270,11 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
     for (int m = p; m >= 1; m--) {
         double y1a = 0.0, y2a = 0.0, y1b = 0.0, y2b = 0.0;
         double twob = 2.0 * m;  // 2 (b + 1) of the row being folded
+        double2 pre = *reinterpret_cast<const double2 *>(gs);
         do {
 #define FG_ROWC(N)                                                                  \
     if constexpr (N <= PMAX) {                                                      \
-        far3_row_cl<N>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b);           \
+        far3_row_cl<N>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b, pre);      \
         if (m == N) break;                                                          \
     }
             FG_ROWC(1) FG_ROWC(2) FG_ROWC(3) FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7)
@@ -307,7 +313,7 @@ __device__ double eval_local_lane(const double (&x)[D], const double (&c)[D],
 // kind 0 = far-field moments A_a = sum_r w_r/a! ((x_r-c)/sc)^a (:76-92),
 // kind 1 = direct local B_b = sum_r w_r/b! h_b((x_r-c)/sc)       (:110-126).
 // Adds inv_fact-scaled sums into out[k] for k < Kp (out may alias shared mem).
-template <int D>
+template <int D, int KSLOTS = kMaxK / 32>
 __device__ void accumulate_warp(int kind, const double *__restrict__ pw_pts, int64_t r0,
                                 int64_t r1, const double (&c)[D], int p, int Kp, double sc,
                                 const uint8_t *__restrict__ digits,
@@ -315,10 +321,10 @@ __device__ void accumulate_warp(int kind, const double *__restrict__ pw_pts, int
                                 bool overwrite) {
     constexpr int S = packed_stride(D);
     const int lane = threadIdx.x & 31;
-    double acc[kMaxK / 32];
-    uint64_t dg[kMaxK / 32];
+    double acc[KSLOTS];
+    uint64_t dg[KSLOTS];
 #pragma unroll
-    for (int j = 0; j < kMaxK / 32; j++) {
+    for (int j = 0; j < KSLOTS; j++) {
         acc[j] = 0.0;
         int k = lane + 32 * j;
         dg[j] = k < Kp ? digits_of(digits, k) : 0;
@@ -334,12 +340,12 @@ __device__ void accumulate_warp(int kind, const double *__restrict__ pw_pts, int
             else hermite_ladder(u, p - 1, tab[d]);
         }
 #pragma unroll
-        for (int j = 0; j < kMaxK / 32; j++) {
+        for (int j = 0; j < KSLOTS; j++) {
             if (32 * j < Kp) acc[j] += w * product<D>(dg[j], tab);
         }
     }
 #pragma unroll
-    for (int j = 0; j < kMaxK / 32; j++) {
+    for (int j = 0; j < KSLOTS; j++) {
         int k = lane + 32 * j;
         if (k < Kp) {
             double v = acc[j] * __ldg(inv_fact + k);
@@ -416,7 +422,8 @@ __device__ void l2l_warp_add(const double *__restrict__ B, const double *__restr
 // error_bounds.py:196-225).  p == 0 marks an infeasible method.
 // base = an upper bound on W_R exp(-min_sq / 4h^2) (error_bounds.py:196).
 __device__ __forceinline__ void feasible_orders(double base, double r_ref, double r_query,
-                                                double maxerr, int plimit, const double *ct,
+                                                double maxerr, int plimit, int plimit_loc,
+                                                const double *ct,
                                                 const double *cross, int &p_h, int &p_l,
                                                 int &p_t, double &e_h, double &e_l,
                                                 double &e_t) {
@@ -435,11 +442,11 @@ __device__ __forceinline__ void feasible_orders(double base, double r_ref, doubl
             double err = base * c * x_r;
             if (err <= maxerr) { p_h = p; e_h = err; }
         }
-        if (!p_l) {
+        if (!p_l && p <= plimit_loc) {
             double err = base * c * x_q;
             if (err <= maxerr) { p_l = p; e_l = err; }
         }
-        if (!p_t) {
+        if (!p_t && p <= plimit_loc) {
             double step = sq > 1.0 ? x_sq : 1.0;
             double err = base * c * (x_q + x_sr * cross[p] * step);
             if (err <= maxerr) { p_t = p; e_t = err; }
@@ -466,15 +473,15 @@ __device__ __forceinline__ void feasible_orders(double base, double r_ref, doubl
 // W_R sqrt(K_hi) from its own K_hi = exp(-min_sq / 2h^2) (see there).
 __device__ __forceinline__ void select_method_gpu(double base, double r_ref, double r_query,
                                                   double n_ref, int dim, double maxerr,
-                                                  int plimit, const double *ct,
+                                                  int plimit, int plimit_loc, const double *ct,
                                                   const double *cross, const int *kp, double nq,
                                                   double pair_cost, double herm_c0,
                                                   double herm_c1, int &method, int &order,
                                                   double &bound) {
     int p_h, p_l, p_t;
     double e_h, e_l, e_t;
-    feasible_orders(base, r_ref, r_query, maxerr, plimit, ct, cross, p_h, p_l, p_t, e_h, e_l,
-                    e_t);
+    feasible_orders(base, r_ref, r_query, maxerr, plimit, plimit_loc, ct, cross, p_h, p_l, p_t,
+                    e_h, e_l, e_t);
     const double d = (double)dim;
     double c_h = CUDART_INF, c_l = CUDART_INF, c_t = CUDART_INF;
     if (p_h) c_h = nq * (herm_c0 + kp[p_h] * herm_c1);

@@ -680,7 +680,7 @@ struct FarScratch {
 template <int D>
 static int launch_far_t(TravArgs &A, int64_t ntask) {
     auto kern = far_kernel<D>;
-    const size_t smem = sizeof(double) * (((3 * D + 1) & ~1) + ((A.K + 1) & ~1)) * kFarWarps;
+    const size_t smem = sizeof(double) * (((3 * D + 1) & ~1) + ((A.K_loc + 1) & ~1)) * kFarWarps;
     int dev = 0, sms = 0, occ = 0;
     FG_CUDA_TRY(cudaGetDevice(&dev));
     FG_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -719,7 +719,7 @@ static int queue_far(TreeDev &q, TravArgs &A) {
     FG_TRY(F.est.reserve(sizeof(double) * ntask));
     FG_TRY(F.rcnt.reserve(sizeof(int) * ntask));
     FG_TRY(F.res.reserve(sizeof(int) * ntask * kFarResCap));
-    FG_TRY(F.loc.reserve(sizeof(double) * ntask * std::max(A.K, 1)));
+    FG_TRY(F.loc.reserve(sizeof(double) * ntask * std::max(A.K_loc, 1)));
     A.q_ni = q.node_i.as<int4>();
     A.q_box = q.node_box.as<double>();
     A.q_c = q.node_c.as<double>();
@@ -852,6 +852,10 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
             A.kp[p] = T->h_prefix[p];
         }
         A.floor_c = floor_c;
+        // local expansions live in shared memory per warp: capped order
+        A.plimit_loc = std::min(plimit, kLocOrder);
+        while (A.plimit_loc > 1 && T->h_prefix[A.plimit_loc] > kLocK) A.plimit_loc--;
+        A.K_loc = T->h_prefix[A.plimit_loc];
     }
     // per warp: query box + centroid + local coefficients, 2 x 32 staged FP64
     // points, the FP32 batch
@@ -863,7 +867,7 @@ static int queue_traversal(TreeDev &q, TreeDev &r, int nh, const double *hs,
                                     warp_fixed_doubles<5>(), warp_fixed_doubles<6>(),
                                     warp_fixed_doubles<7>(), warp_fixed_doubles<8>(), 0, 0, 0,
                                     warp_fixed_doubles<12>(), 0, 0, 0, warp_fixed_doubles<16>()};
-        smem = sizeof(double) * (fixd[D] + ((A.K + 1) & ~1)) *kTravWarps;
+        smem = sizeof(double) * (fixd[D] + ((A.K_loc + 1) & ~1)) *kTravWarps;
     }
     TravScratch &g_scr = trav_scratch();
     FG_TRY(g_scr.work.reserve(sizeof(unsigned long long)));
@@ -1003,7 +1007,7 @@ int run_traversal(TreeDev &q, TreeDev &r, double h, double eps, int mode, int pl
     const int D = q.dim;
     if (plimit <= 0) plimit = default_plimit(D);
     if (mode == FG_DITO) {
-        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (10) is not supported");
+        FG_REQUIRE(plimit <= kMaxOrder, FG_EUNSUPPORTED, "plimit above the device order cap (12) is not supported");
         FG_REQUIRE(r.mom_valid && r.mom_h == h && r.mom_order >= plimit, FG_ESTALE,
                    "reference moments missing or stale; call refresh_moments for this "
                    "bandwidth first");

@@ -98,6 +98,7 @@ struct TravArgs {
     int use_tokens, use_series, plimit, K;
     double ct[kMaxOrder + 1], cross[kMaxOrder + 1];
     int kp[kMaxOrder + 1];  // coefficient count for order p
+    int plimit_loc, K_loc;  // order cap and coefficient count of the local expansions
     const uint8_t *digits;
     const double *inv_fact;
     const int *degrees;
@@ -1195,7 +1196,7 @@ traverse_kernel(const TravArgs A) {
     extern __shared__ double smem[];
     __shared__ double s_tab[kExpTab];
     // staging permutation of the D = 3 Hermite items (graded-lex -> nested)
-    __shared__ unsigned char s_nest[D == 3 ? ((Nest3Perm<engine_order_c(3)>::kTotal + 15) & ~15) : 16];
+    __shared__ unsigned short s_nest[D == 3 ? ((Nest3Perm<engine_order_c(3)>::kTotal + 7) & ~7) : 8];
     exp_table_init(s_tab);
     if constexpr (D == 3)
         for (int i = threadIdx.x; i < Nest3Perm<engine_order_c(3)>::kTotal; i += blockDim.x)
@@ -1209,7 +1210,7 @@ traverse_kernel(const TravArgs A) {
     // batch (transposed records and per-group offsets)
     // (fixed-size parts first: every pointer below is sq + a compile-time
     // offset, so the kernel keeps one shared-memory base register)
-    double *sq = smem + wib * (warp_fixed_doubles<D>() + ((A.K + 1) & ~1));
+    double *sq = smem + wib * (warp_fixed_doubles<D>() + ((A.K_loc + 1) & ~1));
     double *sqc = sq + 2 * D;
     double *sbuf = sq + ((3 * D + 1) & ~1);
     float *fst = reinterpret_cast<float *>(sbuf + stage_recs<D>() * S);
@@ -1270,7 +1271,7 @@ traverse_kernel(const TravArgs A) {
         if (lane < 2 * D) sq[lane] = A.qb_box[b * 2 * D + lane];
         if (lane < D) sqc[lane] = A.qb_c[b * D + lane];
         if (A.use_series)
-            for (int k = lane; k < A.K; k += 32) loc[k] = 0.0;
+            for (int k = lane; k < A.K_loc; k += 32) loc[k] = 0.0;
         __syncwarp();
         double xr[xs_smem<D>() ? 1 : kQPL][D];  // query coordinates in registers (D >= 5)
 #pragma unroll
@@ -1455,7 +1456,7 @@ traverse_kernel(const TravArgs A) {
                     }
                     if (possible <= maxerr)
                         select_method_gpu(base, r_ref, r_qu, (double)ni.y, D, maxerr, A.plimit,
-                                          A.ct, A.cross, A.kp, (double)nq, H.pair_cost, H.herm_c0, H.herm_c1, meth, p,
+                                          A.plimit_loc, A.ct, A.cross, A.kp, (double)nq, H.pair_cost, H.herm_c0, H.herm_c1, meth, p,
                                           bound);
                 }
                 const bool cand = meth != 0;
@@ -1869,9 +1870,9 @@ traverse_kernel(const TravArgs A) {
         if (far & 2) {
             // S.local pushed down to this block's centre (translate_l2l,
             // series_expansion.py:197-217), the block's own local terms added below
-            l2l_warp_add<D>(A.far_loc + ft * A.K,
+            l2l_warp_add<D>(A.far_loc + ft * A.K_loc,
                             A.q_c + (int64_t)__ldg(A.sn_node + __ldg(A.qb_super + b)) * D, sqc,
-                            A.plimit, A.K, H.sc, A.digits, loc);
+                            A.plimit_loc, A.K_loc, H.sc, A.digits, loc);
             __syncwarp();
             local_used = true;
         }
@@ -1885,12 +1886,13 @@ traverse_kernel(const TravArgs A) {
             // through a cp.async ring in the (now idle) FP64 staging buffer,
             // kRing - 1 items ahead of the one being evaluated
             constexpr int PF = engine_order_c(D);
-            constexpr int kRing = 4;
             // D = 3: items are staged in the nested layout of their own order
             // (fg_series.cuh, the row machine: 16-byte coefficient loads); other
             // dimensions keep the graded-lex prefix
-            const int slot = D == 3 ? kNest3Slot : (A.K + D + 1) & ~1;
-            const int coff = D == 3 ? kNest3Centre : A.K;  // the centre inside a slot
+            const int slot = D == 3 ? nest3_slot(A.plimit) : (A.K + D + 1) & ~1;
+            const int coff = D == 3 ? slot - 4 : A.K;  // the centre inside a slot
+            // ring depth: 4 items, 2 for the 512-double slots of orders 11, 12
+            const int kRing = D == 3 && slot > 256 ? 2 : 4;
             // the ring may run over the FP32 record area behind the FP64 staging
             // buffer (contiguous at D <= 4, idle after the traversal loop)
             constexpr int kRingDoubles =
@@ -1899,10 +1901,10 @@ traverse_kernel(const TravArgs A) {
             auto stage_item = [&](int k) {
                 const int2 e = sl[k];
                 const int node = e.x, po = e.y & 0xff, kc = A.kp[po];  // the item's own order
-                double *dst = sbuf + (k % kRing) * slot;
+                double *dst = sbuf + (k & (kRing - 1)) * slot;
                 const double *mom = H.r_mom + (int64_t)node * A.mom_K;
                 if constexpr (D == 3) {
-                    const unsigned char *perm = s_nest + c_nest3.off[po];
+                    const unsigned short *perm = s_nest + c_nest3.off[po];
                     for (int q = lane; q < kc; q += 32)
                         __pipeline_memcpy_async(dst + perm[q], mom + q, 8);
                 } else {
@@ -1923,16 +1925,17 @@ traverse_kernel(const TravArgs A) {
                 if (ring) {
                     if (i + kRing - 1 < nh) stage_item(i + kRing - 1);
                     __pipeline_commit();
-                    __pipeline_wait_prior(kRing - 1);
+                    if (kRing == 4) __pipeline_wait_prior(3);
+                    else __pipeline_wait_prior(1);
                     __syncwarp();
-                    const double *buf = sbuf + (i % kRing) * slot;
+                    const double *buf = sbuf + (i & (kRing - 1)) * slot;
                     if constexpr (D == 3) {
                         // the item's own order, both query slots from one pass
                         // over the coefficients (an unused slot holds the centroid)
                         double ta[3], tb[3], qa = 0.0, qb = 0.0;
 #pragma unroll
                         for (int d = 0; d < 3; d++) {
-                            const double c = buf[kNest3Centre + d];
+                            const double c = buf[coff + d];
                             ta[d] = (x[0][d] - c) * H.inv_sc;
                             tb[d] = (x[1][d] - c) * H.inv_sc;
                             qa = fma(ta[d], ta[d], qa);
@@ -1976,7 +1979,7 @@ traverse_kernel(const TravArgs A) {
                 const int meth = e.y >> 8, p = e.y & 0xff;
                 if (meth == 3) {
                     const int4 ni = A.r_ni[e.x];
-                    accumulate_warp<D>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], H.sc,
+                    accumulate_warp<D, kLocK / 32>(1, A.r_pw, ni.x, (int64_t)ni.x + ni.y, qc, p, A.kp[p], H.sc,
                                        A.digits, A.inv_fact, loc, false);
                     c_dl++;
                 } else {
@@ -1994,7 +1997,7 @@ traverse_kernel(const TravArgs A) {
                 for (int qi = 0; qi < nq; qi++) {
                     double xq[D];
                     pick_query<D>(x, qi, xq);
-                    add_slot(pt_est, qi, eval_local_lane<D>(xq, qc, loc, A.plimit, A.K, H.sc, A.digits));
+                    add_slot(pt_est, qi, eval_local_lane<D>(xq, qc, loc, A.plimit_loc, A.K_loc, H.sc, A.digits));
                 }
             }
         }
