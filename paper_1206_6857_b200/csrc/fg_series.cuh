@@ -296,6 +296,19 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
     vb = accb;
 }
 
+// out-of-line instance (the ladders then do not weigh on the caller's registers);
+// the item is addressed through the dynamic shared-memory window so that its
+// loads stay shared-memory loads across the call
+template <int PMAX>
+__device__ __noinline__ double2 far3_rows_cl_call(int p, double a0, double a1, double a2,
+                                                  double b0, double b1, double b2, int off) {
+    extern __shared__ double fg_dyn_smem[];
+    const double ta[3] = {a0, a1, a2}, tb[3] = {b0, b1, b2};
+    double2 r;
+    far3_rows_cl<PMAX>(p, ta, tb, fg_dyn_smem + off, r.x, r.y);
+    return r;
+}
+
 // EVALL: sum_{k<K} B_k prod_d ((x_d - c_d)/sc)^{b_d} (series_expansion.py:129-136)
 template <int D>
 __device__ double eval_local_lane(const double (&x)[D], const double (&c)[D],

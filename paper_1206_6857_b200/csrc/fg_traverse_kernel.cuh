@@ -1943,7 +1943,14 @@ traverse_kernel(const TravArgs A) {
                         }
                         const double ga = fg_exp_fast(-qa, s_tab), gb = fg_exp_fast(-qb, s_tab);
                         double2 v;
-                        far3_rows_cl<PF>(p, ta, tb, buf, v.x, v.y);
+#ifndef FG_FAR3_CALL
+#define FG_FAR3_CALL 1
+#endif
+                        if constexpr (FG_FAR3_CALL)
+                            v = far3_rows_cl_call<PF>(p, ta[0], ta[1], ta[2], tb[0], tb[1], tb[2],
+                                                      (int)(buf - smem));
+                        else
+                            far3_rows_cl<PF>(p, ta, tb, buf, v.x, v.y);
                         // (no inf * 0 for absurdly distant centres)
                         pt_est[0] += ga == 0.0 ? 0.0 : v.x * ga;
                         pt_est[1] += gb == 0.0 ? 0.0 : v.y * gb;
