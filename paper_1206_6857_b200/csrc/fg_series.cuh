@@ -199,34 +199,39 @@ __host__ __device__ constexpr int nest3_slot(int plimit) { return plimit <= 10 ?
 // block_m.  Sum_b S_b H_b(t1) is folded by Clenshaw's recurrence
 // y_b = S_b + 2 t1 y_{b+1} - 2 (b + 1) y_{b+2} (result y_0): two FMAs per row
 // and slot and no middle ladder; H_a(t0) is advanced once per group.
-template <int N>
+constexpr int kRowPairs = (kMaxOrder + 1) / 2;  // 16-byte pairs of the longest row
+template <int N, int PMAX>
 __device__ __forceinline__ void far3_row_cl(const double *gs, const double (&l2a)[kMaxOrder],
                                             const double (&l2b)[kMaxOrder], double t1a,
                                             double t1b, double &twob, double &y1a, double &y2a,
-                                            double &y1b, double &y2b, double2 &pre) {
-    const double2 *row = reinterpret_cast<const double2 *>(gs + nest3_group(N - 1));
-    // the row's first pair was loaded one block ahead (`pre`); load the next
+                                            double &y1b, double &y2b, double2 (&pre)[kRowPairs]) {
+    // this row's coefficients were loaded one block ahead (`pre`); load the next
     // row's now (inside the staged slot even when this is the group's last row)
-    const double2 first = pre;
-    pre = *reinterpret_cast<const double2 *>(gs + nest3_group(N));
+    constexpr int NP = (N + 1) / 2, NPN = N < PMAX ? (N + 2) / 2 : 0;
+    double2 v[NP];
+#pragma unroll
+    for (int k = 0; k < NP; k++) v[k] = pre[k];
+    const double2 *next = reinterpret_cast<const double2 *>(gs + nest3_group(N));
+#pragma unroll
+    for (int k = 0; k < NPN; k++) pre[k] = next[k];
     double ea = 0.0, oa = 0.0, eb = 0.0, ob = 0.0;
 #pragma unroll
     for (int cc = 0; cc < N; cc += 2) {
-        const double2 v = cc == 0 ? first : row[cc >> 1];
+        const double2 w = v[cc >> 1];
         if (cc == 0) {
-            ea = v.x;
-            eb = v.x;
+            ea = w.x;
+            eb = w.x;
         } else {
-            ea = fma(v.x, l2a[cc], ea);
-            eb = fma(v.x, l2b[cc], eb);
+            ea = fma(w.x, l2a[cc], ea);
+            eb = fma(w.x, l2b[cc], eb);
         }
         if (cc + 1 < N) {
             if (N >= 6) {  // two partial sums per slot on long rows
-                oa = cc == 0 ? v.y * l2a[1] : fma(v.y, l2a[cc + 1], oa);
-                ob = cc == 0 ? v.y * l2b[1] : fma(v.y, l2b[cc + 1], ob);
+                oa = cc == 0 ? w.y * l2a[1] : fma(w.y, l2a[cc + 1], oa);
+                ob = cc == 0 ? w.y * l2b[1] : fma(w.y, l2b[cc + 1], ob);
             } else {
-                ea = fma(v.y, l2a[cc + 1], ea);
-                eb = fma(v.y, l2b[cc + 1], eb);
+                ea = fma(w.y, l2a[cc + 1], ea);
+                eb = fma(w.y, l2b[cc + 1], eb);
             }
         }
     }
@@ -270,11 +275,12 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
     for (int m = p; m >= 1; m--) {
         double y1a = 0.0, y2a = 0.0, y1b = 0.0, y2b = 0.0;
         double twob = 2.0 * m;  // 2 (b + 1) of the row being folded
-        double2 pre = *reinterpret_cast<const double2 *>(gs);
+        double2 pre[kRowPairs];
+        pre[0] = *reinterpret_cast<const double2 *>(gs);
         do {
 #define FG_ROWC(N)                                                                  \
     if constexpr (N <= PMAX) {                                                      \
-        far3_row_cl<N>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b, pre);      \
+        far3_row_cl<N, PMAX>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b, pre); \
         if (m == N) break;                                                          \
     }
             FG_ROWC(1) FG_ROWC(2) FG_ROWC(3) FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7)

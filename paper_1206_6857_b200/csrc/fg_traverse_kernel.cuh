@@ -413,6 +413,10 @@ constexpr int fstride() { return (D + 1 + 3) & ~3; }
 #ifndef FG_PAIR_DIFF
 #define FG_PAIR_DIFF 1
 #endif
+// per-item A = fl(-s |X|^2) and the fold of an item's partial sums in FP32
+#ifndef FG_PAIR_F32_PROLOGUE
+#define FG_PAIR_F32_PROLOGUE 1
+#endif
 // floats per record pair: {Y_d a/b} x D, {B a/b}, {W a/b}, padded to 16 bytes
 template <int D>
 constexpr int pstride() { return (2 * (D + 2) + 3) & ~3; }
@@ -750,7 +754,7 @@ __device__ __forceinline__ double fp32_pair_bound(const TravArgs &A, const doubl
     }
     const double c1 = 0x1.0p-21 * sqrt((double)D) * M * inv_h * 0.7071067811865476;
     const double rs = (sqrt(rq2) + sqrt(rr2)) * (1.0 + 0x1.0p-20) * inv_h;
-    const double e = (D + 4.0) * 0x1.0p-24 * 0.5 * rs * rs * 1.01;
+    const double e = (D + 4.0 + (FG_PAIR_F32_PROLOGUE ? D : 0)) * 0x1.0p-24 * 0.5 * rs * rs * 1.01;
     const double room = 0.5 * rho_max - 0x1.0p-17 - e;
     abs_err = CUDART_INF;
     if (!(room > 0.0)) return CUDART_INF;
@@ -842,6 +846,20 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
         unsigned long long xx[kQPL][D], aa[kQPL];
 #pragma unroll
         for (int q = 0; q < kQPL; q++) {
+#if FG_PAIR_F32_PROLOGUE
+            // A = fl(-s |X|^2) in FP32: D + 1 roundings instead of one (the D
+            // extra are covered by fp32_pair_bound's E, see there); no FP64 <->
+            // FP32 conversions (they share the SFU with ex2) per item
+            float a = 0.f;
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const float X = xs[q][d] - idl[it * FD + d];
+                const float Xp = s2f * X;
+                xx[q][d] = f2_pack(Xp, Xp);
+                a = fmaf(X, X, a);
+            }
+            const float av = -sf * a;
+#else
             double a = 0.0;
 #pragma unroll
             for (int d = 0; d < D; d++) {
@@ -851,6 +869,7 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
                 a = fma((double)X, (double)X, a);
             }
             const float av = (float)(-s * a);
+#endif
             aa[q] = f2_pack(av, av);
         }
         const unsigned long long *rec = reinterpret_cast<const unsigned long long *>(pbuf + off * P);
@@ -922,10 +941,19 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
                 f2_fma_acc(acc[q][0], f2_ex2(t), r[D + 1]);
             }
         }
+#if FG_PAIR_F32_PROLOGUE
+        // the four partial sums of a slot are added in FP32 (two more roundings
+        // on accumulators of <= 32 terms each: inside the bounds' 2^-17 reserve)
+        sum0 += (double)((f2_lo(acc[0][0]) + f2_hi(acc[0][0])) +
+                         (f2_lo(acc[0][1]) + f2_hi(acc[0][1])));
+        sum1 += (double)((f2_lo(acc[1][0]) + f2_hi(acc[1][0])) +
+                         (f2_lo(acc[1][1]) + f2_hi(acc[1][1])));
+#else
         sum0 += ((double)f2_lo(acc[0][0]) + (double)f2_hi(acc[0][0])) +
                 ((double)f2_lo(acc[0][1]) + (double)f2_hi(acc[0][1]));
         sum1 += ((double)f2_lo(acc[1][0]) + (double)f2_hi(acc[1][0])) +
                 ((double)f2_lo(acc[1][1]) + (double)f2_hi(acc[1][1]));
+#endif
     }
 }
 

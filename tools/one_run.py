@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--naive", action="store_true")
     ap.add_argument("--ref-leaf", type=int, default=0)
+    ap.add_argument("--plimit", type=int, default=0, help="series order cap (default: the engine's)")
     args = ap.parse_args()
     import paper_1206_6857_b200 as fg
     from paper_1206_6857_b200.configs import config
@@ -34,7 +35,7 @@ def main():
         return
     rt = fg.build_tree(fg.PointStore(wl.references, wl.weights), 25)
     qt = rt if wl.monochromatic else fg.build_tree(fg.PointStore(wl.queries), 25)
-    pl = fg.engine_plimit(wl.dim)
+    pl = args.plimit or fg.engine_plimit(wl.dim)
     rt.refresh_moments(h, pl)
     run = {"dfd": fg.dfd_run, "dfdo": fg.dfdo_run, "dito": fg.dito_run}[args.algo]
     for _ in range(args.reps):
