@@ -200,20 +200,26 @@ __host__ __device__ constexpr int nest3_slot(int plimit) { return plimit <= 10 ?
 // y_b = S_b + 2 t1 y_{b+1} - 2 (b + 1) y_{b+2} (result y_0): two FMAs per row
 // and slot and no middle ladder; H_a(t0) is advanced once per group.
 constexpr int kRowPairs = (kMaxOrder + 1) / 2;  // 16-byte pairs of the longest row
+// 16-byte shared-memory load that stays where it is written (the compiler sinks
+// an ordinary load down to its first use, which undoes the row prefetch)
+__device__ __forceinline__ double2 lds_pair(unsigned addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
 template <int N, int PMAX>
-__device__ __forceinline__ void far3_row_cl(const double *gs, const double (&l2a)[kMaxOrder],
+__device__ __forceinline__ void far3_row_cl(unsigned gs, const double (&l2a)[kMaxOrder],
                                             const double (&l2b)[kMaxOrder], double t1a,
                                             double t1b, double &twob, double &y1a, double &y2a,
-                                            double &y1b, double &y2b, double2 (&pre)[kRowPairs]) {
-    // this row's coefficients were loaded one block ahead (`pre`); load the next
-    // row's now (inside the staged slot even when this is the group's last row)
-    constexpr int NP = (N + 1) / 2, NPN = N < PMAX ? (N + 2) / 2 : 0;
-    double2 v[NP];
+                                            double &y1b, double &y2b,
+                                            const double2 (&v)[kRowPairs],
+                                            double2 (&pre)[kRowPairs]) {
+    // this row's coefficients were loaded one block ahead (`v`); load the next
+    // row's now into the other register set (inside the staged slot even when
+    // this is the group's last row)
+    constexpr int NPN = N < PMAX ? (N + 2) / 2 : 0;
 #pragma unroll
-    for (int k = 0; k < NP; k++) v[k] = pre[k];
-    const double2 *next = reinterpret_cast<const double2 *>(gs + nest3_group(N));
-#pragma unroll
-    for (int k = 0; k < NPN; k++) pre[k] = next[k];
+    for (int k = 0; k < NPN; k++) pre[k] = lds_pair(gs + 8 * nest3_group(N) + 16 * k);
     double ea = 0.0, oa = 0.0, eb = 0.0, ob = 0.0;
 #pragma unroll
     for (int cc = 0; cc < N; cc += 2) {
@@ -270,24 +276,25 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
     }
     const double t1a = 2.0 * ta[1], t1b = 2.0 * tb[1];
     double acca = 0.0, ha = 1.0, ham = 0.0, accb = 0.0, hb = 1.0, hbm = 0.0, twoa = 0.0;
-    const double *gs = A;
+    unsigned gs = (unsigned)__cvta_generic_to_shared(A);  // group start (byte address)
 #pragma unroll 1
     for (int m = p; m >= 1; m--) {
         double y1a = 0.0, y2a = 0.0, y1b = 0.0, y2b = 0.0;
         double twob = 2.0 * m;  // 2 (b + 1) of the row being folded
-        double2 pre[kRowPairs];
-        pre[0] = *reinterpret_cast<const double2 *>(gs);
+        double2 pre0[kRowPairs], pre1[kRowPairs];  // rows of odd / even length
+        pre0[0] = lds_pair(gs);
         do {
 #define FG_ROWC(N)                                                                  \
     if constexpr (N <= PMAX) {                                                      \
-        far3_row_cl<N, PMAX>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b, pre); \
+        far3_row_cl<N, PMAX>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b,       \
+                             (N & 1) ? pre0 : pre1, (N & 1) ? pre1 : pre0);          \
         if (m == N) break;                                                          \
     }
             FG_ROWC(1) FG_ROWC(2) FG_ROWC(3) FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7)
             FG_ROWC(8) FG_ROWC(9) FG_ROWC(10) FG_ROWC(11) FG_ROWC(12)
 #undef FG_ROWC
         } while (0);
-        gs += ((m + 1) >> 1) * (((m + 1) >> 1) + ((m & 1) ? 0 : 1)) * 2;  // G(m)
+        gs += ((m + 1) >> 1) * (((m + 1) >> 1) + ((m & 1) ? 0 : 1)) * 16;  // G(m) doubles
         acca = fma(y1a, ha, acca);
         accb = fma(y1b, hb, accb);
         const double hna = 2.0 * ta[0] * ha - twoa * ham;
