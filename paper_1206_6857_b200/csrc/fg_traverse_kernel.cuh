@@ -1933,8 +1933,10 @@ traverse_kernel(const TravArgs A) {
                 const double *mom = H.r_mom + (int64_t)node * A.mom_K;
                 if constexpr (D == 3) {
                     const unsigned short *perm = s_nest + c_nest3.off[po];
-                    for (int q = lane; q < kc; q += 32)
+                    for (int q = lane; q < kc; q += 32) {
+                        FG_CHECK(po >= 1 && po <= PF && perm[q] < coff && kc <= A.mom_K);
                         __pipeline_memcpy_async(dst + perm[q], mom + q, 8);
+                    }
                 } else {
                     for (int q = lane; q < kc; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
                 }
