@@ -68,7 +68,7 @@ static int ref_leaf_for(const TreeDev &q, double h) {
     // single-run scans per bandwidth with the Jensen bound and run-based query
     // blocks (C3, C4, C5; r_b = median block inf-radius): small items where
     // pruning still bites, bigger ones where nearly every pair is exact
-    // anchored FP32 items: <= kAnchorMax (256) points; 256-point items above
+    // anchored FP32 items: <= kAnchorMax (336) points; 256-point items above
     // r_b measured C5 -2.3 % against 128 (and 128 between r_b and 1.5 r_b: no
     // gain), C2 neutral
     if (q.dim <= 4) {

@@ -30,9 +30,10 @@ constexpr int kTravThreads = 128;
 constexpr int kQPL = 2;
 constexpr int kQBlock = 32 * kQPL;
 // largest anchored FP32 base item (and anchor) in points (D <= 4): with the
-// Jensen mass bound 128-point items beat 64 (C2 sweep -4.7 %)
+// Jensen mass bound 128-point items beat 64 (C2 sweep -4.7 %); 336 = what the
+// pair staging holds (C5 -0.7 %, C2 -1 % against 256)
 #ifndef FG_ANCHOR_MAX
-#define FG_ANCHOR_MAX 256
+#define FG_ANCHOR_MAX 336
 #endif
 constexpr int kAnchorMax = FG_ANCHOR_MAX;
 // FP64 base items up to kStageMax points are staged in shared memory (two
@@ -729,7 +730,9 @@ __device__ __forceinline__ void batch_f32(const unsigned long long (&xf2)[D], co
 // the largest 2-norm offsets of the query box and of the item's node box from
 // c_a (inflated for the coordinate roundings).  rho = 2 (C1 sqrt(a_c) + E +
 // 2^-17), cut at a_c as in fp32_item_bound; the per-item FP32 sums are folded
-// into FP64 after each item, so no FP32 accumulator adds more than 32 terms.
+// into FP64 after each item, so no FP32 accumulator adds more than 84 terms
+// (336-point items: 168 pairs over two accumulator pairs; with ex2, weight and
+// FMA roundings <= 91 u of the 128 u = 2^-17 the bound reserves).
 template <int D>
 __device__ __forceinline__ double fp32_pair_bound(const TravArgs &A, const double *sq, int anc,
                                                   int node, double inv_h, double klo, double wr,
@@ -943,7 +946,7 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
         }
 #if FG_PAIR_F32_PROLOGUE
         // the four partial sums of a slot are added in FP32 (two more roundings
-        // on accumulators of <= 32 terms each: inside the bounds' 2^-17 reserve)
+        // on accumulators of <= 84 terms each: inside the bounds' 2^-17 reserve)
         sum0 += (double)((f2_lo(acc[0][0]) + f2_hi(acc[0][0])) +
                          (f2_lo(acc[0][1]) + f2_hi(acc[0][1])));
         sum1 += (double)((f2_lo(acc[1][0]) + f2_hi(acc[1][0])) +
