@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(32 * kMomWarps)
 mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__restrict__ node_i,
                    const double *__restrict__ node_c, const double *__restrict__ pw, int p,
                    int K, double sc, const uint8_t *__restrict__ digits,
-                   double *__restrict__ partial) {
+                   double *__restrict__ partial, int small_only) {
     constexpr int S = packed_stride(D);
     extern __shared__ double sh[];  // per warp: 32 points x D x p powers (weight folded in d=0)
     const int lane = threadIdx.x & 31;
@@ -90,6 +90,9 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
     for (int it = blockIdx.x * kMomWarps + (threadIdx.x >> 5); it < nitems; it += gwarps) {
         const int2 item = items[it];
         const int4 ni = node_i[item.x];
+        // nodes of more than one chunk get their moments from their children
+        // (mom_h2h_level_kernel) when small_only is set
+        if (small_only && ni.y > kMomChunk) continue;
         double c[D];
 #pragma unroll
         for (int d = 0; d < D; d++) c[d] = node_c[(int64_t)item.x * D + d];
@@ -162,11 +165,12 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
 // the 8 warp sums are added in warp order (deterministic).
 __global__ void __launch_bounds__(256)
 mom_combine_kernel(const int *__restrict__ off, const double *__restrict__ partial, int K,
-                   const double *__restrict__ inv_fact, double *__restrict__ mom) {
+                   const double *__restrict__ inv_fact, double *__restrict__ mom, int small_only) {
     __shared__ double sh[8][kMaxK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t v = blockIdx.x;
     const int i0 = off[v], i1 = off[v + 1];
+    if (small_only && i1 - i0 > 1) return;  // (more than one chunk: from the children)
     if (i1 - i0 == 1) {  // single chunk: copy
         for (int k = threadIdx.x; k < K; k += 256)
             mom[v * K + k] = partial[(int64_t)i0 * K + k] * inv_fact[k];
@@ -184,6 +188,70 @@ mom_combine_kernel(const int *__restrict__ off, const double *__restrict__ parti
 #pragma unroll
         for (int w = 1; w < 8; w++) s += sh[w][k];
         mom[v * K + k] = s * inv_fact[k];
+    }
+}
+
+// Moments of the nodes of one tree level that span more than one chunk, from
+// their children's by H2H (series_expansion.py:139-164, the reference's own
+// upward pass): A'_s = sum over pairs (a, b) -> s of A_a u^b / b!,
+// u = (c_child - c_node) / sc.  One warp per node; lanes own destination
+// coefficients, the pairs come sorted by s (SeriesTables::h2h_ab), the sums run
+// in a fixed order (deterministic).
+template <int D>
+__global__ void __launch_bounds__(128)
+mom_h2h_level_kernel(int v0, int v1, const int4 *__restrict__ node_i,
+                     const double *__restrict__ node_c, int p, int K, double sc,
+                     const uint8_t *__restrict__ digits, const double *__restrict__ inv_fact,
+                     const int *__restrict__ off, const int2 *__restrict__ pr,
+                     double *__restrict__ mom) {
+    extern __shared__ double tab[];  // K shift terms u^b / b!
+    const int v = v0 + blockIdx.x;   // one CTA per node: threads own destination coefficients
+    if (v >= v1) return;
+    const int4 ni = node_i[v];
+    if (ni.y <= kMomChunk || ni.z < 0) return;  // accumulated directly (uniform per CTA)
+    constexpr int KPT = (kMaxK + 127) / 128;
+    double acc[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; j++) acc[j] = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < 2; c++) {
+        const int ch = c == 0 ? ni.z : ni.w;
+        double pwt[D][kMaxOrder];
+#pragma unroll
+        for (int d = 0; d < D; d++)
+            power_ladder((node_c[(int64_t)ch * D + d] - node_c[(int64_t)v * D + d]) / sc, p - 1,
+                         pwt[d]);
+        __syncthreads();
+        for (int k = threadIdx.x; k < K; k += 128)
+            tab[k] = product<D>(digits_of(digits, k), pwt) * inv_fact[k];
+        __syncthreads();
+        const double *A = mom + (int64_t)ch * K;
+#pragma unroll
+        for (int j = 0; j < KPT; j++) {
+            const int t = threadIdx.x + 128 * j;
+            if (t < K) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // fixed order: deterministic
+                const int q1 = off[t + 1];
+                int q = off[t];
+                for (; q + 4 <= q1; q += 4) {
+                    const int2 e0 = pr[q], e1 = pr[q + 1], e2 = pr[q + 2], e3 = pr[q + 3];
+                    a0 = fma(A[e0.x], tab[e0.y], a0);
+                    a1 = fma(A[e1.x], tab[e1.y], a1);
+                    a2 = fma(A[e2.x], tab[e2.y], a2);
+                    a3 = fma(A[e3.x], tab[e3.y], a3);
+                }
+                for (; q < q1; q++) {
+                    const int2 e = pr[q];
+                    a0 = fma(A[e.x], tab[e.y], a0);
+                }
+                acc[j] += (a0 + a1) + (a2 + a3);
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+        const int t = threadIdx.x + 128 * j;
+        if (t < K) mom[(int64_t)v * K + t] = acc[j];
     }
 }
 
@@ -221,6 +289,10 @@ template <int D>
 static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst) {
     const int K = T.K, p = T.order;
     const double sc = kSqrt2 * h;
+    // Nodes of more than one 256-point chunk take their moments from their
+    // children by H2H instead of from their points (C5, order 12: mom_partial
+    // 24 ms -> see DESIGN.md); FG_MOM_DIRECT=1 keeps the direct accumulation.
+    const int h2h = D <= kMaxDim && getenv("FG_MOM_DIRECT") == nullptr ? 1 : 0;
     FG_TRY(mom_items(t));
     struct MomPartial;
     DBuf &s_partial = scratch<MomPartial>();
@@ -252,13 +324,30 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     kern<<<grid, 32 * kMomWarps, smem, stream()>>>(t.mom_nitems, t.mom_items.as<int2>(),
                                                   t.node_i.as<int4>(), t.node_c.as<double>(),
                                                   t.pw.as<double>(), p, K, sc,
-                                                  T.digits.as<uint8_t>(), s_partial.as<double>());
+                                                  T.digits.as<uint8_t>(), s_partial.as<double>(),
+                                                  h2h);
     FG_CUDA_TRY(cudaGetLastError());
     const int64_t nn = t.nnodes;
     count_launch();
     mom_combine_kernel<<<(unsigned)nn, 256, 0, stream()>>>(
-        t.mom_off.as<int>(), s_partial.as<double>(), K, T.inv_fact.as<double>(), dst.as<double>());
+        t.mom_off.as<int>(), s_partial.as<double>(), K, T.inv_fact.as<double>(), dst.as<double>(),
+        h2h);
     FG_CUDA_TRY(cudaGetLastError());
+    if (h2h) {
+        // upward pass over the levels that hold nodes of more than one chunk
+        // (bottom-up: a node's children sit one level below it)
+        const size_t smem2 = sizeof(double) * K;
+        for (int L = t.levels - 2; L >= 0; L--) {
+            const int v0 = (int)t.level_begin[L], v1 = (int)t.level_begin[L + 1];
+            if (v1 <= v0) continue;
+            count_launch();
+            mom_h2h_level_kernel<D><<<(unsigned)(v1 - v0), 128, smem2, stream()>>>(
+                v0, v1, t.node_i.as<int4>(), t.node_c.as<double>(), p, K, sc,
+                T.digits.as<uint8_t>(), T.inv_fact.as<double>(), T.h2h_off.as<int>(),
+                T.h2h_ab.as<int2>(), dst.as<double>());
+        }
+        FG_CUDA_TRY(cudaGetLastError());
+    }
     return FG_OK;
 }
 

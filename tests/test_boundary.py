@@ -50,6 +50,17 @@ def test_public_names_mirror_reference():
     assert sorted(fg.__all__) == sorted(REFERENCE_ALL)
 
 
+def test_engine_order_cap_is_exported():
+    """fg_engine_plimit: the order cap sweeps use when RunConfig.plimit is None
+    (12 at D = 3, the reference's default_plimit elsewhere); no GPU needed."""
+    import paper_1206_6857_b200 as fg
+
+    assert fg.engine_plimit(3) == 12
+    for d in (1, 2, 4, 5, 6, 7, 8, 10, 16):
+        assert fg.engine_plimit(d) == fg.default_plimit(d)
+    assert "engine_plimit" not in fg.__all__  # the reference's name list is unchanged
+
+
 def test_host_side_validation_matches_reference():
     import paper_1206_6857_b200 as fg
 
