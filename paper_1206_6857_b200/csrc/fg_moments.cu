@@ -92,7 +92,7 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
         const int4 ni = node_i[item.x];
         // nodes of more than one chunk get their moments from their children
         // (mom_h2h_level_kernel) when small_only is set
-        if (small_only && ni.y > kMomChunk) continue;
+        if (small_only && ni.y > kMomChunk && ni.z >= 0) continue;  // (large leaves stay direct)
         double c[D];
 #pragma unroll
         for (int d = 0; d < D; d++) c[d] = node_c[(int64_t)item.x * D + d];
@@ -165,12 +165,14 @@ mom_partial_kernel(int nitems, const int2 *__restrict__ items, const int4 *__res
 // the 8 warp sums are added in warp order (deterministic).
 __global__ void __launch_bounds__(256)
 mom_combine_kernel(const int *__restrict__ off, const double *__restrict__ partial, int K,
-                   const double *__restrict__ inv_fact, double *__restrict__ mom, int small_only) {
+                   const double *__restrict__ inv_fact, double *__restrict__ mom, int small_only,
+                   const int4 *__restrict__ node_i) {
     __shared__ double sh[8][kMaxK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t v = blockIdx.x;
     const int i0 = off[v], i1 = off[v + 1];
-    if (small_only && i1 - i0 > 1) return;  // (more than one chunk: from the children)
+    // more than one chunk and children: from the children (mom_h2h_level_kernel)
+    if (small_only && i1 - i0 > 1 && node_i[v].z >= 0) return;
     if (i1 - i0 == 1) {  // single chunk: copy
         for (int k = threadIdx.x; k < K; k += 256)
             mom[v * K + k] = partial[(int64_t)i0 * K + k] * inv_fact[k];
@@ -331,7 +333,7 @@ static int moments_direct(TreeDev &t, const SeriesTables &T, double h, DBuf &dst
     count_launch();
     mom_combine_kernel<<<(unsigned)nn, 256, 0, stream()>>>(
         t.mom_off.as<int>(), s_partial.as<double>(), K, T.inv_fact.as<double>(), dst.as<double>(),
-        h2h);
+        h2h, t.node_i.as<int4>());
     FG_CUDA_TRY(cudaGetLastError());
     if (h2h) {
         // upward pass over the levels that hold nodes of more than one chunk

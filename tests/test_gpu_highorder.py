@@ -103,3 +103,24 @@ def test_tight_eps_uses_the_high_orders(fg, oracle):
         # the higher cap never evaluates more pairs exactly
         assert (r.counters.exact_pairs + r.counters.fp32_pairs
                 <= r6.counters.exact_pairs + r6.counters.fp32_pairs)
+
+
+@pytest.mark.parametrize("plimit", [6, 12])
+def test_moments_by_h2h_match_the_oracle(fg, oracle, plimit):
+    """Nodes of more than 256 points take their moments from their children
+    (H2H level pass), smaller ones and large LEAVES (identical points) from
+    their points: every node's moments against the oracle's (leaf moments +
+    H2H, spatial_index.py:171-197), in preorder like the reference."""
+    rng = np.random.default_rng(3)
+    pts = np.concatenate([rng.random((6000, 3)), np.tile([[0.31, 0.62, 0.17]], (700, 1)),
+                          0.8 + 0.01 * rng.standard_normal((3000, 3))])
+    w = rng.uniform(0.5, 1.5, len(pts))
+    tree = fg.build_tree(fg.PointStore(pts, w), 25)
+    ref = oracle.Tree(pts, w, 25)
+    for h in (0.07, 0.4):
+        tree.refresh_moments(h, plimit)
+        ref.refresh_moments(h, plimit)
+        m, r = tree.moments_array(), ref.moments()
+        assert m.shape == r.shape
+        scale = np.abs(r).max(axis=1, keepdims=True) + 1e-300
+        assert np.max(np.abs(m - r) / scale) <= 1e-10
