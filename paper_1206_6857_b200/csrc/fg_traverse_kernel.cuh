@@ -782,10 +782,16 @@ __device__ __forceinline__ double fp32_pair_bound(const TravArgs &A, const doubl
 constexpr int kPairDiff = 1 << 30;
 // One difference-form item (out of line: rare, and it keeps the dot-form
 // loop's register allocation intact).
+// (query offsets by value and sums returned by value: reference parameters of an
+// out-of-line function would pin the caller's copies to local memory)
 template <int D>
-__device__ __noinline__ void item_pairs_diff(const float (&xs)[kQPL][D], const float *pitem,
-                                             int np, const float *dli, unsigned long long nss,
-                                             double &sum0, double &sum1) {
+struct SlotOffsets {
+    float v[kQPL][D];
+};
+template <int D>
+__device__ __noinline__ double2 item_pairs_diff(SlotOffsets<D> xsv, const float *pitem, int np,
+                                                const float *dli, unsigned long long nss) {
+    const float (&xs)[kQPL][D] = xsv.v;
     constexpr int P = pstride<D>(), P2 = P / 2;
     unsigned long long xq[kQPL][D];
 #pragma unroll
@@ -826,10 +832,10 @@ __device__ __noinline__ void item_pairs_diff(const float (&xs)[kQPL][D], const f
                 if (u < nu) f2_fma_acc(acc[q][u], e, r[u][D + 1]);
             }
     }
-    sum0 += ((double)f2_lo(acc[0][0]) + (double)f2_hi(acc[0][0])) +
-            ((double)f2_lo(acc[0][1]) + (double)f2_hi(acc[0][1]));
-    sum1 += ((double)f2_lo(acc[1][0]) + (double)f2_hi(acc[1][0])) +
-            ((double)f2_lo(acc[1][1]) + (double)f2_hi(acc[1][1]));
+    return make_double2(((double)f2_lo(acc[0][0]) + (double)f2_hi(acc[0][0])) +
+                            ((double)f2_lo(acc[0][1]) + (double)f2_hi(acc[0][1])),
+                        ((double)f2_lo(acc[1][0]) + (double)f2_hi(acc[1][0])) +
+                            ((double)f2_lo(acc[1][1]) + (double)f2_hi(acc[1][1])));
 }
 
 template <int D>
@@ -843,7 +849,14 @@ __device__ __forceinline__ void batch_pairs(const float (&xs)[kQPL][D], const fl
     for (int it = 0; it < nitems; it++) {
         const int off = ioff[it], np = icnt[it] & (kPairDiff - 1);
         if (icnt[it] & kPairDiff) {
-            item_pairs_diff<D>(xs, pbuf + off * P, np, idl + it * FD, nss, sum0, sum1);
+            SlotOffsets<D> xsv;
+#pragma unroll
+            for (int q = 0; q < kQPL; q++)
+#pragma unroll
+                for (int d = 0; d < D; d++) xsv.v[q][d] = xs[q][d];
+            const double2 r = item_pairs_diff<D>(xsv, pbuf + off * P, np, idl + it * FD, nss);
+            sum0 += r.x;
+            sum1 += r.y;
             continue;
         }
         unsigned long long xx[kQPL][D], aa[kQPL];
@@ -1965,8 +1978,11 @@ traverse_kernel(const TravArgs A) {
                     __pipeline_commit();
                 }
             }
+            int p_next = nh > 0 ? sl[0].y & 0xff : 0;
             for (int i = 0; i < nh; i++) {
-                const int p = sl[i].y & 0xff;
+                const int p = p_next;
+                // (the next entry's order is loaded one evaluation ahead)
+                if (i + 1 < nh) p_next = sl[i + 1].y & 0xff;
                 c_ht += (unsigned long long)A.kp[p] * qn;
                 if (ring) {
                     if (i + kRing - 1 < nh) stage_item(i + kRing - 1);
