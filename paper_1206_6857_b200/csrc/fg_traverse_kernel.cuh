@@ -1962,9 +1962,17 @@ traverse_kernel(const TravArgs A) {
                 const double *mom = H.r_mom + (int64_t)node * A.mom_K;
                 if constexpr (D == 3) {
                     const unsigned short *perm = s_nest + c_nest3.off[po];
-                    for (int q = lane; q < kc; q += 32) {
-                        FG_CHECK(po >= 1 && po <= PF && perm[q] < coff && kc <= A.mom_K);
-                        __pipeline_memcpy_async(dst + perm[q], mom + q, 8);
+                    // four positions per round: the permutation loads overlap
+                    for (int q = lane; q < kc; q += 128) {
+                        int pos[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) pos[u] = q + 32 * u < kc ? perm[q + 32 * u] : -1;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            FG_CHECK(po >= 1 && po <= PF && pos[u] < coff && kc <= A.mom_K);
+                            if (pos[u] >= 0)
+                                __pipeline_memcpy_async(dst + pos[u], mom + q + 32 * u, 8);
+                        }
                     }
                 } else {
                     for (int q = lane; q < kc; q += 32) __pipeline_memcpy_async(dst + q, mom + q, 8);
