@@ -1063,7 +1063,25 @@ int run_sweep(TreeDev &q, TreeDev &r, const double *hs, int nh, double eps, int 
     const int D = q.dim;
     // the engine's own order cap unless the caller fixes one (padded
     // dimensions: the caller's dimension decides, as for the bounds)
-    if (plimit <= 0) plimit = engine_plimit(q.dim_user > 0 ? q.dim_user : D);
+    if (plimit <= 0) {
+        const int du = q.dim_user > 0 ? q.dim_user : D;
+        plimit = engine_plimit(du);
+        // The engine's own cap must not outgrow the device: a chunk of the sweep
+        // keeps one moment set per bandwidth (nodes x K doubles each, plus the
+        // base set and the partial sums).  Fall back towards the reference's
+        // cap while they would take more than 40 % of the free memory.
+        if (mode == FG_DITO) {
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+                const double sets = (double)std::min(nh, kMaxSweep) + 3.0;
+                while (plimit > default_plimit(du) &&
+                       sets * (double)r.nnodes * iset_count(du, plimit) * 8.0 > 0.4 * (double)fr)
+                    plimit--;
+            } else {
+                cudaGetLastError();
+            }
+        }
+    }
     FG_REQUIRE(nh >= 1, FG_EINVAL, "need at least one bandwidth");
     for (int j = 0; j < nh; j++) FG_REQUIRE(hs[j] > 0.0, FG_EINVAL, "bandwidth must be positive");
     const bool series = mode == FG_DITO;

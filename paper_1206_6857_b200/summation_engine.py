@@ -266,8 +266,10 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
     hs = np.ascontiguousarray(np.atleast_1d(np.asarray(bandwidths, dtype=float)))
     if hs.size == 0 or np.any(hs <= 0.0):
         raise ValueError("bandwidths must be positive")
-    # the engine's own order cap unless the caller fixes one (any order keeps eps)
-    plimit = config.plimit if config.plimit is not None else engine_plimit(qtree.dim)
+    # the engine's own order cap unless the caller fixes one (any order keeps
+    # eps): 0 lets the engine apply engine_plimit(dim), lowered if the moment
+    # sets of that order would not fit the device's memory
+    plimit = config.plimit if config.plimit is not None else 0
     nh = hs.shape[0]
     shapes = [(nh, qtree.n)] + ([(qtree.n,)] if nh == 1 else [])
     vals = _lib.check_out(out, shapes) if out is not None else (
@@ -285,7 +287,12 @@ def sweep_run(config: RunConfig, qtree: KdTree, rtree: KdTree, bandwidths,
                       float(config.epsilon), _lib.MODES[config.algorithm], int(plimit),
                       int(b0), int(b1), int(stride), _lib.ptr(vals), cnt, _lib.ptr(secs))
     if config.algorithm == "dito":
-        rtree._moments_refreshed(float(hs[-1]), plimit)
+        # the order the engine left the moments at (its own cap may have been
+        # lowered to fit the device's memory)
+        order = ctypes.c_int32(0)
+        _lib.call("fg_moments_export", rtree.handle, None, None, None, ctypes.byref(order))
+        rtree._moments_refreshed(float(hs[-1]),
+                                 int(order.value) or int(plimit) or engine_plimit(qtree.dim))
     rows = vals.reshape(nh, qtree.n)
     return [ResultVector(rows[j], float(secs[j]), TraversalCounters._from_c(cnt[j]), None)
             for j in range(nh)]
