@@ -199,6 +199,9 @@ __host__ __device__ constexpr int nest3_slot(int plimit) { return plimit <= 10 ?
 // block_m.  Sum_b S_b H_b(t1) is folded by Clenshaw's recurrence
 // y_b = S_b + 2 t1 y_{b+1} - 2 (b + 1) y_{b+2} (result y_0): two FMAs per row
 // and slot and no middle ladder; H_a(t0) is advanced once per group.
+#ifndef FG_ROWS123
+#define FG_ROWS123 1
+#endif
 constexpr int kRowPairs = (kMaxOrder + 1) / 2;  // 16-byte pairs of the longest row
 // 16-byte shared-memory load that stays where it is written (the compiler sinks
 // an ordinary load down to its first use, which undoes the row prefetch)
@@ -282,6 +285,41 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
         double y1a = 0.0, y2a = 0.0, y1b = 0.0, y2b = 0.0;
         double twob = 2.0 * m;  // 2 (b + 1) of the row being folded
         double2 pre0[kRowPairs], pre1[kRowPairs];  // rows of odd / even length
+#if FG_ROWS123
+        if (m >= 3 && PMAX >= 4) {
+            // rows 1, 2, 3 of the group (6 coefficients in 4 pairs) in one block:
+            // one branch instead of three, their sums independent
+            const double2 r1 = lds_pair(gs), r2 = lds_pair(gs + 16), r3 = lds_pair(gs + 32),
+                          r3b = lds_pair(gs + 48);
+            pre1[0] = lds_pair(gs + 64);  // row 4, should the group have one
+            pre1[1] = lds_pair(gs + 80);
+            const double s2a = fma(r2.y, l2a[1], r2.x), s2b = fma(r2.y, l2b[1], r2.x);
+            const double s3a = fma(r3b.x, l2a[2], fma(r3.y, l2a[1], r3.x));
+            const double s3b = fma(r3b.x, l2b[2], fma(r3.y, l2b[1], r3.x));
+            // Clenshaw: y(row 1) = S1; y(row 2) = S2 + t1 S1; y(row 3) = S3 + t1 y(row 2) - (2m - 4) S1
+            const double ya = fma(t1a, r1.x, s2a), yb = fma(t1b, r1.x, s2b);
+            const double c3 = 4.0 - twob;
+            y1a = fma(t1a, ya, fma(c3, r1.x, s3a));
+            y1b = fma(t1b, yb, fma(c3, r1.x, s3b));
+            y2a = ya;
+            y2b = yb;
+            twob -= 6.0;
+            if (m > 3) {
+                do {
+#define FG_ROWC(N)                                                                  \
+    if constexpr (N <= PMAX) {                                                      \
+        far3_row_cl<N, PMAX>(gs, l2a, l2b, t1a, t1b, twob, y1a, y2a, y1b, y2b,       \
+                             (N & 1) ? pre0 : pre1, (N & 1) ? pre1 : pre0);          \
+        if (m == N) break;                                                          \
+    }
+                    FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7) FG_ROWC(8) FG_ROWC(9)
+                    FG_ROWC(10) FG_ROWC(11) FG_ROWC(12)
+#undef FG_ROWC
+                } while (0);
+            }
+        } else
+#endif
+        {
         pre0[0] = lds_pair(gs);
         do {
 #define FG_ROWC(N)                                                                  \
@@ -290,10 +328,15 @@ __device__ __forceinline__ void far3_rows_cl(int p, const double (&ta)[3], const
                              (N & 1) ? pre0 : pre1, (N & 1) ? pre1 : pre0);          \
         if (m == N) break;                                                          \
     }
+#if FG_ROWS123
+            FG_ROWC(1) FG_ROWC(2)
+#else
             FG_ROWC(1) FG_ROWC(2) FG_ROWC(3) FG_ROWC(4) FG_ROWC(5) FG_ROWC(6) FG_ROWC(7)
             FG_ROWC(8) FG_ROWC(9) FG_ROWC(10) FG_ROWC(11) FG_ROWC(12)
+#endif
 #undef FG_ROWC
         } while (0);
+        }
         gs += ((m + 1) >> 1) * (((m + 1) >> 1) + ((m & 1) ? 0 : 1)) * 16;  // G(m) doubles
         acca = fma(y1a, ha, acca);
         accb = fma(y1b, hb, accb);
